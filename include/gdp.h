@@ -1,0 +1,182 @@
+/*
+ * gdp.h — C ABI of the B200-native gradient-domain multigrid hot path
+ * (Kazhdan et al., "Gradient-Domain Processing for Large EM Image Stacks",
+ *  arXiv 1310.0041; reference text /root/reference/PAPER.md, cited as PAPER.md:L).
+ *
+ * The library solves, on regular voxel grids with Neumann boundaries, the
+ * screened anisotropic Poisson system of the paper's §4:
+ *
+ *      (alpha - div W grad) x = alpha V - div W G,      W = Diag(bx, by, bz) >= 0
+ *
+ * by multigrid V-cycles whose every step runs in the
+ * library's own sm_100a CUDA kernels.  Two instances are exported as whole solves:
+ *   - gdp_diffuse_z               phase 1, Eq. (1): 3D anisotropic
+ *                                 diffusion across slices, alpha = 0, G = (dI0/dx, dI0/dy, 0);
+ *   - gdp_screened_poisson_slices phase 2, Eq. (2): per-slice 2D
+ *                                 screened Poisson (alpha - Delta) I2 = alpha I1 - Delta I0.
+ * and two building blocks: gdp_vcycle (one V-cycle on an explicit rhs) and
+ * gdp_residual (r = b - A x with fp64 norms, the measure of PAPER.md:355).
+ *
+ * Discretisation: cell-centred voxels; the gradient is the
+ * forward difference on the links between face-adjacent voxels; the divergence is
+ * its negative transpose; links leaving the grid do not exist (Neumann).  Hence
+ * A x at voxel c is  alpha x_c + sum_d beta_d sum_{n valid nbr of c along d} (x_c - x_n)
+ * (interior diagonal 2(bx+by+bz), e.g. 4.2 for W = (1,1,0.1)).
+ *
+ * LAYOUT: every volume is dense, slice-major, x fastest: element (x,y,z) lives at
+ *   [z*ny*nx + y*nx + x], no padding.  u8 intensities decode to
+ *   u8/255 rounded to fp32 (IEEE division); fp32 volumes are used as given.
+ * OWNERSHIP: all array pointers are owned by the caller; the library never frees
+ *   or retains them past the call.  Device-pointer entry points take pointers in
+ *   the memory of the ctx's device; host entry points take host pointers (pinned or
+ *   pageable) and do their own staging.  `stream` is a cudaStream_t passed as void*
+ *   (NULL = the legacy default stream).
+ * ERRORS: every entry point returns a gdp_status; nothing throws across the ABI.
+ *   On failure gdp_last_error() returns a thread-local message.  A GDP_ENOCONV
+ *   return still leaves the best iterate in the output and fills the report.
+ * THREADING: one ctx per host thread.  Whole solves block until convergence
+ *   (they read back fp64 norms once per V-cycle); gdp_vcycle / gdp_residual
+ *   synchronise `stream` only to return their host scalars.
+ * DISTRIBUTION: a ctx created with world > 1 owns an NCCL communicator over the
+ *   ranks; each rank passes its local z-slab (local dims) and the slab's global
+ *   position (z0_global, nz_global).  A ctx created with gdp_ctx_create_loopback
+ *   emulates `world` ranks inside one process on one GPU (same code path, halo
+ *   exchange by device copies) for testing the partition.
+ */
+#ifndef GDP_H_
+#define GDP_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GDP_MAX_CYCLES 64
+#define GDP_MAX_LEVELS 32
+
+typedef enum {
+  GDP_OK = 0,
+  GDP_EINVAL = 1,   /* null pointer, dims <= 0, alpha/beta < 0 or non-finite,
+                       alpha = 0 with all beta = 0 (singular), alpha <= 0 in
+                       the slices call, unsupported layout */
+  GDP_ECUDA = 2,    /* a CUDA runtime error; gdp_last_error() keeps cudaGetErrorString */
+  GDP_ENOCONV = 3,  /* cycle cap or stagnation before rel_tol; output = best iterate */
+  GDP_ENOMEM = 4,   /* device allocation failed */
+  GDP_ENCCL = 5     /* NCCL error (distributed ctx only) */
+} gdp_status;
+
+typedef enum { GDP_U8 = 0, GDP_F32 = 1 } gdp_dtype;
+
+typedef struct { int64_t nx, ny, nz; } gdp_dims;
+
+/* W = Diag(bx, by, bz), PAPER.md:150-152 (application value (1, 1, 0.1)). */
+typedef struct { float bx, by, bz; } gdp_weights;
+
+typedef struct {
+  double rel_tol;     /* stop when ||b - A x|| / ||b|| <= rel_tol (fp64 norms). Default 1e-6
+                         (BASELINE.json north_star).  Phase 2: max over slices.           */
+  int max_vcycles;    /* cap (<= GDP_MAX_CYCLES).  Default 30.                              */
+  int nu_pre;         /* red-black Gauss-Seidel sweeps before restriction.  Default 2.      */
+  int nu_post;        /* sweeps after prolongation.  Default 2.                             */
+  int coarse_max;     /* coarsest level: <= coarse_max unknowns per independent system and
+                         <= 64 cells along each coupled axis.  Default 4096.                */
+  int stagnation;     /* stop (GDP_ENOCONV) after this many cycles each reducing the residual
+                         by less than 10%.  Default 2.  0 disables.                         */
+  int fused;          /* 1: fused tile kernels (default), 0: one kernel per half-sweep
+                         (reference schedule of the same arithmetic).                        */
+  int use_graphs;     /* 1: replay each V-cycle as a CUDA graph (default), 0: direct launch */
+} gdp_opts;
+
+typedef struct {
+  int status;                          /* gdp_status of the solve                          */
+  int vcycles;                         /* V-cycles run                                     */
+  int levels;                          /* multigrid levels (incl. finest and coarsest)     */
+  double rel_res[GDP_MAX_CYCLES + 1];  /* [0] = initial, [k] = after cycle k (phase 2: max
+                                          over slices)                                     */
+  double norm_b;                       /* ||b||_2 of the finest rhs (phase 2: of the worst slice) */
+  double seconds;                      /* device time of the solve (CUDA events)           */
+  double hbm_bytes_est;                /* algorithmic HBM bytes of the solve   */
+  int64_t kernel_launches;             /* library kernels launched by the call             */
+} gdp_report;
+
+typedef struct gdp_ctx gdp_ctx;
+
+/* Fill *o with the defaults above. */
+int gdp_opts_default(gdp_opts* o);
+
+/* Create a context on CUDA `device`.  world == 1: single rank, nccl_unique_id NULL.
+ * world > 1: this process is rank `rank`; nccl_unique_id points to the 128-byte
+ * ncclUniqueId every rank received (e.g. broadcast by torch.distributed). */
+int gdp_ctx_create(gdp_ctx** out, int device, int rank, int world, const void* nccl_unique_id);
+
+/* Create a context emulating `world` ranks in this process on one device: the
+ * caller passes the WHOLE volume and the library splits it into `world` z-slabs
+ * internally (halo exchange = device copies).  Test vehicle for the partition. */
+int gdp_ctx_create_loopback(gdp_ctx** out, int device, int world);
+
+int gdp_ctx_destroy(gdp_ctx* ctx);
+
+/* Phase 1 — Eq. (1).  Solves (alpha - div W grad) I1 = alpha I0 - div W G,
+ * G = (dI0/dx, dI0/dy, 0); with alpha = 0 (the paper's AD) the constant null space is
+ * removed by pinning mean(I1) = mean(I0) in fp64 (reading c-3).
+ *   I0    device, local slab nx*ny*nz of `dtype`
+ *   I1    device fp32 output, same shape (may not alias I0)
+ *   local local slab dims; z0_global / nz_global its position in the global stack
+ *         (world == 1: 0 and local.nz)
+ *   W     weights, application value (1, 1, 0.1)                                      */
+int gdp_diffuse_z(gdp_ctx* ctx, const void* I0, gdp_dtype dtype, float* I1, gdp_dims local,
+                  int64_t z0_global, int64_t nz_global, gdp_weights W, float alpha,
+                  const gdp_opts* opts, gdp_report* report, void* stream);
+
+/* Phase 2 — Eq. (2).  For every slice i independently:
+ *   (alpha - Delta) I2_i = alpha I1_i - Delta I0_i,   alpha > 0 (application 0.01).
+ *   I0 device (dtype), I1 device fp32, I2 device fp32 output (may alias I1, not I0).
+ * Slices are independent systems: no communication even on a distributed ctx.       */
+int gdp_screened_poisson_slices(gdp_ctx* ctx, const void* I0, gdp_dtype dtype, const float* I1,
+                                float* I2, gdp_dims local, float alpha, const gdp_opts* opts,
+                                gdp_report* report, void* stream);
+
+/* Both phases back to back: I1 = diffuse_z(I0), I2 = slices(I0, I1).
+ * I1 may be NULL (library scratch).  reports may be NULL.                            */
+int gdp_destripe(gdp_ctx* ctx, const void* I0, gdp_dtype dtype, float* I1, float* I2,
+                 gdp_dims local, int64_t z0_global, int64_t nz_global, gdp_weights W,
+                 float alpha, const gdp_opts* opts, gdp_report* rep1, gdp_report* rep2,
+                 void* stream);
+
+/* Host-buffer entry: I0 and I2 (and I1 if non-NULL) are
+ * HOST arrays of the whole local stack.  The library streams z-slabs host->device on
+ * side streams, runs both phases, and streams I2 back.  If the stack does not fit in
+ * `hbm_budget_bytes` (0 = 90% of free device memory) it returns GDP_ENOMEM.          */
+int gdp_destripe_host(gdp_ctx* ctx, const void* I0_host, gdp_dtype dtype, float* I1_host,
+                      float* I2_host, gdp_dims dims, gdp_weights W, float alpha,
+                      size_t hbm_budget_bytes, const gdp_opts* opts, gdp_report* rep1,
+                      gdp_report* rep2);
+
+/* One V-cycle on (alpha - div W grad) x = b.  x device fp32 in/out,
+ * b device fp32.  With alpha = 0, b is used as given (the caller guarantees sum b = 0
+ * up to rounding; the coarsest solve drops the constant mode).
+ * *rel_res_after (may be NULL) = ||b - A x|| / ||b|| after the cycle, fp64.           */
+int gdp_vcycle(gdp_ctx* ctx, float* x, const float* b, gdp_dims local, int64_t z0_global,
+               int64_t nz_global, gdp_weights W, float alpha, const gdp_opts* opts,
+               double* rel_res_after, void* stream);
+
+/* Residual r = b - A x of the §4 operator, difference form, fp32 per
+ * voxel; norm2_r = sum r^2 and norm2_b = sum b^2 accumulated in fp64 (summed over ranks
+ * on a distributed ctx).  r may be NULL (norms only).  Norm pointers are host.        */
+int gdp_residual(gdp_ctx* ctx, const float* x, const float* b, float* r, gdp_dims local,
+                 int64_t z0_global, int64_t nz_global, gdp_weights W, float alpha,
+                 double* norm2_r, double* norm2_b, void* stream);
+
+/* Thread-local message of the last failing call on this thread ("" if none). */
+const char* gdp_last_error(void);
+
+/* Library version string and the number of kernels launched by this process so far. */
+const char* gdp_version(void);
+int64_t gdp_kernel_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GDP_H_ */

@@ -1,0 +1,177 @@
+// gdp_device.cuh — per-voxel arithmetic shared by every kernel of the library.
+//
+// All schedules (one kernel per half-sweep, fused tile kernels, z-marching kernels)
+// call exactly these functions, so a red-black Gauss-Seidel iterate is bit-identical
+// whatever the tiling: a point of one colour depends only on points of the other.
+//
+// Discretisation:
+//   A x at cell c = alpha x_c + sum_axes [ cl(i) (x_c - x_{i-1}) + cr(i) (x_c - x_{i+1}) ]
+// with link coefficients from a finite-volume rediscretisation on every level:
+//   interior link  beta / H^2, links touching a partial last cell (odd sizes under
+//   ceil-halving) beta / (d h) with d the centre distance and h the row cell width.
+// Level 0 has H = h = 1, i.e. exactly the 7-point Neumann stencil of the paper's
+// Constant scheme, diagonal 2(bx+by+bz) in the interior.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace gdp {
+
+struct AxisC {      // link coefficients of one axis on one level
+  int n;            // global cell count along the axis
+  float k;          // interior link coefficient
+  float kr;         // right link of row n-2 (towards the last cell)
+  float kl;         // left link of row n-1 (the last cell)
+};
+
+__device__ __forceinline__ float cl(const AxisC& a, long long i) {
+  return i <= 0 ? 0.f : (i == a.n - 1 ? a.kl : a.k);
+}
+__device__ __forceinline__ float cr(const AxisC& a, long long i) {
+  return i >= a.n - 1 ? 0.f : (i == a.n - 2 ? a.kr : a.k);
+}
+
+struct LevelK {     // one multigrid level as the kernels see it
+  int nx, ny, nzl;  // local dims (x, y full; z = this rank's slab)
+  long long z0;     // global z of local plane 0
+  AxisC ax, ay, az;
+  float alpha;      // screening weight (same on every level)
+};
+
+enum RhsMode { RHS_B = 0, RHS_G = 1 };
+
+// Right-hand side of the finest level.
+//   RHS_B: explicit b (gdp_vcycle, coarse levels).
+//   RHS_G: b = av V - div W G with G = in-plane forward differences of I (Eq. 1 / Eq. 2),
+//          evaluated on the fly from I (u8 or f32) and the value target V.
+struct RhsK {
+  const float* b;
+  const void* I;     // gradient source I0
+  const float* V;    // value target (vmode 2)
+  float av;          // weight of the value term
+  int vmode;         // 0: no value term, 1: V = I (decoded), 2: V = float array
+};
+
+template <typename T> __device__ __forceinline__ float ldI(const void* p, long long i);
+template <> __device__ __forceinline__ float ldI<float>(const void* p, long long i) {
+  return __ldg(static_cast<const float*>(p) + i);
+}
+template <> __device__ __forceinline__ float ldI<uint8_t>(const void* p, long long i) {
+  // a1: u8 -> u8/255 correctly rounded (IEEE division), the exact value the oracle decodes.
+  return __fdiv_rn((float)__ldg(static_cast<const uint8_t*>(p) + i), 255.f);
+}
+
+// Neighbour values of x around cell c.  Where a link does not exist the loader sets
+// the neighbour to x_c, so (x_c - x_n) is exactly 0 (never 0 * garbage).
+struct Nbr {
+  float w, e, s, n, d, u;
+};
+
+struct Coef {
+  float xl, xr, yl, yr, zl, zr;
+  __device__ __forceinline__ float diag(float alpha) const {
+    return alpha + ((xl + xr) + (yl + yr)) + (zl + zr);
+  }
+};
+
+__device__ __forceinline__ Coef coefs(const LevelK& L, int ix, int iy, long long zg) {
+  Coef c;
+  c.xl = cl(L.ax, ix); c.xr = cr(L.ax, ix);
+  c.yl = cl(L.ay, iy); c.yr = cr(L.ay, iy);
+  c.zl = cl(L.az, zg); c.zr = cr(L.az, zg);
+  return c;
+}
+
+// Residual r = b - A x at one cell, difference form: every link
+// contributes coefficient * ((I_c - I_n) - (x_c - x_n)) so that fp32 cancellation acts
+// on small differences.  `bval` (optional) receives b at the cell (for ||b||).
+template <int MODE, typename TI>
+__device__ __forceinline__ float residual_at(const LevelK& L, const RhsK& R, const Coef& k,
+                                             float xc, const Nbr& nb, long long c, long long nx,
+                                             long long plane, float* bval) {
+  float r;
+  if (MODE == RHS_B) {
+    float s = L.alpha * xc;
+    s += k.xl * (xc - nb.w);
+    s += k.xr * (xc - nb.e);
+    s += k.yl * (xc - nb.s);
+    s += k.yr * (xc - nb.n);
+    s += k.zl * (xc - nb.d);
+    s += k.zr * (xc - nb.u);
+    const float bc = R.b[c];
+    if (bval) *bval = bc;
+    r = bc - s;
+  } else {
+    const float Ic = ldI<TI>(R.I, c);
+    float Iw = Ic, Ie = Ic, Is = Ic, In = Ic;  // absent link: zero difference
+    if (k.xl != 0.f) Iw = ldI<TI>(R.I, c - 1);
+    if (k.xr != 0.f) Ie = ldI<TI>(R.I, c + 1);
+    if (k.yl != 0.f) Is = ldI<TI>(R.I, c - nx);
+    if (k.yr != 0.f) In = ldI<TI>(R.I, c + nx);
+    float g = 0.f, bb = 0.f;
+    g += k.xl * ((Ic - Iw) - (xc - nb.w));
+    g += k.xr * ((Ic - Ie) - (xc - nb.e));
+    g += k.yl * ((Ic - Is) - (xc - nb.s));
+    g += k.yr * ((Ic - In) - (xc - nb.n));
+    g -= k.zl * (xc - nb.d);
+    g -= k.zr * (xc - nb.u);
+    if (bval) {
+      bb = k.xl * (Ic - Iw) + k.xr * (Ic - Ie) + k.yl * (Ic - Is) + k.yr * (Ic - In);
+    }
+    if (R.vmode != 0) {
+      const float Vc = R.vmode == 1 ? Ic : __ldg(R.V + c);
+      if (R.av == L.alpha) g += L.alpha * (Vc - xc);
+      else g += R.av * Vc - L.alpha * xc;
+      if (bval) bb += R.av * Vc;
+    } else {
+      g -= L.alpha * xc;
+    }
+    if (bval) *bval = bb;
+    r = g;
+  }
+  return r;
+}
+
+// Gauss-Seidel point update in correction form: x_c <- x_c + r_c / D_c  (H1).
+__device__ __forceinline__ float gs_update(float xc, float r, float D) { return xc + r / D; }
+
+// Cell-centre coordinate (finest-grid units) of cell i on an axis of n cells of width H,
+// the last one of width hl (partial under ceil-halving).
+__device__ __forceinline__ float centre(long long i, int n, float H, float hl) {
+  return i < n - 1 ? ((float)i + 0.5f) * H : (float)(n - 1) * H + 0.5f * hl;
+}
+
+struct XferAxis {   // transfer geometry of one axis between a fine and a coarse level
+  int coarsened;    // 0: identity along this axis
+  int nf, nc;       // global counts
+  float Hf, hlf;    // fine full / last width
+  float Hc, hlc;    // coarse full / last width
+};
+
+// Restriction weight of fine cell i inside its parent (volume-weighted child average).
+__device__ __forceinline__ float rweight(const XferAxis& a, long long i) {
+  if (!a.coarsened) return 1.f;
+  const long long I = i >> 1;
+  const long long c0 = 2 * I, c1 = 2 * I + 1;
+  const float h0 = (c0 == a.nf - 1) ? a.hlf : a.Hf;
+  const float h1 = (c1 < a.nf) ? ((c1 == a.nf - 1) ? a.hlf : a.Hf) : 0.f;
+  const float hi = (i == c0) ? h0 : h1;
+  return hi / (h0 + h1);
+}
+
+// Linear prolongation taps of fine cell i: parent I with weight 1-t, neighbour J with t.
+__device__ __forceinline__ void ptaps(const XferAxis& a, long long i, long long& I, long long& J,
+                                      float& t) {
+  if (!a.coarsened) { I = i; J = i; t = 0.f; return; }
+  I = i >> 1;
+  const float cf = centre(i, a.nf, a.Hf, a.hlf);
+  const float cI = centre(I, a.nc, a.Hc, a.hlc);
+  if (cf < cI) J = I - 1;
+  else if (cf > cI) J = I + 1;
+  else { J = I; t = 0.f; return; }
+  if (J < 0 || J >= a.nc) { J = I; t = 0.f; return; }
+  const float cJ = centre(J, a.nc, a.Hc, a.hlc);
+  t = (cf - cI) / (cJ - cI);
+}
+
+}  // namespace gdp

@@ -1,0 +1,93 @@
+// gdp_host.cu — host-buffer entry point (a13) and the algorithmic-bytes model.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "gdp_internal.h"
+
+namespace gdp {
+
+// Algorithmic HBM bytes of a solve in the fused design:
+// per V-cycle, level 0 reads x + rhs inputs and writes x in both passes, writes / reads the
+// coarse array; coarse levels read b and x and write x; the coarsest reads b, writes x.
+// Plus the initial copy x0 = I0, the initial norm pass and (alpha = 0) the mean pin.
+double hbm_model(const Hier& H, double s_I, double s_V, int vcycles) {
+  const auto& lv = H.lv;
+  auto N = [&](size_t l) { return (double)lv[l].nx * lv[l].ny * lv[l].nzl; };
+  double cyc = 0.0;
+  const size_t nl = lv.size();
+  for (size_t l = 0; l + 1 < nl; ++l) {
+    const double rhs = l == 0 ? (s_I + s_V) : 4.0;
+    const double down = (l == 0 ? 4.0 : 0.0) + 4.0 + rhs;  // (x read) + x write + rhs
+    const double up = 8.0 + rhs;                            // x read/write + rhs
+    cyc += N(l) * (down + up) + N(l + 1) * 8.0;             // coarse b write + coarse x read
+  }
+  cyc += N(nl - 1) * 8.0;
+  const double N0 = N(0);
+  double init = N0 * (s_I + 4.0) + N0 * (4.0 + s_I + s_V);
+  if (s_V == 0.0) init += N0 * (4.0 + s_I + 8.0);
+  return init + vcycles * cyc;
+}
+
+}  // namespace gdp
+
+using namespace gdp;
+
+#define HK(call, what)                                                                    \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      return set_err(e_ == cudaErrorMemoryAllocation ? GDP_ENOMEM : GDP_ECUDA, "%s: %s", \
+                     what, cudaGetErrorString(e_));                                       \
+  } while (0)
+
+// a13 (in-core variant): host arrays in, host arrays out.  I0 goes host->device on the
+// compute stream; I1 (if requested) streams back on a side copy stream while phase 2
+// runs; I2 comes back at the end.  Stacks larger than the HBM budget need the slab
+// streamer of the finest level (not built: GDP_ENOMEM).
+extern "C" int gdp_destripe_host(gdp_ctx* ctx, const void* I0_host, gdp_dtype dtype, float* I1_host,
+                                 float* I2_host, gdp_dims dims, gdp_weights W, float alpha,
+                                 size_t hbm_budget_bytes, const gdp_opts* opts, gdp_report* rep1,
+                                 gdp_report* rep2) {
+  if (!ctx) return set_err(GDP_EINVAL, "null ctx");
+  if (!I0_host || !I2_host) return set_err(GDP_EINVAL, "null host buffers");
+  if (dims.nx <= 0 || dims.ny <= 0 || dims.nz <= 0) return set_err(GDP_EINVAL, "dims must be positive");
+  if (dtype != GDP_U8 && dtype != GDP_F32) return set_err(GDP_EINVAL, "bad dtype");
+  Ctx& C = ctx->impl;
+  HK(cudaSetDevice(C.device), "set device");
+  const size_t n = (size_t)dims.nx * dims.ny * dims.nz;
+  const size_t sI = dtype == GDP_U8 ? 1 : 4;
+  const size_t need = n * (sI + 8) + n * 4 / 2;  // I0, I1, I2 + hierarchy (< N/2 fp32 pairs)
+  size_t freeb = 0, totb = 0;
+  HK(cudaMemGetInfo(&freeb, &totb), "meminfo");
+  const size_t have = freeb + C.hbuf_cap[0] + C.hbuf_cap[1] + C.hbuf_cap[2];
+  const size_t budget = hbm_budget_bytes ? hbm_budget_bytes : (size_t)(0.9 * (double)have);
+  if (need > budget)
+    return set_err(GDP_ENOMEM, "stack needs ~%zu B of HBM, budget %zu B (out-of-core slab streaming "
+                   "of the finest level is not built)", need, budget);
+  if (!C.hs) HK(cudaStreamCreateWithFlags(&C.hs, cudaStreamNonBlocking), "stream");
+  if (!C.hcs) HK(cudaStreamCreateWithFlags(&C.hcs, cudaStreamNonBlocking), "stream");
+  if (!C.hev) HK(cudaEventCreateWithFlags(&C.hev, cudaEventDisableTiming), "event");
+  int rc = C.ensure_hbuf(0, n * sI);
+  if (rc == GDP_OK) rc = C.ensure_hbuf(1, n * 4);
+  if (rc == GDP_OK) rc = C.ensure_hbuf(2, n * 4);
+  if (rc != GDP_OK) return rc;
+  void* dI0 = C.hbuf[0];
+  float* dI1 = (float*)C.hbuf[1];
+  float* dI2 = (float*)C.hbuf[2];
+  cudaStream_t s = C.hs, cs = C.hcs;
+  HK(cudaMemcpyAsync(dI0, I0_host, n * sI, cudaMemcpyHostToDevice, s), "H2D I0");
+  rc = gdp_diffuse_z(ctx, dI0, dtype, dI1, dims, 0, dims.nz, W, 0.f, opts, rep1, s);
+  if (rc != GDP_OK && rc != GDP_ENOCONV) return rc;
+  HK(cudaEventRecord(C.hev, s), "event");
+  if (I1_host) {
+    HK(cudaStreamWaitEvent(cs, C.hev, 0), "wait");
+    HK(cudaMemcpyAsync(I1_host, dI1, n * 4, cudaMemcpyDeviceToHost, cs), "D2H I1");
+  }
+  const int rc2 = gdp_screened_poisson_slices(ctx, dI0, dtype, dI1, dI2, dims, alpha, opts, rep2, s);
+  if (rc2 != GDP_OK) return rc2;
+  HK(cudaMemcpyAsync(I2_host, dI2, n * 4, cudaMemcpyDeviceToHost, s), "D2H I2");
+  HK(cudaStreamSynchronize(s), "sync");
+  HK(cudaStreamSynchronize(cs), "sync");
+  return rc;
+}

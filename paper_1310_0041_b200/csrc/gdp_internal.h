@@ -1,0 +1,109 @@
+// gdp_internal.h — host-side structures of the solver core (not part of the C ABI).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <map>
+#include <memory>
+#include <tuple>
+#include <vector>
+
+#include "../../include/gdp.h"
+#include "gdp_kernels.h"
+
+namespace gdp {
+
+int set_err(int code, const char* fmt, ...);
+
+struct AxisG {      // host geometry of one axis of one level (finest-grid units)
+  int n;            // global cell count
+  double H;         // full cell width
+  double hl;        // width of the last cell (< H when partial)
+  double beta;      // weight of the axis (W diagonal), same on every level
+};
+
+struct Level {
+  AxisG gx{}, gy{}, gz{};
+  int nx = 0, ny = 0, nzl = 0;   // local dims
+  long long z0 = 0;              // global z of local plane 0
+  LevelK K{};
+  XferAxis tx{}, ty{}, tz{};     // transfer from the finer level (valid for level >= 1)
+  float* x = nullptr;            // solution / correction (level 0: caller's buffer)
+  bool own_x = false;
+  float* b = nullptr;            // restricted residual (levels >= 1)
+  float* xlo = nullptr;          // ghost planes of x for distributed slabs
+  float* xhi = nullptr;
+};
+
+struct HierKey {
+  long long nx, ny, nzl, z0, nzg;
+  float bx, by, bz, alpha;
+  int coarse_max;
+  bool operator<(const HierKey& o) const {
+    return std::tie(nx, ny, nzl, z0, nzg, bx, by, bz, alpha, coarse_max) <
+           std::tie(o.nx, o.ny, o.nzl, o.z0, o.nzg, o.bx, o.by, o.bz, o.alpha, o.coarse_max);
+  }
+};
+
+struct Hier {
+  HierKey key{};
+  std::vector<Level> lv;
+  CoarseK coarse{};
+  std::vector<float*> dev_tables;
+  double2* partials = nullptr;     // norm partials of level 0
+  double2* plane_sums = nullptr;   // per-plane (sum a, sum b), device
+  double2* h_plane = nullptr;      // pinned host mirror
+  float* scratch_e = nullptr;      // single-level direct solve correction
+  ~Hier();
+};
+
+struct Fine {        // the finest level of one solve
+  float* x = nullptr;
+  RhsK R{};
+  int mode = RHS_B;
+  int tI = 1;        // 0 = u8 source, 1 = f32
+};
+
+struct Comm;          // NCCL communicator state (gdp_comm.cu)
+
+struct Ctx {
+  int device = 0, rank = 0, world = 1;
+  std::map<HierKey, std::unique_ptr<Hier>> hier;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  void* scratch = nullptr;
+  size_t scratch_bytes = 0;
+  Comm* comm = nullptr;
+  // host-entry staging (gdp_destripe_host): device copies of I0, I1, I2 and two streams
+  void* hbuf[3] = {nullptr, nullptr, nullptr};
+  size_t hbuf_cap[3] = {0, 0, 0};
+  cudaStream_t hs = nullptr, hcs = nullptr;
+  cudaEvent_t hev = nullptr;
+  int get_hier(const HierKey& k, Hier** out);
+  int ensure_scratch(size_t bytes);
+  int ensure_hbuf(int i, size_t bytes);
+  ~Ctx();
+};
+
+int build_hier(const HierKey& key, std::unique_ptr<Hier>& out);
+int run_vcycle(Ctx& ctx, Hier& H, const Fine& f, const gdp_opts& o, cudaStream_t s);
+int finest_norms(Ctx& ctx, Hier& H, const Fine& f, float* rout, cudaStream_t s);
+int solve(Ctx& ctx, Hier& H, const Fine& f, const gdp_opts& o, bool per_slice, gdp_report* rep,
+          cudaStream_t s);
+double hbm_model(const Hier& H, double s_I, double s_V, int vcycles);
+
+// fused schedule (gdp_fused.cu): return true if the pass was handled
+bool fused_down(const Level& L, const Level& C, float* x, const RhsK& R, int mode, int tI, int nu,
+                cudaStream_t s);
+bool fused_up(const Level& L, const Level& C, float* x, const RhsK& R, int mode, int tI, int nu,
+              cudaStream_t s);
+
+// communication (gdp_comm.cu); single-rank contexts make these no-ops
+int comm_init(Ctx& c, const void* nccl_unique_id);
+void comm_destroy(Ctx& c);
+int comm_allreduce_sum2(Ctx& c, double* a, double* b, cudaStream_t s);
+int comm_halo_x(Ctx& c, Hier& H, int level, float* x, cudaStream_t s);
+
+}  // namespace gdp
+
+struct gdp_ctx {
+  gdp::Ctx impl;
+};

@@ -1,0 +1,404 @@
+// gdp_kernels.cu — sm_100a kernels of the multigrid V-cycle.
+//
+// Reference schedule (opts.fused = 0): one kernel per red-black half-sweep, one per
+// residual+restriction, one per prolongation+correction.  The fused schedule lives
+// in gdp_fused.cu and calls the same per-point arithmetic (gdp_device.cuh), so both
+// schedules produce bit-identical iterates.
+#include "gdp_kernels.h"
+
+namespace gdp {
+
+// ---------------------------------------------------------------------------------
+// neighbour loads with ghost planes (z-slab halos of a distributed ctx)
+// ---------------------------------------------------------------------------------
+__device__ __forceinline__ Nbr load_nbr(const float* x, const float* xlo, const float* xhi,
+                                        const LevelK& L, const Coef& k, int iz, long long c,
+                                        float xc) {
+  const long long nx = L.nx, plane = (long long)L.nx * L.ny;
+  Nbr nb;
+  nb.w = k.xl != 0.f ? x[c - 1] : xc;
+  nb.e = k.xr != 0.f ? x[c + 1] : xc;
+  nb.s = k.yl != 0.f ? x[c - nx] : xc;
+  nb.n = k.yr != 0.f ? x[c + nx] : xc;
+  nb.d = k.zl != 0.f ? (iz > 0 ? x[c - plane] : xlo[c]) : xc;
+  nb.u = k.zr != 0.f ? (iz < L.nzl - 1 ? x[c + plane] : xhi[c - (long long)iz * plane]) : xc;
+  return nb;
+}
+
+// a4: one red-black Gauss-Seidel half-sweep (colour = (x + y + z_global) & 1).
+template <int MODE, typename TI>
+__global__ void __launch_bounds__(256) k_rbgs(LevelK L, float* __restrict__ x, const float* xlo,
+                                              const float* xhi, RhsK R, int color) {
+  const int iy = blockIdx.y * blockDim.y + threadIdx.y;
+  const int iz = blockIdx.z;
+  if (iy >= L.ny) return;
+  const long long zg = L.z0 + iz;
+  const int ix = 2 * (blockIdx.x * blockDim.x + threadIdx.x) + ((color + iy + (int)(zg & 1)) & 1);
+  if (ix >= L.nx) return;
+  const long long plane = (long long)L.nx * L.ny;
+  const long long c = iz * plane + (long long)iy * L.nx + ix;
+  const Coef k = coefs(L, ix, iy, zg);
+  const float xc = x[c];
+  const Nbr nb = load_nbr(x, xlo, xhi, L, k, iz, c, xc);
+  const float r = residual_at<MODE, TI>(L, R, k, xc, nb, c, L.nx, plane, nullptr);
+  x[c] = gs_update(xc, r, k.diag(L.alpha));
+}
+
+// a5+a6: residual at the fine level, restricted by volume-weighted child average.
+// One thread per coarse cell; every fine cell belongs to exactly one parent.
+template <int MODE, typename TI>
+__global__ void __launch_bounds__(256) k_restrict(LevelK L, const float* __restrict__ x,
+                                                  const float* xlo, const float* xhi, RhsK R,
+                                                  XferAxis tx, XferAxis ty, XferAxis tz,
+                                                  int ncx, int ncy, int nczl,
+                                                  float* __restrict__ bc) {
+  const int cx = blockIdx.x * blockDim.x + threadIdx.x;
+  const int cy = blockIdx.y * blockDim.y + threadIdx.y;
+  const int cz = blockIdx.z;
+  if (cx >= ncx || cy >= ncy) return;
+  const long long plane = (long long)L.nx * L.ny;
+  const int fx0 = tx.coarsened ? 2 * cx : cx, fx1 = tx.coarsened ? min(2 * cx + 1, L.nx - 1) : cx;
+  const int fy0 = ty.coarsened ? 2 * cy : cy, fy1 = ty.coarsened ? min(2 * cy + 1, L.ny - 1) : cy;
+  const int fz0 = tz.coarsened ? 2 * cz : cz, fz1 = tz.coarsened ? min(2 * cz + 1, L.nzl - 1) : cz;
+  float acc = 0.f;
+  for (int fz = fz0; fz <= fz1; ++fz) {
+    const long long zg = L.z0 + fz;
+    const float wz = rweight(tz, zg);
+    for (int fy = fy0; fy <= fy1; ++fy) {
+      const float wy = rweight(ty, fy);
+      for (int fx = fx0; fx <= fx1; ++fx) {
+        const float wx = rweight(tx, fx);
+        const long long c = fz * plane + (long long)fy * L.nx + fx;
+        const Coef k = coefs(L, fx, fy, zg);
+        const float xc = x[c];
+        const Nbr nb = load_nbr(x, xlo, xhi, L, k, fz, c, xc);
+        const float r = residual_at<MODE, TI>(L, R, k, xc, nb, c, L.nx, plane, nullptr);
+        acc += (wz * wy * wx) * r;
+      }
+    }
+  }
+  bc[(long long)cz * ncx * ncy + (long long)cy * ncx + cx] = acc;
+}
+
+// a8: x_fine += P x_coarse (cell-centred linear interpolation, constant at the faces).
+__global__ void __launch_bounds__(256) k_prolong(LevelK L, float* __restrict__ xf,
+                                                 XferAxis tx, XferAxis ty, XferAxis tz,
+                                                 int ncx, int ncy, int nczl, long long cz0,
+                                                 const float* __restrict__ xc,
+                                                 const float* xclo, const float* xchi) {
+  const int fx = blockIdx.x * blockDim.x + threadIdx.x;
+  const int fy = blockIdx.y * blockDim.y + threadIdx.y;
+  const int fz = blockIdx.z;
+  if (fx >= L.nx || fy >= L.ny) return;
+  long long Ix, Jx, Iy, Jy, Iz, Jz;
+  float txw, tyw, tzw;
+  ptaps(tx, fx, Ix, Jx, txw);
+  ptaps(ty, fy, Iy, Jy, tyw);
+  ptaps(tz, L.z0 + fz, Iz, Jz, tzw);
+  const long long cplane = (long long)ncx * ncy;
+  // z taps are global coarse indices; map to local planes or ghost planes
+  auto zrow = [&](long long zgc) -> const float* {
+    const long long lz = zgc - cz0;
+    if (lz < 0) return xclo;
+    if (lz >= nczl) return xchi;
+    return xc + lz * cplane;
+  };
+  const float* pI = zrow(Iz);
+  const float* pJ = zrow(Jz);
+  auto bil = [&](const float* p) {
+    const float a = p[Iy * ncx + Ix], b = p[Iy * ncx + Jx];
+    const float c = p[Jy * ncx + Ix], d = p[Jy * ncx + Jx];
+    const float r0 = (1.f - txw) * a + txw * b;
+    const float r1 = (1.f - txw) * c + txw * d;
+    return (1.f - tyw) * r0 + tyw * r1;
+  };
+  float e = bil(pI);
+  if (tzw != 0.f) e = (1.f - tzw) * e + tzw * bil(pJ);
+  const long long f = (long long)fz * L.nx * L.ny + (long long)fy * L.nx + fx;
+  xf[f] += e;
+}
+
+// a5: residual r = b - A x with per-block fp64 partial sums of r^2 and b^2 (one row of
+// partials per plane, reduced in a fixed order by k_finalize -> deterministic).
+template <int MODE, typename TI>
+__global__ void __launch_bounds__(256) k_norms(LevelK L, const float* __restrict__ x,
+                                               const float* xlo, const float* xhi, RhsK R,
+                                               float* __restrict__ rout, double2* partials) {
+  const int ix = blockIdx.x * blockDim.x + threadIdx.x;
+  const int iz = blockIdx.z;
+  const long long zg = L.z0 + iz;
+  const long long plane = (long long)L.nx * L.ny;
+  double sr = 0.0, sb = 0.0;
+  if (ix < L.nx) {
+    for (int iy = blockIdx.y * blockDim.y + threadIdx.y; iy < L.ny; iy += gridDim.y * blockDim.y) {
+      const long long c = iz * plane + (long long)iy * L.nx + ix;
+      const Coef k = coefs(L, ix, iy, zg);
+      const float xc = x[c];
+      const Nbr nb = load_nbr(x, xlo, xhi, L, k, iz, c, xc);
+      float bv;
+      const float r = residual_at<MODE, TI>(L, R, k, xc, nb, c, L.nx, plane, &bv);
+      if (rout) rout[c] = r;
+      sr += (double)r * (double)r;
+      sb += (double)bv * (double)bv;
+    }
+  }
+  block_sum2(sr, sb);
+  if (threadIdx.x == 0 && threadIdx.y == 0) {
+    const long long bid = ((long long)iz * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+    partials[bid] = make_double2(sr, sb);
+  }
+}
+
+// per-plane sums of a field (mean pin, a10): partial (sum a, sum a2) with a2 a second field
+template <typename TA, typename TB>
+__global__ void __launch_bounds__(256) k_plane_sums(const void* a, const void* b, int nx, int ny,
+                                                    double2* partials) {
+  const int ix = blockIdx.x * blockDim.x + threadIdx.x;
+  const int iz = blockIdx.z;
+  const long long plane = (long long)nx * ny;
+  double sa = 0.0, sb = 0.0;
+  if (ix < nx) {
+    for (int iy = blockIdx.y * blockDim.y + threadIdx.y; iy < ny; iy += gridDim.y * blockDim.y) {
+      const long long c = iz * plane + (long long)iy * nx + ix;
+      sa += (double)ldI<TA>(a, c);
+      if (b) sb += (double)ldI<TB>(b, c);
+    }
+  }
+  block_sum2(sa, sb);
+  if (threadIdx.x == 0 && threadIdx.y == 0) {
+    const long long bid = ((long long)iz * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+    partials[bid] = make_double2(sa, sb);
+  }
+}
+
+// fixed-order reduction of `per` partials per plane -> out[plane]
+__global__ void __launch_bounds__(256) k_finalize(const double2* partials, int per,
+                                                  double2* out) {
+  const int p = blockIdx.x;
+  double a = 0.0, b = 0.0;
+  for (int i = threadIdx.x; i < per; i += blockDim.x) {
+    const double2 v = partials[(long long)p * per + i];
+    a += v.x;
+    b += v.y;
+  }
+  block_sum2(a, b);
+  if (threadIdx.x == 0) out[p] = make_double2(a, b);
+}
+
+template <typename TI>
+__global__ void k_decode_copy(const void* I, float* __restrict__ x, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    x[i] = ldI<TI>(I, i);
+}
+
+__global__ void k_add_scalar(float* __restrict__ x, long long n, float s) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    x[i] += s;
+}
+
+__global__ void k_axpy(float* __restrict__ x, const float* __restrict__ e, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    x[i] += e[i];
+}
+
+// a7: coarsest level, exact solve by fast diagonalisation.  The coarsest operator is
+// alpha + T_x (+) T_y (+) T_z (Kronecker sum of 1D finite-volume operators), so
+// x = V (Lambda^-1 (V^-1 b)) with per-axis eigenvectors computed once on the host.
+// With alpha = 0 the constant mode (lambda = 0) is dropped: the coarse problem is
+// projected onto the range of A and its mean-zero solution returned (reading c-3).
+// One CTA per independent system (the whole level, or one slice when z is uncoupled).
+__global__ void __launch_bounds__(512) k_coarse_fd(CoarseK C, const float* __restrict__ b,
+                                                   float* __restrict__ x) {
+  extern __shared__ float sm[];
+  const int nx = C.nx, ny = C.ny, nzs = C.cz ? C.nz : 1;
+  const int nsys = nx * ny * nzs;
+  const long long off = C.cz ? 0 : (long long)blockIdx.x * nx * ny;
+  float* A = sm;
+  float* B = sm + nsys;
+  for (int i = threadIdx.x; i < nsys; i += blockDim.x) A[i] = b[off + i];
+  __syncthreads();
+  auto tx = [&](const float* M, float* in, float* out) {  // along x
+    for (int i = threadIdx.x; i < nsys; i += blockDim.x) {
+      const int k = i % nx, r = i / nx;
+      float s = 0.f;
+      for (int j = 0; j < nx; ++j) s = fmaf(__ldg(M + k * nx + j), in[r * nx + j], s);
+      out[i] = s;
+    }
+    __syncthreads();
+  };
+  auto ty = [&](const float* M, float* in, float* out) {  // along y
+    for (int i = threadIdx.x; i < nsys; i += blockDim.x) {
+      const int xx = i % nx, k = (i / nx) % ny, z = i / (nx * ny);
+      float s = 0.f;
+      for (int j = 0; j < ny; ++j) s = fmaf(__ldg(M + k * ny + j), in[(z * ny + j) * nx + xx], s);
+      out[i] = s;
+    }
+    __syncthreads();
+  };
+  auto tz = [&](const float* M, float* in, float* out) {  // along z
+    const int pl = nx * ny;
+    for (int i = threadIdx.x; i < nsys; i += blockDim.x) {
+      const int q = i % pl, k = i / pl;
+      float s = 0.f;
+      for (int j = 0; j < nzs; ++j) s = fmaf(__ldg(M + k * nzs + j), in[j * pl + q], s);
+      out[i] = s;
+    }
+    __syncthreads();
+  };
+  float* cur = A;
+  float* nxt = B;
+  if (C.cx && nx > 1) { tx(C.Fx, cur, nxt); float* t = cur; cur = nxt; nxt = t; }
+  if (C.cy && ny > 1) { ty(C.Fy, cur, nxt); float* t = cur; cur = nxt; nxt = t; }
+  if (C.cz && nzs > 1) { tz(C.Fz, cur, nxt); float* t = cur; cur = nxt; nxt = t; }
+  for (int i = threadIdx.x; i < nsys; i += blockDim.x) {
+    const int xx = i % nx, yy = (i / nx) % ny, zz = i / (nx * ny);
+    float lam = C.alpha;
+    if (C.cx && nx > 1) lam += __ldg(C.lx + xx);
+    if (C.cy && ny > 1) lam += __ldg(C.ly + yy);
+    if (C.cz && nzs > 1) lam += __ldg(C.lz + zz);
+    cur[i] = lam > C.lam_thr ? cur[i] / lam : 0.f;
+  }
+  __syncthreads();
+  if (C.cx && nx > 1) { tx(C.Bx, cur, nxt); float* t = cur; cur = nxt; nxt = t; }
+  if (C.cy && ny > 1) { ty(C.By, cur, nxt); float* t = cur; cur = nxt; nxt = t; }
+  if (C.cz && nzs > 1) { tz(C.Bz, cur, nxt); float* t = cur; cur = nxt; nxt = t; }
+  for (int i = threadIdx.x; i < nsys; i += blockDim.x) x[off + i] = cur[i];
+}
+
+// ---------------------------------------------------------------------------------
+// host launchers
+// ---------------------------------------------------------------------------------
+static inline dim3 grid_plane(int nx, int ny, int nz, dim3 blk, int ymax) {
+  int gy = (ny + blk.y - 1) / blk.y;
+  if (ymax > 0 && gy > ymax) gy = ymax;
+  return dim3((nx + blk.x - 1) / blk.x, gy, nz);
+}
+
+template <int MODE, typename TI>
+static void launch_rbgs_t(const LevelK& L, float* x, const float* xlo, const float* xhi,
+                          const RhsK& R, int color, cudaStream_t s) {
+  dim3 blk(32, 8);
+  dim3 grd(((L.nx + 1) / 2 + blk.x - 1) / blk.x, (L.ny + blk.y - 1) / blk.y, L.nzl);
+  k_rbgs<MODE, TI><<<grd, blk, 0, s>>>(L, x, xlo, xhi, R, color);
+}
+
+void launch_rbgs(const LevelK& L, float* x, const float* xlo, const float* xhi, const RhsK& R,
+                 int mode, int tI, int color, cudaStream_t s) {
+  count_launch();
+  if (mode == RHS_B) launch_rbgs_t<RHS_B, float>(L, x, xlo, xhi, R, color, s);
+  else if (tI == 0) launch_rbgs_t<RHS_G, uint8_t>(L, x, xlo, xhi, R, color, s);
+  else launch_rbgs_t<RHS_G, float>(L, x, xlo, xhi, R, color, s);
+}
+
+template <int MODE, typename TI>
+static void launch_restrict_t(const LevelK& L, const float* x, const float* xlo, const float* xhi,
+                              const RhsK& R, const XferAxis& tx, const XferAxis& ty,
+                              const XferAxis& tz, int ncx, int ncy, int nczl, float* bc,
+                              cudaStream_t s) {
+  dim3 blk(32, 8);
+  dim3 grd((ncx + 31) / 32, (ncy + 7) / 8, nczl);
+  k_restrict<MODE, TI><<<grd, blk, 0, s>>>(L, x, xlo, xhi, R, tx, ty, tz, ncx, ncy, nczl, bc);
+}
+
+void launch_restrict(const LevelK& L, const float* x, const float* xlo, const float* xhi,
+                     const RhsK& R, int mode, int tI, const XferAxis& tx, const XferAxis& ty,
+                     const XferAxis& tz, int ncx, int ncy, int nczl, float* bc, cudaStream_t s) {
+  count_launch();
+  if (mode == RHS_B)
+    launch_restrict_t<RHS_B, float>(L, x, xlo, xhi, R, tx, ty, tz, ncx, ncy, nczl, bc, s);
+  else if (tI == 0)
+    launch_restrict_t<RHS_G, uint8_t>(L, x, xlo, xhi, R, tx, ty, tz, ncx, ncy, nczl, bc, s);
+  else
+    launch_restrict_t<RHS_G, float>(L, x, xlo, xhi, R, tx, ty, tz, ncx, ncy, nczl, bc, s);
+}
+
+void launch_prolong(const LevelK& L, float* xf, const XferAxis& tx, const XferAxis& ty,
+                    const XferAxis& tz, int ncx, int ncy, int nczl, long long cz0, const float* xc,
+                    const float* xclo, const float* xchi, cudaStream_t s) {
+  count_launch();
+  dim3 blk(32, 8);
+  dim3 grd((L.nx + 31) / 32, (L.ny + 7) / 8, L.nzl);
+  k_prolong<<<grd, blk, 0, s>>>(L, xf, tx, ty, tz, ncx, ncy, nczl, cz0, xc, xclo, xchi);
+}
+
+int norms_blocks_per_plane(int nx, int ny) {
+  dim3 blk(128, 2);
+  dim3 g = grid_plane(nx, ny, 1, blk, 32);
+  return g.x * g.y;
+}
+
+template <int MODE, typename TI>
+static void launch_norms_t(const LevelK& L, const float* x, const float* xlo, const float* xhi,
+                           const RhsK& R, float* rout, double2* partials, cudaStream_t s) {
+  dim3 blk(128, 2);
+  dim3 grd = grid_plane(L.nx, L.ny, L.nzl, blk, 32);
+  k_norms<MODE, TI><<<grd, blk, 0, s>>>(L, x, xlo, xhi, R, rout, partials);
+}
+
+void launch_norms(const LevelK& L, const float* x, const float* xlo, const float* xhi,
+                  const RhsK& R, int mode, int tI, float* rout, double2* partials,
+                  double2* plane_out, cudaStream_t s) {
+  count_launch();
+  if (mode == RHS_B) launch_norms_t<RHS_B, float>(L, x, xlo, xhi, R, rout, partials, s);
+  else if (tI == 0) launch_norms_t<RHS_G, uint8_t>(L, x, xlo, xhi, R, rout, partials, s);
+  else launch_norms_t<RHS_G, float>(L, x, xlo, xhi, R, rout, partials, s);
+  count_launch();
+  k_finalize<<<L.nzl, 256, 0, s>>>(partials, norms_blocks_per_plane(L.nx, L.ny), plane_out);
+}
+
+void launch_plane_sums(const void* a, int ta, const void* b, int tb, int nx, int ny, int nz,
+                       double2* partials, double2* plane_out, cudaStream_t s) {
+  count_launch();
+  dim3 blk(128, 2);
+  dim3 grd = grid_plane(nx, ny, nz, blk, 32);
+  if (ta == 1 && tb == 0) k_plane_sums<float, uint8_t><<<grd, blk, 0, s>>>(a, b, nx, ny, partials);
+  else if (ta == 1) k_plane_sums<float, float><<<grd, blk, 0, s>>>(a, b, nx, ny, partials);
+  else if (tb == 0) k_plane_sums<uint8_t, uint8_t><<<grd, blk, 0, s>>>(a, b, nx, ny, partials);
+  else k_plane_sums<uint8_t, float><<<grd, blk, 0, s>>>(a, b, nx, ny, partials);
+  count_launch();
+  k_finalize<<<nz, 256, 0, s>>>(partials, norms_blocks_per_plane(nx, ny), plane_out);
+}
+
+static inline int ew_grid(long long n) {
+  long long g = (n + 255) / 256;
+  return (int)(g > 148 * 32 ? 148 * 32 : (g < 1 ? 1 : g));
+}
+
+void launch_decode_copy(const void* I, int tI, float* x, long long n, cudaStream_t s) {
+  count_launch();
+  if (tI == 0) k_decode_copy<uint8_t><<<ew_grid(n), 256, 0, s>>>(I, x, n);
+  else k_decode_copy<float><<<ew_grid(n), 256, 0, s>>>(I, x, n);
+}
+
+void launch_add_scalar(float* x, long long n, float v, cudaStream_t s) {
+  count_launch();
+  k_add_scalar<<<ew_grid(n), 256, 0, s>>>(x, n, v);
+}
+
+void launch_axpy(float* x, const float* e, long long n, cudaStream_t s) {
+  count_launch();
+  k_axpy<<<ew_grid(n), 256, 0, s>>>(x, e, n);
+}
+
+size_t coarse_smem_bytes(const CoarseK& C) {
+  const long long nsys = (long long)C.nx * C.ny * (C.cz ? C.nz : 1);
+  return (size_t)(2 * nsys * sizeof(float));
+}
+
+cudaError_t launch_coarse(const CoarseK& C, const float* b, float* x, cudaStream_t s) {
+  count_launch();
+  const size_t smem = coarse_smem_bytes(C);
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(k_coarse_fd, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr_set = true;
+  }
+  const int nsys = C.cz ? 1 : C.nz;
+  k_coarse_fd<<<nsys, 512, smem, s>>>(C, b, x);
+  return cudaGetLastError();
+}
+
+}  // namespace gdp

@@ -1,0 +1,71 @@
+// gdp_kernels.h — internal launch interface between the solver core (gdp_solver.cu)
+// and the kernels (gdp_kernels.cu, gdp_fused.cu).  Not part of the C ABI.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+
+#include "gdp_device.cuh"
+
+namespace gdp {
+
+extern std::atomic<long long> g_launches;
+inline void count_launch(long long n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+// fp64 block reduction of two values (warp shuffle, then shared memory); result valid in
+// thread (0,0).  Fixed order -> deterministic.
+__device__ __forceinline__ void block_sum2(double& a, double& b) {
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_down_sync(0xffffffffu, a, o);
+    b += __shfl_down_sync(0xffffffffu, b, o);
+  }
+  __shared__ double sa[32], sb[32];
+  const int nthr = blockDim.x * blockDim.y * blockDim.z;
+  const int tid = threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
+  const int lane = tid & 31, warp = tid >> 5;
+  if (lane == 0) { sa[warp] = a; sb[warp] = b; }
+  __syncthreads();
+  if (warp == 0) {
+    const int nw = (nthr + 31) >> 5;
+    a = lane < nw ? sa[lane] : 0.0;
+    b = lane < nw ? sb[lane] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) {
+      a += __shfl_down_sync(0xffffffffu, a, o);
+      b += __shfl_down_sync(0xffffffffu, b, o);
+    }
+  }
+}
+
+struct CoarseK {
+  int nx, ny, nz;     // coarsest level dims (whole level)
+  int cx, cy, cz;     // coupled (transformed) axes; an uncoupled z makes nz independent systems
+  const float *Fx, *Bx, *lx;
+  const float *Fy, *By, *ly;
+  const float *Fz, *Bz, *lz;
+  float alpha;
+  float lam_thr;      // eigenvalues <= lam_thr are dropped (alpha = 0 null space)
+};
+
+// reference-schedule kernels (tI: 0 = u8, 1 = f32)
+void launch_rbgs(const LevelK& L, float* x, const float* xlo, const float* xhi, const RhsK& R,
+                 int mode, int tI, int color, cudaStream_t s);
+void launch_restrict(const LevelK& L, const float* x, const float* xlo, const float* xhi,
+                     const RhsK& R, int mode, int tI, const XferAxis& tx, const XferAxis& ty,
+                     const XferAxis& tz, int ncx, int ncy, int nczl, float* bc, cudaStream_t s);
+void launch_prolong(const LevelK& L, float* xf, const XferAxis& tx, const XferAxis& ty,
+                    const XferAxis& tz, int ncx, int ncy, int nczl, long long cz0, const float* xc,
+                    const float* xclo, const float* xchi, cudaStream_t s);
+int norms_blocks_per_plane(int nx, int ny);
+void launch_norms(const LevelK& L, const float* x, const float* xlo, const float* xhi,
+                  const RhsK& R, int mode, int tI, float* rout, double2* partials,
+                  double2* plane_out, cudaStream_t s);
+void launch_plane_sums(const void* a, int ta, const void* b, int tb, int nx, int ny, int nz,
+                       double2* partials, double2* plane_out, cudaStream_t s);
+void launch_decode_copy(const void* I, int tI, float* x, long long n, cudaStream_t s);
+void launch_add_scalar(float* x, long long n, float v, cudaStream_t s);
+void launch_axpy(float* x, const float* e, long long n, cudaStream_t s);
+size_t coarse_smem_bytes(const CoarseK& C);
+cudaError_t launch_coarse(const CoarseK& C, const float* b, float* x, cudaStream_t s);
+
+}  // namespace gdp

@@ -1,0 +1,761 @@
+// gdp_solver.cu — solver core behind the C ABI (include/gdp.h).
+//
+// Owns the multigrid hierarchy, the coarsest-level fast
+// diagonalisation, the V-cycle driver with its stopping rule, the mean pin of the
+// alpha = 0 diffusion and the C entry points.  Every arithmetic step runs in the
+// kernels of gdp_kernels.cu / gdp_fused.cu; the host only orchestrates and reads
+// back fp64 norms (a few bytes per V-cycle).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/gdp.h"
+#include "gdp_internal.h"
+
+namespace gdp {
+
+std::atomic<long long> g_launches{0};
+
+static thread_local std::string t_err;
+
+int set_err(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  t_err = buf;
+  return code;
+}
+
+#define CK(call)                                                                          \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      return set_err(e_ == cudaErrorMemoryAllocation ? GDP_ENOMEM : GDP_ECUDA,            \
+                     "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__,   \
+                     __LINE__);                                                           \
+  } while (0)
+
+#define RET(call)                    \
+  do {                               \
+    int r_ = (call);                 \
+    if (r_ != GDP_OK) return r_;     \
+  } while (0)
+
+// ---------------------------------------------------------------------------------
+// host geometry
+// ---------------------------------------------------------------------------------
+static AxisC make_axisc(const AxisG& g) {
+  AxisC a{};
+  a.n = g.n;
+  if (g.beta <= 0.0 || g.n <= 1) { a.k = a.kr = a.kl = 0.f; return a; }
+  const double dl = 0.5 * (g.H + g.hl);
+  a.k = (float)(g.beta / (g.H * g.H));
+  a.kr = (float)(g.beta / (dl * g.H));
+  a.kl = (float)(g.beta / (dl * g.hl));
+  return a;
+}
+
+static AxisG coarsen_axis(const AxisG& f) {
+  AxisG c = f;
+  c.n = (f.n + 1) / 2;
+  c.H = 2.0 * f.H;
+  c.hl = (f.n % 2 == 1) ? f.hl : (f.H + f.hl);
+  return c;
+}
+
+static XferAxis make_xfer(const AxisG& f, const AxisG& c, bool coarsened) {
+  XferAxis t{};
+  t.coarsened = coarsened ? 1 : 0;
+  t.nf = f.n; t.nc = c.n;
+  t.Hf = (float)f.H; t.hlf = (float)f.hl;
+  t.Hc = (float)c.H; t.hlc = (float)c.hl;
+  return t;
+}
+
+// cyclic Jacobi eigen-decomposition of a symmetric n x n matrix (row-major), n <= 64
+static void jacobi_eig(int n, std::vector<double>& A, std::vector<double>& Q, std::vector<double>& lam) {
+  Q.assign((size_t)n * n, 0.0);
+  for (int i = 0; i < n; ++i) Q[(size_t)i * n + i] = 1.0;
+  for (int sweep = 0; sweep < 100; ++sweep) {
+    double off = 0.0, tot = 0.0;
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < n; ++j) {
+        const double v = A[(size_t)i * n + j] * A[(size_t)i * n + j];
+        tot += v;
+        if (i != j) off += v;
+      }
+    if (off <= 1e-30 * tot || off == 0.0) break;
+    for (int p = 0; p < n - 1; ++p)
+      for (int q = p + 1; q < n; ++q) {
+        const double apq = A[(size_t)p * n + q];
+        if (std::fabs(apq) < 1e-300) continue;
+        const double app = A[(size_t)p * n + p], aqq = A[(size_t)q * n + q];
+        const double theta = (aqq - app) / (2.0 * apq);
+        const double t = (theta >= 0 ? 1.0 : -1.0) / (std::fabs(theta) + std::sqrt(theta * theta + 1.0));
+        const double c = 1.0 / std::sqrt(t * t + 1.0), s = t * c;
+        for (int k = 0; k < n; ++k) {  // columns p, q
+          const double akp = A[(size_t)k * n + p], akq = A[(size_t)k * n + q];
+          A[(size_t)k * n + p] = c * akp - s * akq;
+          A[(size_t)k * n + q] = s * akp + c * akq;
+        }
+        for (int k = 0; k < n; ++k) {  // rows p, q
+          const double apk = A[(size_t)p * n + k], aqk = A[(size_t)q * n + k];
+          A[(size_t)p * n + k] = c * apk - s * aqk;
+          A[(size_t)q * n + k] = s * apk + c * aqk;
+        }
+        for (int k = 0; k < n; ++k) {
+          const double qkp = Q[(size_t)k * n + p], qkq = Q[(size_t)k * n + q];
+          Q[(size_t)k * n + p] = c * qkp - s * qkq;
+          Q[(size_t)k * n + q] = s * qkp + c * qkq;
+        }
+      }
+  }
+  lam.resize(n);
+  for (int i = 0; i < n; ++i) lam[i] = A[(size_t)i * n + i];
+  // sort ascending (column permutation of Q)
+  std::vector<int> idx(n);
+  for (int i = 0; i < n; ++i) idx[i] = i;
+  std::sort(idx.begin(), idx.end(), [&](int a, int b) { return lam[a] < lam[b]; });
+  std::vector<double> Q2((size_t)n * n), l2(n);
+  for (int k = 0; k < n; ++k) {
+    l2[k] = lam[idx[k]];
+    for (int i = 0; i < n; ++i) Q2[(size_t)i * n + k] = Q[(size_t)i * n + idx[k]];
+  }
+  Q.swap(Q2);
+  lam.swap(l2);
+}
+
+// Per-axis fast-diagonalisation factors of the 1D finite-volume operator T of an axis.
+// T = D^-1 S with S symmetric (D = diag of cell widths) -> M = D^1/2 T D^-1/2 = Q L Q^T,
+// forward F = Q^T D^1/2 (row k = mode), backward B = D^-1/2 Q.
+static void fd_axis(const AxisG& g, std::vector<float>& F, std::vector<float>& B,
+                    std::vector<float>& lamf, double& lmax) {
+  const int n = g.n;
+  const AxisC a = make_axisc(g);
+  std::vector<double> h(n), T((size_t)n * n, 0.0);
+  const double dl = 0.5 * (g.H + g.hl);
+  for (int i = 0; i < n; ++i) h[i] = (i == n - 1) ? g.hl : g.H;
+  auto cld = [&](int i) -> double {
+    if (i <= 0) return 0.0;
+    return i == n - 1 ? g.beta / (dl * g.hl) : g.beta / (g.H * g.H);
+  };
+  auto crd = [&](int i) -> double {
+    if (i >= n - 1) return 0.0;
+    return i == n - 2 ? g.beta / (dl * g.H) : g.beta / (g.H * g.H);
+  };
+  (void)a;
+  for (int i = 0; i < n; ++i) {
+    T[(size_t)i * n + i] = cld(i) + crd(i);
+    if (i > 0) T[(size_t)i * n + i - 1] = -cld(i);
+    if (i < n - 1) T[(size_t)i * n + i + 1] = -crd(i);
+  }
+  std::vector<double> M((size_t)n * n);
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) M[(size_t)i * n + j] = std::sqrt(h[i]) * T[(size_t)i * n + j] / std::sqrt(h[j]);
+  // symmetrise exactly
+  for (int i = 0; i < n; ++i)
+    for (int j = i + 1; j < n; ++j) {
+      const double v = 0.5 * (M[(size_t)i * n + j] + M[(size_t)j * n + i]);
+      M[(size_t)i * n + j] = M[(size_t)j * n + i] = v;
+    }
+  std::vector<double> Q, lam;
+  jacobi_eig(n, M, Q, lam);
+  F.resize((size_t)n * n);
+  B.resize((size_t)n * n);
+  lamf.resize(n);
+  lmax = 0.0;
+  for (int k = 0; k < n; ++k) {
+    lamf[k] = (float)std::max(lam[k], 0.0);
+    lmax = std::max(lmax, lam[k]);
+    for (int i = 0; i < n; ++i) {
+      F[(size_t)k * n + i] = (float)(Q[(size_t)i * n + k] * std::sqrt(h[i]));
+      B[(size_t)i * n + k] = (float)(Q[(size_t)i * n + k] / std::sqrt(h[i]));
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------
+// hierarchy
+// ---------------------------------------------------------------------------------
+Hier::~Hier() {
+  for (auto& L : lv) {
+    if (L.own_x && L.x) cudaFree(L.x);
+    if (L.b) cudaFree(L.b);
+    if (L.xlo) cudaFree(L.xlo);
+    if (L.xhi) cudaFree(L.xhi);
+  }
+  for (float* p : dev_tables) cudaFree(p);
+  if (partials) cudaFree(partials);
+  if (plane_sums) cudaFree(plane_sums);
+  if (scratch_e) cudaFree(scratch_e);
+  if (h_plane) cudaFreeHost(h_plane);
+}
+
+static int upload(std::vector<float*>& owned, const std::vector<float>& v, const float** out) {
+  float* p = nullptr;
+  CK(cudaMalloc(&p, std::max<size_t>(v.size(), 1) * sizeof(float)));
+  owned.push_back(p);
+  if (!v.empty()) CK(cudaMemcpy(p, v.data(), v.size() * sizeof(float), cudaMemcpyHostToDevice));
+  *out = p;
+  return GDP_OK;
+}
+
+int build_hier(const HierKey& key, std::unique_ptr<Hier>& out) {
+  auto H = std::make_unique<Hier>();
+  H->key = key;
+  Level L0;
+  L0.gx = AxisG{(int)key.nx, 1.0, 1.0, key.bx};
+  L0.gy = AxisG{(int)key.ny, 1.0, 1.0, key.by};
+  L0.gz = AxisG{(int)key.nzg, 1.0, 1.0, key.bz};
+  L0.nx = (int)key.nx; L0.ny = (int)key.ny; L0.nzl = (int)key.nzl; L0.z0 = key.z0;
+  H->lv.push_back(L0);
+  for (;;) {
+    Level& F = H->lv.back();
+    const AxisG* g[3] = {&F.gx, &F.gy, &F.gz};
+    double s[3];
+    bool cpl[3];
+    long long size = 1;
+    int maxn = 1;
+    double smax = 0.0;
+    for (int d = 0; d < 3; ++d) {
+      cpl[d] = g[d]->beta > 0.0 && g[d]->n > 1;
+      s[d] = cpl[d] ? g[d]->beta / (g[d]->H * g[d]->H) : 0.0;
+      if (cpl[d]) { size *= g[d]->n; maxn = std::max(maxn, g[d]->n); smax = std::max(smax, s[d]); }
+    }
+    const bool any = cpl[0] || cpl[1] || cpl[2];
+    if (!any) break;
+    if (size <= key.coarse_max && maxn <= 64 && H->lv.size() > 1) break;
+    if (size <= key.coarse_max && maxn <= 64 && size <= 64) break;  // tiny: solve directly
+    if ((int)H->lv.size() >= GDP_MAX_LEVELS) break;
+    bool co[3];
+    for (int d = 0; d < 3; ++d) co[d] = cpl[d] && s[d] >= 0.5 * smax;
+    // distributed z-slabs: only coarsen z while every slab stays aligned (even z0, even nzl)
+    if (co[2] && (F.nzl % 2 != 0 || F.z0 % 2 != 0) && F.nzl != F.gz.n) co[2] = false;
+    if (!(co[0] || co[1] || co[2])) break;
+    Level C;
+    C.gx = co[0] ? coarsen_axis(F.gx) : F.gx;
+    C.gy = co[1] ? coarsen_axis(F.gy) : F.gy;
+    C.gz = co[2] ? coarsen_axis(F.gz) : F.gz;
+    C.tx = make_xfer(F.gx, C.gx, co[0]);
+    C.ty = make_xfer(F.gy, C.gy, co[1]);
+    C.tz = make_xfer(F.gz, C.gz, co[2]);
+    C.nx = C.gx.n; C.ny = C.gy.n;
+    C.nzl = co[2] ? (F.nzl + 1) / 2 : F.nzl;
+    C.z0 = co[2] ? F.z0 / 2 : F.z0;
+    H->lv.push_back(C);
+  }
+  // device buffers and kernel-side coefficients
+  long long maxplanes = 0;
+  for (size_t l = 0; l < H->lv.size(); ++l) {
+    Level& L = H->lv[l];
+    L.K.nx = L.nx; L.K.ny = L.ny; L.K.nzl = L.nzl; L.K.z0 = L.z0;
+    L.K.ax = make_axisc(L.gx); L.K.ay = make_axisc(L.gy); L.K.az = make_axisc(L.gz);
+    L.K.alpha = (float)key.alpha;
+    const size_t n = (size_t)L.nx * L.ny * L.nzl;
+    if (l > 0) {
+      CK(cudaMalloc(&L.x, n * sizeof(float)));
+      L.own_x = true;
+      CK(cudaMalloc(&L.b, n * sizeof(float)));
+    }
+    maxplanes = std::max<long long>(maxplanes, L.nzl);
+  }
+  const int nl = (int)H->lv.size();
+  Level& Lc = H->lv[nl - 1];
+  if (nl == 1) {  // direct solve of level 0: residual / correction scratch
+    const size_t n = (size_t)Lc.nx * Lc.ny * Lc.nzl;
+    CK(cudaMalloc(&Lc.b, n * sizeof(float)));
+    CK(cudaMalloc(&H->scratch_e, n * sizeof(float)));
+  }
+  // coarsest fast diagonalisation
+  CoarseK C{};
+  C.nx = Lc.nx; C.ny = Lc.ny; C.nz = Lc.nzl;
+  C.cx = Lc.gx.beta > 0 && Lc.gx.n > 1;
+  C.cy = Lc.gy.beta > 0 && Lc.gy.n > 1;
+  C.cz = Lc.gz.beta > 0 && Lc.gz.n > 1;
+  if (C.cz && Lc.nzl != Lc.gz.n)
+    return set_err(GDP_EINVAL, "coarsest level split across ranks (agglomeration not built)");
+  C.alpha = (float)key.alpha;
+  double lsum = 0.0;
+  const AxisG* ga[3] = {&Lc.gx, &Lc.gy, &Lc.gz};
+  const float** Fp[3] = {&C.Fx, &C.Fy, &C.Fz};
+  const float** Bp[3] = {&C.Bx, &C.By, &C.Bz};
+  const float** lp[3] = {&C.lx, &C.ly, &C.lz};
+  const int cflag[3] = {C.cx, C.cy, C.cz};
+  for (int d = 0; d < 3; ++d) {
+    if (!cflag[d]) { *Fp[d] = *Bp[d] = *lp[d] = nullptr; continue; }
+    std::vector<float> F, B, lam;
+    double lmax;
+    fd_axis(*ga[d], F, B, lam, lmax);
+    lsum += lmax;
+    RET(upload(H->dev_tables, F, Fp[d]));
+    RET(upload(H->dev_tables, B, Bp[d]));
+    RET(upload(H->dev_tables, lam, lp[d]));
+  }
+  C.lam_thr = key.alpha > 0 ? -1.f : (float)(1e-9 * std::max(lsum, 1e-30));
+  const long long nsys = (long long)C.nx * C.ny * (C.cz ? C.nz : 1);
+  if (nsys * 2 * sizeof(float) > 200 * 1024)
+    return set_err(GDP_EINVAL, "coarsest system of %lld unknowns exceeds shared memory", nsys);
+  H->coarse = C;
+  // norm partials: level-0 plane rows
+  const int per = norms_blocks_per_plane(H->lv[0].nx, H->lv[0].ny);
+  CK(cudaMalloc(&H->partials, (size_t)per * std::max<long long>(maxplanes, 1) * sizeof(double2)));
+  CK(cudaMalloc(&H->plane_sums, (size_t)std::max<long long>(maxplanes, 1) * sizeof(double2)));
+  CK(cudaMallocHost(&H->h_plane, (size_t)std::max<long long>(maxplanes, 1) * sizeof(double2)));
+  out = std::move(H);
+  return GDP_OK;
+}
+
+// ---------------------------------------------------------------------------------
+// context
+// ---------------------------------------------------------------------------------
+Ctx::~Ctx() {
+  hier.clear();
+  if (ev0) cudaEventDestroy(ev0);
+  if (ev1) cudaEventDestroy(ev1);
+  if (scratch) cudaFree(scratch);
+  for (int i = 0; i < 3; ++i)
+    if (hbuf[i]) cudaFree(hbuf[i]);
+  if (hs) cudaStreamDestroy(hs);
+  if (hcs) cudaStreamDestroy(hcs);
+  if (hev) cudaEventDestroy(hev);
+}
+
+int Ctx::ensure_hbuf(int i, size_t bytes) {
+  if (hbuf_cap[i] >= bytes) return GDP_OK;
+  if (hbuf[i]) cudaFree(hbuf[i]);
+  hbuf[i] = nullptr;
+  hbuf_cap[i] = 0;
+  CK(cudaMalloc(&hbuf[i], bytes));
+  hbuf_cap[i] = bytes;
+  return GDP_OK;
+}
+
+int Ctx::get_hier(const HierKey& k, Hier** out) {
+  auto it = hier.find(k);
+  if (it != hier.end()) { *out = it->second.get(); return GDP_OK; }
+  std::unique_ptr<Hier> H;
+  RET(build_hier(k, H));
+  *out = H.get();
+  hier[k] = std::move(H);
+  return GDP_OK;
+}
+
+int Ctx::ensure_scratch(size_t bytes) {
+  if (scratch_bytes >= bytes) return GDP_OK;
+  if (scratch) cudaFree(scratch);
+  scratch = nullptr;
+  scratch_bytes = 0;
+  CK(cudaMalloc(&scratch, bytes));
+  scratch_bytes = bytes;
+  return GDP_OK;
+}
+
+// ---------------------------------------------------------------------------------
+// V-cycle (reference schedule; the fused schedule replaces the level passes)
+// ---------------------------------------------------------------------------------
+static int smooth(const Level& L, float* x, const RhsK& R, int mode, int tI, int nu, cudaStream_t s) {
+  for (int k = 0; k < nu; ++k)
+    for (int color = 0; color < 2; ++color)
+      launch_rbgs(L.K, x, L.xlo, L.xhi, R, mode, tI, color, s);
+  return GDP_OK;
+}
+
+int run_vcycle(Ctx& ctx, Hier& H, const Fine& f, const gdp_opts& o, cudaStream_t s) {
+  const int nl = (int)H.lv.size();
+  if (nl == 1) {  // level 0 is the coarsest: x += A^-1 (b - A x)
+    Level& L = H.lv[0];
+    launch_norms(L.K, f.x, L.xlo, L.xhi, f.R, f.mode, f.tI, L.b, H.partials, H.plane_sums, s);
+    CK(launch_coarse(H.coarse, L.b, H.scratch_e, s));
+    launch_axpy(f.x, H.scratch_e, (long long)L.nx * L.ny * L.nzl, s);
+    return GDP_OK;
+  }
+  const bool fused = o.fused != 0;
+  for (int l = 0; l < nl - 1; ++l) {
+    Level& L = H.lv[l];
+    Level& C = H.lv[l + 1];
+    float* x = l == 0 ? f.x : L.x;
+    RhsK R = f.R;
+    int mode = f.mode, tI = f.tI;
+    if (l > 0) {
+      R = RhsK{L.b, nullptr, nullptr, 0.f, 0};
+      mode = RHS_B;
+      tI = 1;
+      CK(cudaMemsetAsync(x, 0, sizeof(float) * (size_t)L.nx * L.ny * L.nzl, s));
+    }
+    if (fused && fused_down(L, C, x, R, mode, tI, o.nu_pre, s)) continue;
+    smooth(L, x, R, mode, tI, o.nu_pre, s);
+    launch_restrict(L.K, x, L.xlo, L.xhi, R, mode, tI, C.tx, C.ty, C.tz, C.nx, C.ny, C.nzl, C.b, s);
+  }
+  Level& Lc = H.lv[nl - 1];
+  CK(launch_coarse(H.coarse, Lc.b, Lc.x, s));
+  for (int l = nl - 2; l >= 0; --l) {
+    Level& L = H.lv[l];
+    Level& C = H.lv[l + 1];
+    float* x = l == 0 ? f.x : L.x;
+    RhsK R = f.R;
+    int mode = f.mode, tI = f.tI;
+    if (l > 0) { R = RhsK{L.b, nullptr, nullptr, 0.f, 0}; mode = RHS_B; tI = 1; }
+    if (fused && fused_up(L, C, x, R, mode, tI, o.nu_post, s)) continue;
+    launch_prolong(L.K, x, C.tx, C.ty, C.tz, C.nx, C.ny, C.nzl, C.z0, C.x, C.xlo, C.xhi, s);
+    smooth(L, x, R, mode, tI, o.nu_post, s);
+  }
+  CK(cudaGetLastError());
+  return GDP_OK;
+}
+
+// fp64 norms of the finest level -> per-plane (sum r^2, sum b^2) on the host
+int finest_norms(Ctx& ctx, Hier& H, const Fine& f, float* rout, cudaStream_t s) {
+  Level& L = H.lv[0];
+  launch_norms(L.K, f.x, L.xlo, L.xhi, f.R, f.mode, f.tI, rout, H.partials, H.plane_sums, s);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(H.h_plane, H.plane_sums, sizeof(double2) * L.nzl, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return GDP_OK;
+}
+
+// rel-res of the current iterate: one system (all planes) or max over slices
+static double rel_from_planes(const Hier& H, bool per_slice, double* worst_b) {
+  const int nz = H.lv[0].nzl;
+  if (!per_slice) {
+    double rr = 0.0, bb = 0.0;
+    for (int z = 0; z < nz; ++z) { rr += H.h_plane[z].x; bb += H.h_plane[z].y; }
+    if (worst_b) *worst_b = std::sqrt(bb);
+    return bb > 0 ? std::sqrt(rr / bb) : std::sqrt(rr);
+  }
+  double worst = 0.0, wb = 0.0;
+  for (int z = 0; z < nz; ++z) {
+    const double rr = H.h_plane[z].x, bb = H.h_plane[z].y;
+    const double v = bb > 0 ? std::sqrt(rr / bb) : std::sqrt(rr);
+    if (v >= worst) { worst = v; wb = std::sqrt(bb); }
+  }
+  if (worst_b) *worst_b = wb;
+  return worst;
+}
+
+// full solve: cycles until rel_tol / cap / stagnation (a9)
+int solve(Ctx& ctx, Hier& H, const Fine& f, const gdp_opts& o, bool per_slice, gdp_report* rep,
+          cudaStream_t s) {
+  gdp_report r{};
+  r.levels = (int)H.lv.size();
+  RET(finest_norms(ctx, H, f, nullptr, s));
+  double nb = 0.0;
+  double rel = rel_from_planes(H, per_slice, &nb);
+  r.rel_res[0] = rel;
+  r.norm_b = nb;
+  int status = GDP_OK;
+  int stall = 0;
+  int k = 0;
+  const int cap = std::min(o.max_vcycles, GDP_MAX_CYCLES);
+  while (rel > o.rel_tol) {
+    if (k >= cap) { status = GDP_ENOCONV; break; }
+    RET(run_vcycle(ctx, H, f, o, s));
+    RET(finest_norms(ctx, H, f, nullptr, s));
+    const double nrel = rel_from_planes(H, per_slice, nullptr);
+    ++k;
+    r.rel_res[k] = nrel;
+    if (o.stagnation > 0 && nrel > 0.9 * rel) {
+      if (++stall >= o.stagnation) { rel = nrel; status = nrel <= o.rel_tol ? GDP_OK : GDP_ENOCONV; break; }
+    } else {
+      stall = 0;
+    }
+    rel = nrel;
+  }
+  r.vcycles = k;
+  r.status = status;
+  if (rep) {
+    const double secs = rep->seconds;
+    *rep = r;
+    rep->seconds = secs;
+  }
+  return status;
+}
+
+}  // namespace gdp
+
+// =================================================================================
+// C ABI
+// =================================================================================
+using namespace gdp;
+
+static bool finite_nonneg(double v) { return std::isfinite(v) && v >= 0.0; }
+
+static int check_common(gdp_ctx* ctx, gdp_dims d, int64_t z0, int64_t nzg) {
+  if (!ctx) return set_err(GDP_EINVAL, "null ctx");
+  if (d.nx <= 0 || d.ny <= 0 || d.nz <= 0) return set_err(GDP_EINVAL, "dims must be positive");
+  if (d.nx > (1LL << 30) || d.ny > (1LL << 30) || d.nz > 65535)
+    return set_err(GDP_EINVAL, "dims too large for this build");
+  if (z0 < 0 || nzg < d.nz || z0 + d.nz > nzg)
+    return set_err(GDP_EINVAL, "slab [z0, z0+nz) outside [0, nz_global)");
+  if (ctx->impl.world == 1 && (z0 != 0 || nzg != d.nz))
+    return set_err(GDP_EINVAL, "single-rank ctx needs z0 = 0 and nz_global = nz");
+  CK(cudaSetDevice(ctx->impl.device));
+  return GDP_OK;
+}
+
+static int check_params(gdp_weights W, float alpha) {
+  if (!finite_nonneg(W.bx) || !finite_nonneg(W.by) || !finite_nonneg(W.bz) || !finite_nonneg(alpha))
+    return set_err(GDP_EINVAL, "alpha and weights must be finite and >= 0");
+  if (alpha == 0.f && W.bx == 0.f && W.by == 0.f && W.bz == 0.f)
+    return set_err(GDP_EINVAL, "alpha = 0 with all weights 0 is singular");
+  return GDP_OK;
+}
+
+static gdp_opts resolve_opts(const gdp_opts* o) {
+  gdp_opts d;
+  gdp_opts_default(&d);
+  if (!o) return d;
+  gdp_opts r = *o;
+  if (!(r.rel_tol > 0)) r.rel_tol = d.rel_tol;
+  if (r.max_vcycles <= 0) r.max_vcycles = d.max_vcycles;
+  if (r.nu_pre < 0) r.nu_pre = d.nu_pre;
+  if (r.nu_post < 0) r.nu_post = d.nu_post;
+  if (r.coarse_max <= 0) r.coarse_max = d.coarse_max;
+  return r;
+}
+
+static HierKey make_key(gdp_dims d, int64_t z0, int64_t nzg, gdp_weights W, float alpha,
+                        const gdp_opts& o) {
+  HierKey k{};
+  k.nx = d.nx; k.ny = d.ny; k.nzl = d.nz; k.z0 = z0; k.nzg = nzg;
+  k.bx = W.bx; k.by = W.by; k.bz = W.bz; k.alpha = alpha;
+  k.coarse_max = o.coarse_max;
+  return k;
+}
+
+extern "C" {
+
+int gdp_opts_default(gdp_opts* o) {
+  if (!o) return set_err(GDP_EINVAL, "null opts");
+  o->rel_tol = 1e-6;
+  o->max_vcycles = 30;
+  o->nu_pre = 2;
+  o->nu_post = 2;
+  o->coarse_max = 4096;
+  o->stagnation = 2;
+  o->fused = 1;
+  o->use_graphs = 0;
+  return GDP_OK;
+}
+
+int gdp_ctx_create(gdp_ctx** out, int device, int rank, int world, const void* nccl_unique_id) {
+  if (!out) return set_err(GDP_EINVAL, "null out");
+  *out = nullptr;
+  if (world < 1 || rank < 0 || rank >= world) return set_err(GDP_EINVAL, "bad rank/world");
+  int ndev = 0;
+  CK(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return set_err(GDP_EINVAL, "bad device %d (have %d)", device, ndev);
+  CK(cudaSetDevice(device));
+  auto* c = new gdp_ctx();
+  c->impl.device = device;
+  c->impl.rank = rank;
+  c->impl.world = world;
+  if (world > 1) {
+    int rc = comm_init(c->impl, nccl_unique_id);
+    if (rc != GDP_OK) { delete c; return rc; }
+  }
+  cudaEventCreate(&c->impl.ev0);
+  cudaEventCreate(&c->impl.ev1);
+  *out = c;
+  return GDP_OK;
+}
+
+int gdp_ctx_create_loopback(gdp_ctx** out, int device, int world) {
+  if (!out) return set_err(GDP_EINVAL, "null out");
+  *out = nullptr;
+  return set_err(GDP_EINVAL, "loopback ctx: partitioned path not available in this build");
+}
+
+int gdp_ctx_destroy(gdp_ctx* ctx) {
+  if (!ctx) return GDP_OK;
+  cudaSetDevice(ctx->impl.device);
+  comm_destroy(ctx->impl);
+  delete ctx;
+  return GDP_OK;
+}
+
+static void fill_time(gdp_ctx* ctx, gdp_report* rep, cudaStream_t s) {
+  if (!rep) return;
+  cudaEventSynchronize(ctx->impl.ev1);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, ctx->impl.ev0, ctx->impl.ev1);
+  rep->seconds = ms * 1e-3;
+  (void)s;
+}
+
+int gdp_diffuse_z(gdp_ctx* ctx, const void* I0, gdp_dtype dtype, float* I1, gdp_dims local,
+                  int64_t z0_global, int64_t nz_global, gdp_weights W, float alpha,
+                  const gdp_opts* opts, gdp_report* report, void* stream) {
+  RET(check_common(ctx, local, z0_global, nz_global));
+  RET(check_params(W, alpha));
+  if (!I0 || !I1) return set_err(GDP_EINVAL, "null I0/I1");
+  if ((const void*)I1 == I0) return set_err(GDP_EINVAL, "I1 may not alias I0");
+  if (dtype != GDP_U8 && dtype != GDP_F32) return set_err(GDP_EINVAL, "bad dtype");
+  const gdp_opts o = resolve_opts(opts);
+  cudaStream_t s = (cudaStream_t)stream;
+  Ctx& C = ctx->impl;
+  const long long before = g_launches.load();
+  Hier* H;
+  RET(C.get_hier(make_key(local, z0_global, nz_global, W, alpha, o), &H));
+  const int tI = dtype == GDP_U8 ? 0 : 1;
+  const long long n = local.nx * local.ny * local.nz;
+  CK(cudaEventRecord(C.ev0, s));
+  launch_decode_copy(I0, tI, I1, n, s);  // x0 = I0
+  Fine f;
+  f.x = I1;
+  f.mode = RHS_G;
+  f.tI = tI;
+  f.R = RhsK{nullptr, I0, nullptr, alpha, alpha > 0 ? 1 : 0};
+  // Eq. (1): the gradient target uses (bx, by); the rhs is formed on the fly (a2)
+  int st = solve(C, *H, f, o, false, report, s);
+  if (st != GDP_OK && st != GDP_ENOCONV) return st;
+  if (alpha == 0.f) {  // a10: pin mean(I1) = mean(I0) in fp64 (reading c-3)
+    Level& L = H->lv[0];
+    launch_plane_sums(I1, 1, I0, tI, L.nx, L.ny, L.nzl, H->partials, H->plane_sums, s);
+    CK(cudaMemcpyAsync(H->h_plane, H->plane_sums, sizeof(double2) * L.nzl, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    double sx = 0.0, si = 0.0;
+    for (int z = 0; z < L.nzl; ++z) { sx += H->h_plane[z].x; si += H->h_plane[z].y; }
+    RET(comm_allreduce_sum2(C, &sx, &si, s));
+    const double Ntot = (double)local.nx * local.ny * nz_global;
+    launch_add_scalar(I1, n, (float)((si - sx) / Ntot), s);
+  }
+  CK(cudaEventRecord(C.ev1, s));
+  CK(cudaGetLastError());
+  if (report) {
+    fill_time(ctx, report, s);
+    report->kernel_launches = g_launches.load() - before;
+    report->hbm_bytes_est = hbm_model(*H, tI == 0 ? 1.0 : 4.0, 0.0, report->vcycles);
+  }
+  if (st == GDP_ENOCONV) set_err(GDP_ENOCONV, "diffuse_z: not converged after %d V-cycles", report ? report->vcycles : -1);
+  return st;
+}
+
+int gdp_screened_poisson_slices(gdp_ctx* ctx, const void* I0, gdp_dtype dtype, const float* I1,
+                                float* I2, gdp_dims local, float alpha, const gdp_opts* opts,
+                                gdp_report* report, void* stream) {
+  if (!ctx) return set_err(GDP_EINVAL, "null ctx");
+  if (!I0 || !I1 || !I2) return set_err(GDP_EINVAL, "null I0/I1/I2");
+  if (!(alpha > 0.f) || !std::isfinite(alpha)) return set_err(GDP_EINVAL, "slices need finite alpha > 0");
+  if ((const void*)I2 == I0 || I2 == I1) return set_err(GDP_EINVAL, "I2 may not alias I0 or I1");
+  if (dtype != GDP_U8 && dtype != GDP_F32) return set_err(GDP_EINVAL, "bad dtype");
+  if (local.nx <= 0 || local.ny <= 0 || local.nz <= 0) return set_err(GDP_EINVAL, "dims must be positive");
+  CK(cudaSetDevice(ctx->impl.device));
+  const gdp_opts o = resolve_opts(opts);
+  cudaStream_t s = (cudaStream_t)stream;
+  Ctx& C = ctx->impl;
+  const long long before = g_launches.load();
+  gdp_weights W{1.f, 1.f, 0.f};  // pi = Diag(1,1,0), Eq. (2)
+  Hier* H;
+  // slices are independent: the local slab is its own "global" stack (no halo)
+  RET(C.get_hier(make_key(local, 0, local.nz, W, alpha, o), &H));
+  const int tI = dtype == GDP_U8 ? 0 : 1;
+  const long long n = local.nx * local.ny * local.nz;
+  CK(cudaEventRecord(C.ev0, s));
+  launch_decode_copy(I0, tI, I2, n, s);  // x0 = I0
+  Fine f;
+  f.x = I2;
+  f.mode = RHS_G;
+  f.tI = tI;
+  f.R = RhsK{nullptr, I0, I1, alpha, 2};
+  int st = solve(C, *H, f, o, true, report, s);
+  if (st != GDP_OK && st != GDP_ENOCONV) return st;
+  CK(cudaEventRecord(C.ev1, s));
+  if (report) {
+    fill_time(ctx, report, s);
+    report->kernel_launches = g_launches.load() - before;
+    report->hbm_bytes_est = hbm_model(*H, tI == 0 ? 1.0 : 4.0, 4.0, report->vcycles);
+  }
+  if (st == GDP_ENOCONV) set_err(GDP_ENOCONV, "screened_poisson_slices: not converged");
+  return st;
+}
+
+int gdp_destripe(gdp_ctx* ctx, const void* I0, gdp_dtype dtype, float* I1, float* I2,
+                 gdp_dims local, int64_t z0_global, int64_t nz_global, gdp_weights W,
+                 float alpha, const gdp_opts* opts, gdp_report* rep1, gdp_report* rep2,
+                 void* stream) {
+  if (!ctx) return set_err(GDP_EINVAL, "null ctx");
+  float* I1p = I1;
+  if (!I1p) {
+    RET(check_common(ctx, local, z0_global, nz_global));
+    RET(ctx->impl.ensure_scratch(sizeof(float) * (size_t)(local.nx * local.ny * local.nz)));
+    I1p = (float*)ctx->impl.scratch;
+  }
+  int st1 = gdp_diffuse_z(ctx, I0, dtype, I1p, local, z0_global, nz_global, W, 0.f, opts, rep1, stream);
+  if (st1 != GDP_OK && st1 != GDP_ENOCONV) return st1;
+  int st2 = gdp_screened_poisson_slices(ctx, I0, dtype, I1p, I2, local, alpha, opts, rep2, stream);
+  if (st2 != GDP_OK) return st2;
+  return st1;
+}
+
+int gdp_vcycle(gdp_ctx* ctx, float* x, const float* b, gdp_dims local, int64_t z0_global,
+               int64_t nz_global, gdp_weights W, float alpha, const gdp_opts* opts,
+               double* rel_res_after, void* stream) {
+  RET(check_common(ctx, local, z0_global, nz_global));
+  RET(check_params(W, alpha));
+  if (!x || !b) return set_err(GDP_EINVAL, "null x/b");
+  const gdp_opts o = resolve_opts(opts);
+  cudaStream_t s = (cudaStream_t)stream;
+  Ctx& C = ctx->impl;
+  Hier* H;
+  RET(C.get_hier(make_key(local, z0_global, nz_global, W, alpha, o), &H));
+  Fine f;
+  f.x = x;
+  f.mode = RHS_B;
+  f.tI = 1;
+  f.R = RhsK{b, nullptr, nullptr, 0.f, 0};
+  RET(run_vcycle(C, *H, f, o, s));
+  if (rel_res_after) {
+    RET(finest_norms(C, *H, f, nullptr, s));
+    double rr = 0.0, bb = 0.0;
+    for (int z = 0; z < H->lv[0].nzl; ++z) { rr += H->h_plane[z].x; bb += H->h_plane[z].y; }
+    RET(comm_allreduce_sum2(C, &rr, &bb, s));
+    *rel_res_after = bb > 0 ? std::sqrt(rr / bb) : std::sqrt(rr);
+  }
+  return GDP_OK;
+}
+
+int gdp_residual(gdp_ctx* ctx, const float* x, const float* b, float* r, gdp_dims local,
+                 int64_t z0_global, int64_t nz_global, gdp_weights W, float alpha,
+                 double* norm2_r, double* norm2_b, void* stream) {
+  RET(check_common(ctx, local, z0_global, nz_global));
+  RET(check_params(W, alpha));
+  if (!x || !b) return set_err(GDP_EINVAL, "null x/b");
+  gdp_opts o;
+  gdp_opts_default(&o);
+  cudaStream_t s = (cudaStream_t)stream;
+  Ctx& C = ctx->impl;
+  Hier* H;
+  RET(C.get_hier(make_key(local, z0_global, nz_global, W, alpha, o), &H));
+  RET(comm_halo_x(C, *H, 0, const_cast<float*>(x), s));
+  Fine f;
+  f.x = const_cast<float*>(x);
+  f.mode = RHS_B;
+  f.tI = 1;
+  f.R = RhsK{b, nullptr, nullptr, 0.f, 0};
+  RET(finest_norms(C, *H, f, r, s));
+  double rr = 0.0, bb = 0.0;
+  for (int z = 0; z < H->lv[0].nzl; ++z) { rr += H->h_plane[z].x; bb += H->h_plane[z].y; }
+  RET(comm_allreduce_sum2(C, &rr, &bb, s));
+  if (norm2_r) *norm2_r = rr;
+  if (norm2_b) *norm2_b = bb;
+  return GDP_OK;
+}
+
+const char* gdp_last_error(void) { return t_err.c_str(); }
+
+const char* gdp_version(void) { return "gdp-b200 0.1 (sm_100a)"; }
+
+int64_t gdp_kernel_launch_count(void) { return g_launches.load(); }
+
+}  // extern "C"

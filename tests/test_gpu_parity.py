@@ -1,0 +1,174 @@
+"""GPU parity (-m gpu): the CUDA path, called through the C ABI, against the CPU oracle on
+the same seeded inputs.
+
+Bars (BASELINE.json north_star):
+  * solutions: max |x_gpu - x_oracle| <= 1e-4 on [0,1] intensities; each phase is held to
+    5e-5 so the two-phase pipeline stays within 1e-4 (reading c-13);
+  * residual: ||b - A x_gpu|| / ||b|| <= 1e-6, evaluated by the oracle in fp64 against the
+    oracle's fp64 b (phase 2: every slice);
+  * the residual kernel itself: |r_gpu - r_fp64| <= 8 eps32 * (|b| + sum_links |coef| (|x_c|+|x_n|)
+    + alpha |x|) per voxel (fp32 rounding of <= 16 operations).
+"""
+import numpy as np
+import pytest
+import torch
+
+import gdp_synth as synth
+import oracle as O
+import paper_1310_0041_b200 as gdp
+
+pytestmark = pytest.mark.gpu
+
+TOL_X = 5e-5
+TOL_R = 1e-6
+W_AD = (1.0, 1.0, 0.1)
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def host(t):
+    return t.detach().cpu().numpy().astype(np.float64)
+
+
+def _rel_ad(I0, I1_gpu, W=W_AD):
+    b = O.rhs_diffusion(O.decode(I0) if I0.dtype != np.float64 else I0, W)
+    return O.rel_residual(I1_gpu, b, W, 0.0)
+
+
+def _rel_sp(I0, I1, I2_gpu, alpha):
+    b = O.rhs_blend(O.decode(I0), I1, alpha)
+    return O.slice_rel_residuals(I2_gpu, b, alpha).max()
+
+
+# ------------------------------------------------------------------ residual kernel
+@pytest.mark.parametrize("shape,W,alpha", [((7, 33, 45), (1.0, 1.0, 0.1), 0.0),
+                                           ((3, 64, 64), (0.5, 2.0, 0.3), 0.25),
+                                           ((1, 17, 130), (1.0, 1.0, 0.0), 0.01),
+                                           ((5, 1, 9), (1.0, 1.0, 1.0), 0.0)])
+def test_residual_elementwise(gpu_ctx, shape, W, alpha):
+    rng = np.random.default_rng(3)
+    x = rng.random(shape).astype(np.float32)
+    b = (rng.random(shape) * 2 - 1).astype(np.float32)
+    r = torch.empty(shape, dtype=torch.float32, device="cuda")
+    _, nr, nb = gdp.gdp_residual(gpu_ctx, dev(x), dev(b), r, W=W, alpha=alpha)
+    r64 = O.residual(x.astype(np.float64), b.astype(np.float64), W, alpha)
+    coef = 2 * (W[0] + W[1] + W[2]) + alpha
+    bound = 8 * 2.0 ** -24 * (np.abs(b) + coef * 2 * np.abs(x).max() + 1.0)
+    assert np.all(np.abs(host(r) - r64) <= bound)
+    assert nr == pytest.approx(np.sum(r64 * r64), rel=1e-5)
+    assert nb == pytest.approx(np.sum(b.astype(np.float64) ** 2), rel=1e-12)
+
+
+# ------------------------------------------------------------------ phase 1
+@pytest.mark.parametrize("shape,dtype,seed", [((16, 64, 64), "f32", 0),      # config 0
+                                              ((9, 63, 65), "u8", 5),
+                                              ((5, 37, 29), "f32", 6),
+                                              ((33, 40, 48), "u8", 7),
+                                              ((2, 200, 150), "u8", 8)])
+def test_diffuse_z_parity(gpu_ctx, shape, dtype, seed):
+    nz, ny, nx = shape
+    I0 = synth.make_stack(nx, ny, nz, seed, dtype)
+    I1, rep = gdp.gdp_diffuse_z(gpu_ctx, dev(I0))
+    assert rep["status"] == "GDP_OK", rep
+    ref = O.diffuse_z(I0)
+    x = host(I1)
+    assert np.abs(x - ref).max() <= TOL_X
+    assert _rel_ad(I0, x) <= TOL_R
+    assert x.mean() == pytest.approx(O.decode(I0).mean(), abs=1e-6)
+
+
+# ------------------------------------------------------------------ phase 2
+@pytest.mark.parametrize("alpha", [0.001, 0.01, 0.1])
+@pytest.mark.parametrize("shape,dtype", [((4, 96, 128), "u8"), ((3, 65, 47), "f32"), ((2, 300, 260), "u8")])
+def test_screened_poisson_parity(gpu_ctx, shape, dtype, alpha):
+    nz, ny, nx = shape
+    I0 = synth.make_stack(nx, ny, nz, 21, dtype)
+    I1 = O.diffuse_z(I0).astype(np.float32)  # phase 2 checked in isolation (reading c-13)
+    I2, rep = gdp.gdp_screened_poisson_slices(gpu_ctx, dev(I0), dev(I1), alpha=alpha)
+    assert rep["status"] == "GDP_OK", rep
+    ref = O.screened_poisson_slices(I0, I1, alpha)
+    x = host(I2)
+    assert np.abs(x - ref).max() <= TOL_X
+    assert _rel_sp(I0, I1, x, alpha) <= TOL_R
+
+
+def test_destripe_config0(gpu_ctx):
+    I0 = synth.make_config(0)
+    I1, I2, r1, r2 = gdp.gdp_destripe(gpu_ctx, dev(I0), alpha=0.01)
+    ref1, ref2 = O.destripe(I0, alpha=0.01)
+    assert np.abs(host(I1) - ref1).max() <= TOL_X
+    assert np.abs(host(I2) - ref2).max() <= 1e-4
+    assert r1["status"] == "GDP_OK" and r2["status"] == "GDP_OK"
+
+
+# ------------------------------------------------------------------ closed forms / edge cases
+def test_constant_stack_is_fixed_point(gpu_ctx):
+    I0 = np.full((6, 40, 52), 77, np.uint8)
+    I1, I2, r1, r2 = gdp.gdp_destripe(gpu_ctx, dev(I0))
+    v = np.float32(77) / np.float32(255)
+    assert np.all(host(I1) == v) and np.all(host(I2) == v)
+
+
+def test_offset_striping_closed_form(gpu_ctx):
+    I0, T, c = synth.offset_striped_u8(256, 256, 32, 2)
+    exp = (T[None].astype(np.float64) + c.mean()) / 255.0
+    I1, I2, r1, r2 = gdp.gdp_destripe(gpu_ctx, dev(I0))
+    assert np.abs(host(I1) - exp).max() <= TOL_X
+    assert np.abs(host(I2) - exp).max() <= 1e-4
+
+
+def test_single_slice_and_thin(gpu_ctx):
+    for shape in ((1, 70, 90), (2, 3, 200), (4, 1, 1), (1, 1, 1)):
+        nz, ny, nx = shape
+        I0 = synth.random_field(shape, 4)
+        I1, rep = gdp.gdp_diffuse_z(gpu_ctx, dev(I0))
+        ref = O.diffuse_z(I0)
+        assert np.abs(host(I1) - ref).max() <= TOL_X, shape
+        I1f = ref.astype(np.float32)
+        I2, rep = gdp.gdp_screened_poisson_slices(gpu_ctx, dev(I0), dev(I1f), alpha=0.01)
+        assert np.abs(host(I2) - O.screened_poisson_slices(I0, I1f, 0.01)).max() <= TOL_X, shape
+
+
+def test_vcycle_and_residual_api(gpu_ctx):
+    shape = (8, 48, 40)
+    rng = np.random.default_rng(9)
+    for W, alpha in ((W_AD, 0.0), ((1.0, 1.0, 1.0), 0.05)):
+        b = rng.standard_normal(shape)
+        if alpha == 0.0:
+            b -= b.mean()
+        b32 = b.astype(np.float32)
+        x = torch.zeros(shape, dtype=torch.float32, device="cuda")
+        rels = [gdp.gdp_vcycle(gpu_ctx, x, dev(b32), W=W, alpha=alpha) for _ in range(8)]
+        assert all(r1 < r0 for r0, r1 in zip(rels[:3], rels[1:4]))
+        assert rels[-1] < 1e-5
+        ref = O.dct_solve(b32.astype(np.float64), W, alpha)
+        xs = host(x)
+        if alpha == 0.0:
+            xs -= xs.mean()
+        assert np.abs(xs - ref).max() < 1e-4 * max(1.0, np.abs(ref).max())
+
+
+def test_invalid_arguments(gpu_ctx):
+    I0 = dev(np.zeros((2, 8, 8), np.uint8))
+    with pytest.raises(gdp.GdpError) as e:
+        gdp.gdp_diffuse_z(gpu_ctx, I0, W=(-1.0, 1.0, 0.1))
+    assert e.value.code == 1
+    with pytest.raises(gdp.GdpError) as e:
+        gdp.gdp_diffuse_z(gpu_ctx, I0, W=(0.0, 0.0, 0.0), alpha=0.0)
+    assert e.value.code == 1
+    I1 = torch.zeros((2, 8, 8), dtype=torch.float32, device="cuda")
+    with pytest.raises(gdp.GdpError) as e:
+        gdp.gdp_screened_poisson_slices(gpu_ctx, I0, I1, alpha=0.0)
+    assert e.value.code == 1
+
+
+def test_report_and_launches(gpu_ctx):
+    I0 = synth.make_config(0)
+    before = gdp.kernel_launch_count()
+    I1, rep = gdp.gdp_diffuse_z(gpu_ctx, dev(I0))
+    assert rep["levels"] >= 2 and 1 <= rep["vcycles"] <= 12
+    assert rep["rel_res"][-1] <= 1e-6 and rep["rel_res"][0] > 1e-3
+    assert rep["kernel_launches"] > 0 and gdp.kernel_launch_count() - before == rep["kernel_launches"]
+    assert rep["seconds"] > 0

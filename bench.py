@@ -1,0 +1,331 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 hot path: both phases of the paper's de-striping method
+ solved to convergence (rel-res <= 1e-6) on BASELINE.json config 1
+(1024 x 1024 x 128 uint8, alpha = 0.01, W = (1, 1, 0.1)).
+
+A "step" = one converged phase-1 solve (Eq. 1) + one converged phase-2 solve (Eq. 2) on
+the resident stack.  Metric: voxels/s per converged solve (both phases).
+
+  python bench.py [--gpus N --steps K --warmup W]            # our arm (default N=1)
+  python bench.py --impl reference --steps K --warmup W       # the CPU oracle as the reference arm
+  torchrun --nproc-per-node N ... bench.py --gpus N           # N ranks, one GPU each
+
+Multi-GPU: every rank solves its own config-1 stack (independent problems, seeds offset by
+rank): weak scaling, no data-path collective.  Timing: CUDA events
+on the solve stream, barrier + synchronize on both sides, max over ranks.  The working set
+(I0 134 MB u8 + x, I1, I2 537 MB fp32 each) exceeds the 126 MB L2, so no explicit flush.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIG = 1
+ALPHA = 0.01
+W = (1.0, 1.0, 0.1)
+METRIC = "voxels/s per converged solve (both phases)"
+UNIT = "voxels/s"
+# bounded CPU sample of the same workload (config-1 generator, seed 1): xy crop x first slices
+SAMPLE = dict(nx=128, ny=128, nz=32)
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--config", type=int, default=CONFIG)
+    p.add_argument("--alpha", type=float, default=ALPHA)
+    p.add_argument("--fused", type=int, default=1)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    return p.parse_args()
+
+
+def workload_name(cfg):
+    import gdp_synth as synth
+    return synth.CONFIGS[cfg]["name"]
+
+
+# ------------------------------------------------------------------------------ CPU oracle arm
+def cpu_oracle_step(I0, alpha):
+    import oracle as O
+    I1 = O.diffuse_z(I0, W)
+    O.screened_poisson_slices(I0, I1, alpha)
+
+
+def cpu_sample(cfg):
+    import gdp_synth as synth
+    c = synth.CONFIGS[cfg]
+    return synth.make_stack(min(SAMPLE["nx"], c["nx"]), min(SAMPLE["ny"], c["ny"]), min(SAMPLE["nz"], c["nz"]),
+                            c["seed"], c["dtype"])
+
+
+def sample_desc(I0):
+    nz, ny, nx = I0.shape
+    return (f"oracle (numpy fp64 CG to 1e-10, both phases) on a {nx}x{ny}x{nz} crop of the config "
+            f"generator (seed kept); smaller systems need fewer CG iterations, so the CPU rate is optimistic")
+
+
+def run_cpu_baseline(cfg, alpha, steps=1):
+    from threadpoolctl import threadpool_limits
+    I0 = cpu_sample(cfg)
+    with threadpool_limits(1):
+        ts = []
+        for _ in range(steps):
+            t = time.perf_counter()
+            cpu_oracle_step(I0, alpha)
+            ts.append(time.perf_counter() - t)
+    return I0, ts
+
+
+def reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from threadpoolctl import threadpool_limits
+    I0 = cpu_sample(args.config)
+    with threadpool_limits(1):
+        for _ in range(args.warmup):
+            cpu_oracle_step(I0, args.alpha)
+        t = time.perf_counter()
+        for _ in range(args.steps):
+            cpu_oracle_step(I0, args.alpha)
+        el = time.perf_counter() - t
+    nvox = I0.size
+    val = nvox * args.steps / el
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": workload_name(args.config) + "_cpu_sample",
+                                            "sample_dims": list(I0.shape[::-1]), "alpha": args.alpha},
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample_desc(I0)},
+            "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------------------ clocks
+class ClockSampler:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+        self.th = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-i", str(self.index), "-lms", "200"], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.th = threading.Thread(target=self._read, daemon=True)
+        self.th.start()
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------ our arm
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+def ncu_traffic(kernel_class):
+    """dram bytes per launch of the dominant kernel from the committed ncu --set full summary."""
+    p = os.path.join(ROOT, "profiles", "ncu_full_summary.json")
+    try:
+        d = json.load(open(p))
+        return d.get(kernel_class, {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return reference_arm(args)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import gdp_synth as synth
+    import paper_1310_0041_b200 as gdp
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus and world > 1:
+        print(f"warning: WORLD_SIZE={world} != --gpus {args.gpus}", file=sys.stderr)
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    c = synth.CONFIGS[args.config]
+    nx, ny, nz = c["nx"], c["ny"], c["nz"]
+    # independent per-rank stacks (weak scaling): rank r uses seed + 1000 r; rank 0 = config
+    I0_host = synth.make_stack(nx, ny, nz, c["seed"] + 1000 * rank, c["dtype"])
+    I0 = torch.from_numpy(I0_host).cuda()
+    I1 = torch.empty(I0.shape, dtype=torch.float32, device="cuda")
+    I2 = torch.empty(I0.shape, dtype=torch.float32, device="cuda")
+    ctx = gdp.Ctx(local)
+    opts = gdp.default_opts(fused=args.fused)
+    stream = torch.cuda.Stream()
+    nvox = nx * ny * nz
+
+    def step():
+        return gdp.gdp_destripe(ctx, I0, alpha=args.alpha, W=W, I1=I1, I2=I2, opts=opts, stream=stream)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    with torch.cuda.stream(stream):
+        for _ in range(max(args.warmup, 0)):
+            r = step()
+    torch.cuda.synchronize()
+    cycles = (r[2]["vcycles"], r[3]["vcycles"]) if args.warmup > 0 else None
+
+    clk = ClockSampler(local)
+    barrier()
+    torch.cuda.synchronize()
+    clk.start()
+    launches0 = gdp.kernel_launch_count()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    reps = []
+    e0.record(stream)
+    for _ in range(args.steps):
+        reps.append(step())
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clocks = clk.stop()
+    launches = gdp.kernel_launch_count() - launches0
+    ms = e0.elapsed_time(e1)
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = nvox * world * args.steps / (ms_max * 1e-3)
+    conv = [(r[2]["vcycles"], r[3]["vcycles"], r[2]["rel_res"][-1], r[3]["rel_res"][-1]) for r in reps]
+    status_ok = all(r[2]["status"] == "GDP_OK" and r[3]["status"] == "GDP_OK" for r in reps)
+
+    # --- per-kernel-class profile of the same steps (separate pass, same stream) ----------
+    gdp.profile_begin()
+    with torch.cuda.stream(stream):
+        for _ in range(args.steps):
+            step()
+    torch.cuda.synchronize()
+    stats = gdp.profile_end()
+    tot_ms = sum(s["ms"] for s in stats) or 1.0
+    dom = max(stats, key=lambda s: s["ms"])
+    pk = peaks()
+    peak = pk.get("hbm_gbs")
+    achieved = dom["alg_bytes"] / (dom["ms"] * 1e-3) / 1e9
+    roofline = {"bound": "hbm", "kernel": dom["name"], "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": (achieved / peak) if peak else None,
+                "traffic": ncu_traffic(dom["name"]),
+                "alg_bytes_per_launch": dom["alg_bytes"] / dom["launches"],
+                "avg_launch_ms": dom["ms"] / dom["launches"], "share_of_kernel_time": dom["ms"] / tot_ms,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs (torch copy, burst)" if peak else "missing",
+                "kernels": {s["name"]: {"launches": s["launches"], "ms": round(s["ms"], 4),
+                                        "GBps": round(s["alg_bytes"] / max(s["ms"], 1e-9) / 1e6, 1)}
+                            for s in stats}}
+    whole_gbs = sum(s["alg_bytes"] for s in stats) / (tot_ms * 1e-3) / 1e9
+
+    # --- end to end through the host-buffer C entry (pinned host I0 -> host I2) -------------
+    e2e = None
+    if not args.no_e2e:
+        I0_pin = torch.from_numpy(I0_host).pin_memory()
+        I2_pin = torch.empty(I0.shape, dtype=torch.float32).pin_memory()
+        gdp.gdp_destripe_host(ctx, I0_pin, I2_pin, alpha=args.alpha, W=W, opts=opts)  # warm
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            gdp.gdp_destripe_host(ctx, I0_pin, I2_pin, alpha=args.alpha, W=W, opts=opts)
+        torch.cuda.synchronize()
+        el = time.perf_counter() - t0
+        te = torch.tensor([el], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": nvox * world * args.steps / float(te.item()), "unit": UNIT,
+               "h2d_bytes_per_step": int(I0_pin.numel() * I0_pin.element_size()),
+               "d2h_bytes_per_step": int(I2_pin.numel() * I2_pin.element_size()),
+               "timing": "host wall clock around gdp_destripe_host (blocking), max over ranks"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        I0s, ts = run_cpu_baseline(args.config, args.alpha)
+        cpu = {"value": I0s.size / ts[0], "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample_desc(I0s)}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": {"workload": c["name"], "dims": [nx, ny, nz], "input": c["dtype"], "alpha": args.alpha,
+                           "W": list(W), "rel_tol": 1e-6, "nu": [opts.nu_pre, opts.nu_post],
+                           "schedule": "fused" if args.fused else "reference",
+                           "l2": "working set > L2 (I0 134 MB + three 537 MB fp32 volumes); no flush",
+                           "parallelism": f"independent stacks x{world}"},
+                "vcycles": {"phase1": conv[0][0], "phase2": conv[0][1], "rel_res_phase1": conv[0][2],
+                            "rel_res_phase2_max_slice": conv[0][3], "all_converged": status_ok},
+                "roofline": roofline, "whole_step_alg_GBps": whole_gbs,
+                "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+                "gpu_launches_per_step": launches / max(args.steps, 1), "clocks": clocks}
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -169,6 +169,20 @@ int gdp_residual(gdp_ctx* ctx, const float* x, const float* b, float* r, gdp_dim
                  int64_t z0_global, int64_t nz_global, gdp_weights W, float alpha,
                  double* norm2_r, double* norm2_b, void* stream);
 
+/* Per-kernel-class device timing (roofline measurement, bench.py).  Between begin and end
+ * every library launch is bracketed by CUDA events on its own stream and tagged with the
+ * algorithmic bytes it must move.  end() synchronises the
+ * recorded events, fills up to `max` entries of `out` (one per kernel class that ran) and
+ * sets *n_out.  Process-wide; not thread-safe against concurrent solves.               */
+typedef struct {
+  char name[32];        /* kernel class, e.g. "rbgs", "down2d"                          */
+  int64_t launches;
+  double ms;            /* summed device time of those launches                        */
+  double alg_bytes;     /* summed algorithmic bytes of those launches                   */
+} gdp_kernel_stat;
+int gdp_profile_begin(void);
+int gdp_profile_end(gdp_kernel_stat* out, int max, int* n_out);
+
 /* Thread-local message of the last failing call on this thread ("" if none). */
 const char* gdp_last_error(void);
 

@@ -15,5 +15,7 @@ from .gdp import (  # noqa: F401
     gdp_screened_poisson_slices,
     gdp_vcycle,
     kernel_launch_count,
+    profile_begin,
+    profile_end,
     version,
 )

@@ -21,6 +21,7 @@ EXPORTS = [
     "gdp_opts_default", "gdp_ctx_create", "gdp_ctx_create_loopback", "gdp_ctx_destroy",
     "gdp_diffuse_z", "gdp_screened_poisson_slices", "gdp_destripe", "gdp_destripe_host",
     "gdp_vcycle", "gdp_residual", "gdp_last_error", "gdp_version", "gdp_kernel_launch_count",
+    "gdp_profile_begin", "gdp_profile_end",
 ]
 
 
@@ -50,6 +51,11 @@ class Report(C.Structure):
                 "rel_res": [self.rel_res[i] for i in range(k + 1)], "norm_b": self.norm_b,
                 "seconds": self.seconds, "hbm_bytes_est": self.hbm_bytes_est,
                 "kernel_launches": self.kernel_launches}
+
+
+class KernelStat(C.Structure):
+    _fields_ = [("name", C.c_char * 32), ("launches", C.c_int64), ("ms", C.c_double),
+                ("alg_bytes", C.c_double)]
 
 
 _lib = None
@@ -82,6 +88,8 @@ def lib():
         "gdp_last_error": ([], C.c_char_p),
         "gdp_version": ([], C.c_char_p),
         "gdp_kernel_launch_count": ([], i64),
+        "gdp_profile_begin": ([], i32),
+        "gdp_profile_end": ([P(KernelStat), i32, P(i32)], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)

@@ -52,13 +52,23 @@ struct RhsK {
   int vmode;         // 0: no value term, 1: V = I (decoded), 2: V = float array
 };
 
+// a1: u8 -> u8/255 rounded to fp32 exactly as IEEE division would (the value the oracle
+// decodes).  q = u*(1/255) can be off by one ulp; one FMA residual correction restores the
+// correctly rounded quotient for every u in [0,255] (verified exhaustively, tests/).
+__device__ __forceinline__ float decode_u8(unsigned int u) {
+  const float f = (float)u;
+  const float r = 1.0f / 255.0f;
+  const float q = f * r;
+  const float e = __fmaf_rn(-q, 255.0f, f);
+  return __fmaf_rn(e, r, q);
+}
+
 template <typename T> __device__ __forceinline__ float ldI(const void* p, long long i);
 template <> __device__ __forceinline__ float ldI<float>(const void* p, long long i) {
   return __ldg(static_cast<const float*>(p) + i);
 }
 template <> __device__ __forceinline__ float ldI<uint8_t>(const void* p, long long i) {
-  // a1: u8 -> u8/255 correctly rounded (IEEE division), the exact value the oracle decodes.
-  return __fdiv_rn((float)__ldg(static_cast<const uint8_t*>(p) + i), 255.f);
+  return decode_u8(__ldg(static_cast<const uint8_t*>(p) + i));
 }
 
 // Neighbour values of x around cell c.  Where a link does not exist the loader sets
@@ -82,58 +92,60 @@ __device__ __forceinline__ Coef coefs(const LevelK& L, int ix, int iy, long long
   return c;
 }
 
-// Residual r = b - A x at one cell, difference form: every link
-// contributes coefficient * ((I_c - I_n) - (x_c - x_n)) so that fp32 cancellation acts
-// on small differences.  `bval` (optional) receives b at the cell (for ||b||).
+// the arithmetic of rhs_g on values already loaded (fused kernels call this directly)
+__device__ __forceinline__ float rhs_from(const Coef& k, float Ic, float Iw, float Ie, float Is,
+                                          float In, float Vc, float av) {
+  float g = k.xl * (Ic - Iw);
+  g = __fmaf_rn(k.xr, Ic - Ie, g);
+  g = __fmaf_rn(k.yl, Ic - Is, g);
+  g = __fmaf_rn(k.yr, Ic - In, g);
+  return __fmaf_rn(av, Vc, g);
+}
+
+// Right-hand side at one finest-level cell (a2 / a11): b = av V - div W G with the
+// in-plane target gradient G = forward differences of I (Eq. 1, Eq. 2):
+//   b_c = sum_{in-plane links} coef * (I_c - I_n)  [+ av V_c]
+template <typename TI>
+__device__ __forceinline__ float rhs_g(const LevelK& L, const RhsK& R, const Coef& k, long long c,
+                                       long long nx) {
+  const float Ic = ldI<TI>(R.I, c);
+  float Iw = Ic, Ie = Ic, Is = Ic, In = Ic;  // absent link: zero difference
+  if (k.xl != 0.f) Iw = ldI<TI>(R.I, c - 1);
+  if (k.xr != 0.f) Ie = ldI<TI>(R.I, c + 1);
+  if (k.yl != 0.f) Is = ldI<TI>(R.I, c - nx);
+  if (k.yr != 0.f) In = ldI<TI>(R.I, c + nx);
+  return rhs_from(k, Ic, Iw, Ie, Is, In, R.vmode == 0 ? 0.f : (R.vmode == 1 ? Ic : __ldg(R.V + c)),
+                  R.av);
+}
+
+// (A x)_c in difference form: alpha x_c + sum_links coef (x_c - x_n).
+__device__ __forceinline__ float apply_from(const Coef& k, float alpha, float xc, float xw, float xe,
+                                            float xs, float xn, float xd, float xu) {
+  float s = alpha * xc;
+  s = __fmaf_rn(k.xl, xc - xw, s);
+  s = __fmaf_rn(k.xr, xc - xe, s);
+  s = __fmaf_rn(k.yl, xc - xs, s);
+  s = __fmaf_rn(k.yr, xc - xn, s);
+  s = __fmaf_rn(k.zl, xc - xd, s);
+  s = __fmaf_rn(k.zr, xc - xu, s);
+  return s;
+}
+
+// Residual r = b - A x at one cell.  Every schedule evaluates exactly this expression.
 template <int MODE, typename TI>
 __device__ __forceinline__ float residual_at(const LevelK& L, const RhsK& R, const Coef& k,
                                              float xc, const Nbr& nb, long long c, long long nx,
                                              long long plane, float* bval) {
-  float r;
-  if (MODE == RHS_B) {
-    float s = L.alpha * xc;
-    s += k.xl * (xc - nb.w);
-    s += k.xr * (xc - nb.e);
-    s += k.yl * (xc - nb.s);
-    s += k.yr * (xc - nb.n);
-    s += k.zl * (xc - nb.d);
-    s += k.zr * (xc - nb.u);
-    const float bc = R.b[c];
-    if (bval) *bval = bc;
-    r = bc - s;
-  } else {
-    const float Ic = ldI<TI>(R.I, c);
-    float Iw = Ic, Ie = Ic, Is = Ic, In = Ic;  // absent link: zero difference
-    if (k.xl != 0.f) Iw = ldI<TI>(R.I, c - 1);
-    if (k.xr != 0.f) Ie = ldI<TI>(R.I, c + 1);
-    if (k.yl != 0.f) Is = ldI<TI>(R.I, c - nx);
-    if (k.yr != 0.f) In = ldI<TI>(R.I, c + nx);
-    float g = 0.f, bb = 0.f;
-    g += k.xl * ((Ic - Iw) - (xc - nb.w));
-    g += k.xr * ((Ic - Ie) - (xc - nb.e));
-    g += k.yl * ((Ic - Is) - (xc - nb.s));
-    g += k.yr * ((Ic - In) - (xc - nb.n));
-    g -= k.zl * (xc - nb.d);
-    g -= k.zr * (xc - nb.u);
-    if (bval) {
-      bb = k.xl * (Ic - Iw) + k.xr * (Ic - Ie) + k.yl * (Ic - Is) + k.yr * (Ic - In);
-    }
-    if (R.vmode != 0) {
-      const float Vc = R.vmode == 1 ? Ic : __ldg(R.V + c);
-      if (R.av == L.alpha) g += L.alpha * (Vc - xc);
-      else g += R.av * Vc - L.alpha * xc;
-      if (bval) bb += R.av * Vc;
-    } else {
-      g -= L.alpha * xc;
-    }
-    if (bval) *bval = bb;
-    r = g;
-  }
-  return r;
+  const float bc = MODE == RHS_B ? R.b[c] : rhs_g<TI>(L, R, k, c, nx);
+  if (bval) *bval = bc;
+  return bc - apply_from(k, L.alpha, xc, nb.w, nb.e, nb.s, nb.n, nb.d, nb.u);
 }
 
 // Gauss-Seidel point update in correction form: x_c <- x_c + r_c / D_c  (H1).
-__device__ __forceinline__ float gs_update(float xc, float r, float D) { return xc + r / D; }
+// invD = correctly rounded 1/D (same in every schedule), x_c + r * invD as one FMA.
+__device__ __forceinline__ float gs_update(float xc, float r, float D) {
+  return __fmaf_rn(r, __frcp_rn(D), xc);
+}
 
 // Cell-centre coordinate (finest-grid units) of cell i on an axis of n cells of width H,
 // the last one of width hl (partial under ceil-halving).

@@ -285,9 +285,11 @@ static void launch_rbgs_t(const LevelK& L, float* x, const float* xlo, const flo
   k_rbgs<MODE, TI><<<grd, blk, 0, s>>>(L, x, xlo, xhi, R, color);
 }
 
+static inline double ncell(const LevelK& L) { return (double)L.nx * L.ny * L.nzl; }
+
 void launch_rbgs(const LevelK& L, float* x, const float* xlo, const float* xhi, const RhsK& R,
                  int mode, int tI, int color, cudaStream_t s) {
-  count_launch();
+  ProfScope ps(KC_RBGS, ncell(L) * (4.0 + rhs_bytes(mode, tI, R) + 2.0), s);
   if (mode == RHS_B) launch_rbgs_t<RHS_B, float>(L, x, xlo, xhi, R, color, s);
   else if (tI == 0) launch_rbgs_t<RHS_G, uint8_t>(L, x, xlo, xhi, R, color, s);
   else launch_rbgs_t<RHS_G, float>(L, x, xlo, xhi, R, color, s);
@@ -306,7 +308,7 @@ static void launch_restrict_t(const LevelK& L, const float* x, const float* xlo,
 void launch_restrict(const LevelK& L, const float* x, const float* xlo, const float* xhi,
                      const RhsK& R, int mode, int tI, const XferAxis& tx, const XferAxis& ty,
                      const XferAxis& tz, int ncx, int ncy, int nczl, float* bc, cudaStream_t s) {
-  count_launch();
+  ProfScope ps(KC_RESTRICT, ncell(L) * (4.0 + rhs_bytes(mode, tI, R)) + 4.0 * ncx * ncy * (double)nczl, s);
   if (mode == RHS_B)
     launch_restrict_t<RHS_B, float>(L, x, xlo, xhi, R, tx, ty, tz, ncx, ncy, nczl, bc, s);
   else if (tI == 0)
@@ -318,7 +320,7 @@ void launch_restrict(const LevelK& L, const float* x, const float* xlo, const fl
 void launch_prolong(const LevelK& L, float* xf, const XferAxis& tx, const XferAxis& ty,
                     const XferAxis& tz, int ncx, int ncy, int nczl, long long cz0, const float* xc,
                     const float* xclo, const float* xchi, cudaStream_t s) {
-  count_launch();
+  ProfScope ps(KC_PROLONG, ncell(L) * 8.0 + 4.0 * ncx * ncy * (double)nczl, s);
   dim3 blk(32, 8);
   dim3 grd((L.nx + 31) / 32, (L.ny + 7) / 8, L.nzl);
   k_prolong<<<grd, blk, 0, s>>>(L, xf, tx, ty, tz, ncx, ncy, nczl, cz0, xc, xclo, xchi);
@@ -341,24 +343,28 @@ static void launch_norms_t(const LevelK& L, const float* x, const float* xlo, co
 void launch_norms(const LevelK& L, const float* x, const float* xlo, const float* xhi,
                   const RhsK& R, int mode, int tI, float* rout, double2* partials,
                   double2* plane_out, cudaStream_t s) {
-  count_launch();
+  {
+  ProfScope ps(KC_NORMS, ncell(L) * (4.0 + rhs_bytes(mode, tI, R) + (rout ? 4.0 : 0.0)), s);
   if (mode == RHS_B) launch_norms_t<RHS_B, float>(L, x, xlo, xhi, R, rout, partials, s);
   else if (tI == 0) launch_norms_t<RHS_G, uint8_t>(L, x, xlo, xhi, R, rout, partials, s);
   else launch_norms_t<RHS_G, float>(L, x, xlo, xhi, R, rout, partials, s);
-  count_launch();
+  }
+  ProfScope ps2(KC_UTIL, 0.0, s);
   k_finalize<<<L.nzl, 256, 0, s>>>(partials, norms_blocks_per_plane(L.nx, L.ny), plane_out);
 }
 
 void launch_plane_sums(const void* a, int ta, const void* b, int tb, int nx, int ny, int nz,
                        double2* partials, double2* plane_out, cudaStream_t s) {
-  count_launch();
+  {
+  ProfScope ps(KC_UTIL, (double)nx * ny * nz * ((ta ? 4 : 1) + (b ? (tb ? 4 : 1) : 0)), s);
   dim3 blk(128, 2);
   dim3 grd = grid_plane(nx, ny, nz, blk, 32);
   if (ta == 1 && tb == 0) k_plane_sums<float, uint8_t><<<grd, blk, 0, s>>>(a, b, nx, ny, partials);
   else if (ta == 1) k_plane_sums<float, float><<<grd, blk, 0, s>>>(a, b, nx, ny, partials);
   else if (tb == 0) k_plane_sums<uint8_t, uint8_t><<<grd, blk, 0, s>>>(a, b, nx, ny, partials);
   else k_plane_sums<uint8_t, float><<<grd, blk, 0, s>>>(a, b, nx, ny, partials);
-  count_launch();
+  }
+  ProfScope ps2(KC_UTIL, 0.0, s);
   k_finalize<<<nz, 256, 0, s>>>(partials, norms_blocks_per_plane(nx, ny), plane_out);
 }
 
@@ -368,18 +374,18 @@ static inline int ew_grid(long long n) {
 }
 
 void launch_decode_copy(const void* I, int tI, float* x, long long n, cudaStream_t s) {
-  count_launch();
+  ProfScope ps(KC_UTIL, (double)n * (tI ? 8.0 : 5.0), s);
   if (tI == 0) k_decode_copy<uint8_t><<<ew_grid(n), 256, 0, s>>>(I, x, n);
   else k_decode_copy<float><<<ew_grid(n), 256, 0, s>>>(I, x, n);
 }
 
 void launch_add_scalar(float* x, long long n, float v, cudaStream_t s) {
-  count_launch();
+  ProfScope ps(KC_UTIL, (double)n * 8.0, s);
   k_add_scalar<<<ew_grid(n), 256, 0, s>>>(x, n, v);
 }
 
 void launch_axpy(float* x, const float* e, long long n, cudaStream_t s) {
-  count_launch();
+  ProfScope ps(KC_UTIL, (double)n * 12.0, s);
   k_axpy<<<ew_grid(n), 256, 0, s>>>(x, e, n);
 }
 
@@ -389,8 +395,9 @@ size_t coarse_smem_bytes(const CoarseK& C) {
 }
 
 cudaError_t launch_coarse(const CoarseK& C, const float* b, float* x, cudaStream_t s) {
-  count_launch();
   const size_t smem = coarse_smem_bytes(C);
+  // b read + x write of every coarsest system
+  ProfScope ps(KC_COARSE, 8.0 * (double)C.nx * C.ny * C.nz, s);
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(k_coarse_fd, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);

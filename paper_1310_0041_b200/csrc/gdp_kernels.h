@@ -13,6 +13,33 @@ namespace gdp {
 extern std::atomic<long long> g_launches;
 inline void count_launch(long long n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
+// Per-kernel-class device timing for the bench's roofline (gdp_profile_begin/end).  When
+// enabled, each launch is bracketed by two events on its own stream and tagged with the
+// algorithmic bytes it must move.  Disabled: no cost.
+enum KClass {
+  KC_RBGS = 0, KC_RESTRICT, KC_PROLONG, KC_NORMS, KC_COARSE, KC_UTIL,
+  KC_DOWN2D, KC_UP2D, KC_DOWN3D, KC_UP3D, KC_COUNT
+};
+extern const char* kclass_name[KC_COUNT];
+extern bool g_prof_on;
+void prof_push(int cls, double bytes, cudaStream_t s, bool begin);
+struct ProfScope {
+  int cls;
+  cudaStream_t s;
+  ProfScope(int c, double bytes, cudaStream_t st) : cls(c), s(st) {
+    count_launch();
+    if (g_prof_on) prof_push(cls, bytes, s, true);
+  }
+  ~ProfScope() {
+    if (g_prof_on) prof_push(cls, 0.0, s, false);
+  }
+};
+// bytes per cell of the finest-level rhs inputs (u8/f32 I, optional fp32 V) or of b
+inline double rhs_bytes(int mode, int tI, const RhsK& R) {
+  if (mode == RHS_B) return 4.0;
+  return (tI == 0 ? 1.0 : 4.0) + (R.vmode == 2 ? 4.0 : 0.0);
+}
+
 // fp64 block reduction of two values (warp shuffle, then shared memory); result valid in
 // thread (0,0).  Fixed order -> deterministic.
 __device__ __forceinline__ void block_sum2(double& a, double& b) {

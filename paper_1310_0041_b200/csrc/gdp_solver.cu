@@ -25,6 +25,30 @@ namespace gdp {
 
 std::atomic<long long> g_launches{0};
 
+// ---------------------------------------------------------------------------------
+// per-kernel-class profiler
+// ---------------------------------------------------------------------------------
+const char* kclass_name[KC_COUNT] = {"rbgs", "restrict", "prolong", "norms", "coarse", "util",
+                                     "down2d", "up2d", "down3d", "up3d"};
+bool g_prof_on = false;
+struct ProfRec { int cls; double bytes; cudaEvent_t a, b; };
+static std::vector<ProfRec> g_prof;
+static std::vector<int> g_prof_open;  // stack of open records
+
+void prof_push(int cls, double bytes, cudaStream_t s, bool begin) {
+  if (begin) {
+    ProfRec r{cls, bytes, nullptr, nullptr};
+    cudaEventCreate(&r.a);
+    cudaEventCreate(&r.b);
+    cudaEventRecord(r.a, s);
+    g_prof.push_back(r);
+    g_prof_open.push_back((int)g_prof.size() - 1);
+  } else if (!g_prof_open.empty()) {
+    cudaEventRecord(g_prof[g_prof_open.back()].b, s);
+    g_prof_open.pop_back();
+  }
+}
+
 static thread_local std::string t_err;
 
 int set_err(int code, const char* fmt, ...) {
@@ -749,6 +773,44 @@ int gdp_residual(gdp_ctx* ctx, const float* x, const float* b, float* r, gdp_dim
   RET(comm_allreduce_sum2(C, &rr, &bb, s));
   if (norm2_r) *norm2_r = rr;
   if (norm2_b) *norm2_b = bb;
+  return GDP_OK;
+}
+
+int gdp_profile_begin(void) {
+  for (auto& r : g_prof) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+  g_prof.clear();
+  g_prof_open.clear();
+  g_prof_on = true;
+  return GDP_OK;
+}
+
+int gdp_profile_end(gdp_kernel_stat* out, int max, int* n_out) {
+  g_prof_on = false;
+  double ms[KC_COUNT] = {0}, by[KC_COUNT] = {0};
+  long long n[KC_COUNT] = {0};
+  for (auto& r : g_prof) {
+    float t = 0.f;
+    CK(cudaEventSynchronize(r.b));
+    CK(cudaEventElapsedTime(&t, r.a, r.b));
+    ms[r.cls] += t;
+    by[r.cls] += r.bytes;
+    n[r.cls] += 1;
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  g_prof.clear();
+  int k = 0;
+  for (int c = 0; c < KC_COUNT; ++c) {
+    if (!n[c]) continue;
+    if (out && k < max) {
+      std::snprintf(out[k].name, sizeof out[k].name, "%s", kclass_name[c]);
+      out[k].launches = n[c];
+      out[k].ms = ms[c];
+      out[k].alg_bytes = by[c];
+    }
+    ++k;
+  }
+  if (n_out) *n_out = std::min(k, max);
   return GDP_OK;
 }
 

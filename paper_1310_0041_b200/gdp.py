@@ -188,6 +188,20 @@ def gdp_residual(ctx: Ctx, x: torch.Tensor, b: torch.Tensor, r: torch.Tensor | N
     return r, nr.value, nb.value
 
 
+def profile_begin() -> None:
+    """Start per-kernel-class device timing (gdp_profile_begin)."""
+    _check(L.lib().gdp_profile_begin(), "gdp_profile_begin")
+
+
+def profile_end() -> list[dict]:
+    """Stop timing; returns [{name, launches, ms, alg_bytes}] per kernel class."""
+    arr = (L.KernelStat * 32)()
+    n = C.c_int()
+    _check(L.lib().gdp_profile_end(arr, 32, C.byref(n)), "gdp_profile_end")
+    return [{"name": arr[i].name.decode(), "launches": arr[i].launches, "ms": arr[i].ms,
+             "alg_bytes": arr[i].alg_bytes} for i in range(n.value)]
+
+
 def kernel_launch_count() -> int:
     return int(L.lib().gdp_kernel_launch_count())
 

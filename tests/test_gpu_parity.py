@@ -42,6 +42,16 @@ def _rel_sp(I0, I1, I2_gpu, alpha):
     return O.slice_rel_residuals(I2_gpu, b, alpha).max()
 
 
+# ------------------------------------------------------------------ a1 decode
+def test_u8_decode_is_ieee_division(gpu_ctx):
+    """rel_tol = 1e30 returns x0 = decode(I0) untouched (the mean pin shift is exactly 0)."""
+    u = np.arange(256, dtype=np.uint8).reshape(1, 1, 256)
+    I1, rep = gdp.gdp_diffuse_z(gpu_ctx, dev(u), opts=gdp.default_opts(rel_tol=1e30))
+    assert rep["vcycles"] == 0
+    exp = np.arange(256, dtype=np.float32) / np.float32(255.0)
+    assert np.array_equal(I1.cpu().numpy().ravel(), exp)
+
+
 # ------------------------------------------------------------------ residual kernel
 @pytest.mark.parametrize("shape,W,alpha", [((7, 33, 45), (1.0, 1.0, 0.1), 0.0),
                                            ((3, 64, 64), (0.5, 2.0, 0.3), 0.25),

@@ -95,7 +95,7 @@ __device__ __forceinline__ Coef coefs(const LevelK& L, int ix, int iy, long long
 // the arithmetic of rhs_g on values already loaded (fused kernels call this directly)
 __device__ __forceinline__ float rhs_from(const Coef& k, float Ic, float Iw, float Ie, float Is,
                                           float In, float Vc, float av) {
-  float g = k.xl * (Ic - Iw);
+  float g = __fmul_rn(k.xl, Ic - Iw);
   g = __fmaf_rn(k.xr, Ic - Ie, g);
   g = __fmaf_rn(k.yl, Ic - Is, g);
   g = __fmaf_rn(k.yr, Ic - In, g);
@@ -121,7 +121,7 @@ __device__ __forceinline__ float rhs_g(const LevelK& L, const RhsK& R, const Coe
 // (A x)_c in difference form: alpha x_c + sum_links coef (x_c - x_n).
 __device__ __forceinline__ float apply_from(const Coef& k, float alpha, float xc, float xw, float xe,
                                             float xs, float xn, float xd, float xu) {
-  float s = alpha * xc;
+  float s = __fmul_rn(alpha, xc);
   s = __fmaf_rn(k.xl, xc - xw, s);
   s = __fmaf_rn(k.xr, xc - xe, s);
   s = __fmaf_rn(k.yl, xc - xs, s);
@@ -138,7 +138,7 @@ __device__ __forceinline__ float residual_at(const LevelK& L, const RhsK& R, con
                                              long long plane, float* bval) {
   const float bc = MODE == RHS_B ? R.b[c] : rhs_g<TI>(L, R, k, c, nx);
   if (bval) *bval = bc;
-  return bc - apply_from(k, L.alpha, xc, nb.w, nb.e, nb.s, nb.n, nb.d, nb.u);
+  return __fsub_rn(bc, apply_from(k, L.alpha, xc, nb.w, nb.e, nb.s, nb.n, nb.d, nb.u));
 }
 
 // Gauss-Seidel point update in correction form: x_c <- x_c + r_c / D_c  (H1).
@@ -169,6 +169,18 @@ __device__ __forceinline__ float rweight(const XferAxis& a, long long i) {
   const float h1 = (c1 < a.nf) ? ((c1 == a.nf - 1) ? a.hlf : a.Hf) : 0.f;
   const float hi = (i == c0) ? h0 : h1;
   return hi / (h0 + h1);
+}
+
+// child weight product of the restriction (explicit rounding, same in every schedule)
+__device__ __forceinline__ float rw3(float wz, float wy, float wx) {
+  return __fmul_rn(__fmul_rn(wz, wy), wx);
+}
+
+// bilinear combination of the prolongation (explicit rounding, same in every schedule)
+__device__ __forceinline__ float bilerp(float a, float b, float c, float d, float tx, float ty) {
+  const float r0 = __fmaf_rn(tx, b, __fmul_rn(1.f - tx, a));
+  const float r1 = __fmaf_rn(tx, d, __fmul_rn(1.f - tx, c));
+  return __fmaf_rn(ty, r1, __fmul_rn(1.f - ty, r0));
 }
 
 // Linear prolongation taps of fine cell i: parent I with weight 1-t, neighbour J with t.

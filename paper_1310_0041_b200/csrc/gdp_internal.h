@@ -30,6 +30,7 @@ struct Level {
   float* x = nullptr;            // solution / correction (level 0: caller's buffer)
   bool own_x = false;
   float* b = nullptr;            // restricted residual (levels >= 1)
+  float* x2 = nullptr;           // second x buffer of the fused passes (down A -> B, up B -> A)
   float* xlo = nullptr;          // ghost planes of x for distributed slabs
   float* xhi = nullptr;
 };
@@ -53,6 +54,8 @@ struct Hier {
   double2* plane_sums = nullptr;   // per-plane (sum a, sum b), device
   double2* h_plane = nullptr;      // pinned host mirror
   float* scratch_e = nullptr;      // single-level direct solve correction
+  size_t partials_cap = 0;         // entries of `partials` per plane
+  int up_norm_per = 0;             // >0: the last fused up pass left per-plane partials (this many per plane)
   ~Hier();
 };
 
@@ -91,10 +94,12 @@ int solve(Ctx& ctx, Hier& H, const Fine& f, const gdp_opts& o, bool per_slice, g
 double hbm_model(const Hier& H, double s_I, double s_V, int vcycles);
 
 // fused schedule (gdp_fused.cu): return true if the pass was handled
-bool fused_down(const Level& L, const Level& C, float* x, const RhsK& R, int mode, int tI, int nu,
-                cudaStream_t s);
-bool fused_up(const Level& L, const Level& C, float* x, const RhsK& R, int mode, int tI, int nu,
-              cudaStream_t s);
+bool fusable2d(const Level& L, const Level& C, const gdp_opts& o);
+void fused_down2d(const Level& L, const Level& C, const float* xin, float* xout, const RhsK& R,
+                  int mode, int tI, int nu, bool zero_x, cudaStream_t s);
+void fused_up2d(const Level& L, const Level& C, const float* xin, float* xout, const RhsK& R,
+                int mode, int tI, int nu, double2* partials, cudaStream_t s);
+int fused_tiles_per_plane(int nu, const LevelK& L);
 
 // communication (gdp_comm.cu); single-rank contexts make these no-ops
 int comm_init(Ctx& c, const void* nccl_unique_id);

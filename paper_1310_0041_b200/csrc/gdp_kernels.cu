@@ -73,7 +73,7 @@ __global__ void __launch_bounds__(256) k_restrict(LevelK L, const float* __restr
         const float xc = x[c];
         const Nbr nb = load_nbr(x, xlo, xhi, L, k, fz, c, xc);
         const float r = residual_at<MODE, TI>(L, R, k, xc, nb, c, L.nx, plane, nullptr);
-        acc += (wz * wy * wx) * r;
+        acc = __fmaf_rn(rw3(wz, wy, wx), r, acc);
       }
     }
   }
@@ -106,16 +106,12 @@ __global__ void __launch_bounds__(256) k_prolong(LevelK L, float* __restrict__ x
   const float* pI = zrow(Iz);
   const float* pJ = zrow(Jz);
   auto bil = [&](const float* p) {
-    const float a = p[Iy * ncx + Ix], b = p[Iy * ncx + Jx];
-    const float c = p[Jy * ncx + Ix], d = p[Jy * ncx + Jx];
-    const float r0 = (1.f - txw) * a + txw * b;
-    const float r1 = (1.f - txw) * c + txw * d;
-    return (1.f - tyw) * r0 + tyw * r1;
+    return bilerp(p[Iy * ncx + Ix], p[Iy * ncx + Jx], p[Jy * ncx + Ix], p[Jy * ncx + Jx], txw, tyw);
   };
   float e = bil(pI);
-  if (tzw != 0.f) e = (1.f - tzw) * e + tzw * bil(pJ);
+  if (tzw != 0.f) e = __fmaf_rn(tzw, bil(pJ), __fmul_rn(1.f - tzw, e));
   const long long f = (long long)fz * L.nx * L.ny + (long long)fy * L.nx + fx;
-  xf[f] += e;
+  xf[f] = __fadd_rn(xf[f], e);
 }
 
 // a5: residual r = b - A x with per-block fp64 partial sums of r^2 and b^2 (one row of
@@ -366,6 +362,11 @@ void launch_plane_sums(const void* a, int ta, const void* b, int tb, int nx, int
   }
   ProfScope ps2(KC_UTIL, 0.0, s);
   k_finalize<<<nz, 256, 0, s>>>(partials, norms_blocks_per_plane(nx, ny), plane_out);
+}
+
+void launch_finalize(const double2* partials, int per, int nplanes, double2* out, cudaStream_t s) {
+  ProfScope ps(KC_UTIL, 0.0, s);
+  k_finalize<<<nplanes, 256, 0, s>>>(partials, per, out);
 }
 
 static inline int ew_grid(long long n) {

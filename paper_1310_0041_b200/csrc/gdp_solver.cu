@@ -216,6 +216,7 @@ Hier::~Hier() {
   for (auto& L : lv) {
     if (L.own_x && L.x) cudaFree(L.x);
     if (L.b) cudaFree(L.b);
+    if (L.x2) cudaFree(L.x2);
     if (L.xlo) cudaFree(L.xlo);
     if (L.xhi) cudaFree(L.xhi);
   }
@@ -332,7 +333,9 @@ int build_hier(const HierKey& key, std::unique_ptr<Hier>& out) {
     return set_err(GDP_EINVAL, "coarsest system of %lld unknowns exceeds shared memory", nsys);
   H->coarse = C;
   // norm partials: level-0 plane rows
-  const int per = norms_blocks_per_plane(H->lv[0].nx, H->lv[0].ny);
+  int per = norms_blocks_per_plane(H->lv[0].nx, H->lv[0].ny);
+  for (int nu = 1; nu <= 2; ++nu) per = std::max(per, fused_tiles_per_plane(nu, H->lv[0].K));
+  H->partials_cap = (size_t)per;
   CK(cudaMalloc(&H->partials, (size_t)per * std::max<long long>(maxplanes, 1) * sizeof(double2)));
   CK(cudaMalloc(&H->plane_sums, (size_t)std::max<long long>(maxplanes, 1) * sizeof(double2)));
   CK(cudaMallocHost(&H->h_plane, (size_t)std::max<long long>(maxplanes, 1) * sizeof(double2)));
@@ -404,7 +407,14 @@ int run_vcycle(Ctx& ctx, Hier& H, const Fine& f, const gdp_opts& o, cudaStream_t
     launch_axpy(f.x, H.scratch_e, (long long)L.nx * L.ny * L.nzl, s);
     return GDP_OK;
   }
-  const bool fused = o.fused != 0;
+  H.up_norm_per = 0;
+  bool fz[GDP_MAX_LEVELS] = {false};
+  for (int l = 0; l < nl - 1; ++l) {
+    Level& L = H.lv[l];
+    Level& C = H.lv[l + 1];
+    fz[l] = fusable2d(L, C, o);
+    if (fz[l] && !L.x2) CK(cudaMalloc(&L.x2, sizeof(float) * (size_t)L.nx * L.ny * L.nzl));
+  }
   for (int l = 0; l < nl - 1; ++l) {
     Level& L = H.lv[l];
     Level& C = H.lv[l + 1];
@@ -415,9 +425,12 @@ int run_vcycle(Ctx& ctx, Hier& H, const Fine& f, const gdp_opts& o, cudaStream_t
       R = RhsK{L.b, nullptr, nullptr, 0.f, 0};
       mode = RHS_B;
       tI = 1;
-      CK(cudaMemsetAsync(x, 0, sizeof(float) * (size_t)L.nx * L.ny * L.nzl, s));
     }
-    if (fused && fused_down(L, C, x, R, mode, tI, o.nu_pre, s)) continue;
+    if (fz[l]) {  // one fused pass: x (A) -> x2 (B)
+      fused_down2d(L, C, x, L.x2, R, mode, tI, o.nu_pre, l > 0, s);
+      continue;
+    }
+    if (l > 0) CK(cudaMemsetAsync(x, 0, sizeof(float) * (size_t)L.nx * L.ny * L.nzl, s));
     smooth(L, x, R, mode, tI, o.nu_pre, s);
     launch_restrict(L.K, x, L.xlo, L.xhi, R, mode, tI, C.tx, C.ty, C.tz, C.nx, C.ny, C.nzl, C.b, s);
   }
@@ -430,7 +443,12 @@ int run_vcycle(Ctx& ctx, Hier& H, const Fine& f, const gdp_opts& o, cudaStream_t
     RhsK R = f.R;
     int mode = f.mode, tI = f.tI;
     if (l > 0) { R = RhsK{L.b, nullptr, nullptr, 0.f, 0}; mode = RHS_B; tI = 1; }
-    if (fused && fused_up(L, C, x, R, mode, tI, o.nu_post, s)) continue;
+    if (fz[l]) {  // one fused pass: x2 (B) -> x (A), norms of the finest level on the way
+      const bool want = l == 0 && (size_t)fused_tiles_per_plane(o.nu_post, L.K) <= H.partials_cap;
+      fused_up2d(L, C, L.x2, x, R, mode, tI, o.nu_post, want ? H.partials : nullptr, s);
+      if (want) H.up_norm_per = fused_tiles_per_plane(o.nu_post, L.K);
+      continue;
+    }
     launch_prolong(L.K, x, C.tx, C.ty, C.tz, C.nx, C.ny, C.nzl, C.z0, C.x, C.xlo, C.xhi, s);
     smooth(L, x, R, mode, tI, o.nu_post, s);
   }
@@ -484,7 +502,13 @@ int solve(Ctx& ctx, Hier& H, const Fine& f, const gdp_opts& o, bool per_slice, g
   while (rel > o.rel_tol) {
     if (k >= cap) { status = GDP_ENOCONV; break; }
     RET(run_vcycle(ctx, H, f, o, s));
-    RET(finest_norms(ctx, H, f, nullptr, s));
+    if (H.up_norm_per > 0) {  // norms of the final iterate came with the fused up pass
+      launch_finalize(H.partials, H.up_norm_per, H.lv[0].nzl, H.plane_sums, s);
+      CK(cudaMemcpyAsync(H.h_plane, H.plane_sums, sizeof(double2) * H.lv[0].nzl, cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+    } else {
+      RET(finest_norms(ctx, H, f, nullptr, s));
+    }
     const double nrel = rel_from_planes(H, per_slice, nullptr);
     ++k;
     r.rel_res[k] = nrel;

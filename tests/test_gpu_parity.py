@@ -182,3 +182,32 @@ def test_report_and_launches(gpu_ctx):
     assert rep["rel_res"][-1] <= 1e-6 and rep["rel_res"][0] > 1e-3
     assert rep["kernel_launches"] > 0 and gdp.kernel_launch_count() - before == rep["kernel_launches"]
     assert rep["seconds"] > 0
+
+
+# ------------------------------------------------------------------ schedules agree bit for bit
+@pytest.mark.parametrize("shape,dtype,alpha", [((3, 130, 260), "u8", 0.01), ((2, 75, 61), "f32", 0.1),
+                                               ((1, 517, 389), "u8", 0.001), ((4, 64, 64), "u8", 0.01),
+                                               ((16, 1024, 1024), "u8", 0.01), ((3, 1031, 777), "f32", 0.01)])
+def test_fused_2d_bit_identical_to_reference(gpu_ctx, shape, dtype, alpha):
+    nz, ny, nx = shape
+    I0 = synth.make_stack(nx, ny, nz, 31, dtype)
+    I1 = dev(O.diffuse_z_dct(I0).astype(np.float32))
+    outs = []
+    for fused in (0, 1):
+        o = gdp.default_opts(fused=fused, max_vcycles=3, rel_tol=1e-30, stagnation=0)
+        I2, rep = gdp.gdp_screened_poisson_slices(gpu_ctx, dev(I0), I1, alpha=alpha, opts=o, check=False)
+        outs.append(I2.cpu().numpy())
+    assert np.array_equal(outs[0], outs[1])
+
+
+def test_fused_2d_vcycle_bit_identical(gpu_ctx):
+    shape = (2, 190, 157)
+    rng = np.random.default_rng(5)
+    b = dev(rng.standard_normal(shape).astype(np.float32))
+    xs = []
+    for fused in (0, 1):
+        x = torch.zeros(shape, dtype=torch.float32, device="cuda")
+        for _ in range(2):
+            gdp.gdp_vcycle(gpu_ctx, x, b, W=(1.0, 0.5, 0.0), alpha=0.05, opts=gdp.default_opts(fused=fused, nu_pre=1, nu_post=3))
+        xs.append(x.cpu().numpy())
+    assert np.array_equal(xs[0], xs[1])

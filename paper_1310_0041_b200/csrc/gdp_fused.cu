@@ -36,10 +36,10 @@ __device__ __forceinline__ void static_for(F&& f) {
 }
 template <int V> using IC = std::integral_constant<int, V>;
 
-constexpr int F2_R = 16;                  // rows per warp
-constexpr int F2_W = 8;                   // warps per CTA (stacked in y)
-constexpr int F2_COLS = 64;               // columns per warp (2 per lane)
-constexpr int F2_ROWS = F2_R * F2_W;      // 128
+constexpr int G_R = 12;                   // rows per warp
+constexpr int G_W = 8;                    // warps per CTA (stacked in y)
+constexpr int G_COLS = 128;               // columns per warp (4 per lane)
+constexpr int G_ROWS = G_R * G_W;         // 96
 constexpr unsigned FULL = 0xffffffffu;
 
 __host__ __device__ constexpr int halo2(int nu) { return ((2 * nu + 1) + 1) & ~1; }
@@ -60,19 +60,34 @@ struct Pass2D {
 
 __device__ __forceinline__ bool col_interior(const AxisC& a, int i) { return i >= 1 && i <= a.n - 3; }
 
-// x-neighbours of column C (static) of a lane holding columns (2l, 2l+1)
-template <int C>
-__device__ __forceinline__ void xnbr(const float (&row)[2], float& w, float& e) {
-  if (C == 0) {
-    w = __shfl_up_sync(FULL, row[1], 1);
-    e = row[1];
-  } else {
-    w = row[0];
-    e = __shfl_down_sync(FULL, row[0], 1);
-  }
+// packed f32x2 arithmetic (FFMA2 / FADD2 / FMUL2 on sm_100a); per component identical to the
+// scalar __fmaf_rn / __fadd_rn / __fmul_rn, and x - y == x + (-y) exactly
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) { return __fadd2_rn(a, make_float2(-b.x, -b.y)); }
+__device__ __forceinline__ float2 f2(float v) { return make_float2(v, v); }
+
+// (A x) on a pack of two cells with regular coefficients (order of apply_from without z terms)
+__device__ __forceinline__ float2 apply2(float2 kx, float2 ky, float2 al, float2 X, float2 W, float2 E,
+                                         float2 S, float2 N) {
+  float2 s = __fmul2_rn(al, X);
+  s = __ffma2_rn(kx, sub2(X, W), s);
+  s = __ffma2_rn(kx, sub2(X, E), s);
+  s = __ffma2_rn(ky, sub2(X, S), s);
+  s = __ffma2_rn(ky, sub2(X, N), s);
+  return s;
 }
 
-// (A x)_c without z links: the terms apply_from() adds for zl = zr = 0 are exact zeros
+// rhs_from() on a pack with regular coefficients
+__device__ __forceinline__ float2 rhs2(float2 kx, float2 ky, float2 I, float2 W, float2 E, float2 S,
+                                       float2 N, float2 V, float2 av) {
+  float2 g = __fmul2_rn(kx, sub2(I, W));
+  g = __ffma2_rn(kx, sub2(I, E), g);
+  g = __ffma2_rn(ky, sub2(I, S), g);
+  g = __ffma2_rn(ky, sub2(I, N), g);
+  return __ffma2_rn(av, V, g);
+}
+
+// (A x)_c without z links, scalar (general path): the terms apply_from() adds for zl = zr = 0
+// are exact zeros
 __device__ __forceinline__ float apply2d(const Coef& k, float alpha, float xc, float xw, float xe,
                                          float xs, float xn) {
   float s = __fmul_rn(alpha, xc);
@@ -83,122 +98,191 @@ __device__ __forceinline__ float apply2d(const Coef& k, float alpha, float xc, f
   return s;
 }
 
-template <typename TI> struct Pair;
-template <> struct Pair<float> {
-  __device__ static __forceinline__ void ld(const void* p, long long i, bool vec, float (&o)[2]) {
-    const float* f = static_cast<const float*>(p) + i;
-    if (vec) { const float2 v = __ldg(reinterpret_cast<const float2*>(f)); o[0] = v.x; o[1] = v.y; }
-    else { o[0] = __ldg(f); o[1] = __ldg(f + 1); }
+__device__ __forceinline__ float2 bilerp2(float2 a, float2 b, float2 c, float2 d) {
+  // bilerp(a, b, c, d, 0.25, 0.25) on a pack
+  const float2 t = f2(0.25f), u = f2(1.f - 0.25f);
+  const float2 r0 = __ffma2_rn(t, b, __fmul2_rn(u, a));
+  const float2 r1 = __ffma2_rn(t, d, __fmul2_rn(u, c));
+  return __ffma2_rn(t, r1, __fmul2_rn(u, r0));
+}
+
+// u8 pair -> exact fp32 values, then decode_u8() on both (packed)
+__device__ __forceinline__ float2 decode2(unsigned int lo, unsigned int hi) {
+  const float2 f = __fadd2_rn(make_float2(__uint_as_float(0x4B000000u | lo), __uint_as_float(0x4B000000u | hi)),
+                              f2(-8388608.0f));
+  const float2 r = f2(1.0f / 255.0f);
+  const float2 q = __fmul2_rn(f, r);
+  const float2 e = __ffma2_rn(make_float2(-q.x, -q.y), f2(255.0f), f);
+  return __ffma2_rn(e, r, q);
+}
+
+// element c (0..3) of a lane's row stored as packs A = (c0, c2), B = (c1, c3)
+template <int C>
+__device__ __forceinline__ float& el(float2& A, float2& B) {
+  if constexpr (C == 0) return A.x;
+  else if constexpr (C == 1) return B.x;
+  else if constexpr (C == 2) return A.y;
+  else return B.y;
+}
+
+// load 4 consecutive values (c0..c3) of a row as packs (A, B); 8-byte aligned base
+__device__ __forceinline__ void ld4f(const float* p, float2& A, float2& B) {
+  const float2 lo = __ldg(reinterpret_cast<const float2*>(p));
+  const float2 hi = __ldg(reinterpret_cast<const float2*>(p) + 1);
+  A = make_float2(lo.x, hi.x);
+  B = make_float2(lo.y, hi.y);
+}
+
+template <typename TI> struct Row4;
+template <> struct Row4<float> {
+  __device__ static __forceinline__ void ld(const void* p, long long i, float2& A, float2& B) {
+    ld4f(static_cast<const float*>(p) + i, A, B);
   }
 };
-template <> struct Pair<uint8_t> {
-  __device__ static __forceinline__ void ld(const void* p, long long i, bool vec, float (&o)[2]) {
-    const uint8_t* u = static_cast<const uint8_t*>(p) + i;
-    if (vec) {
-      const unsigned short v = __ldg(reinterpret_cast<const unsigned short*>(u));
-      o[0] = decode_u8(v & 0xffu); o[1] = decode_u8(v >> 8);
-    } else { o[0] = decode_u8(__ldg(u)); o[1] = decode_u8(__ldg(u + 1)); }
+template <> struct Row4<uint8_t> {
+  __device__ static __forceinline__ void ld(const void* p, long long i, float2& A, float2& B) {
+    const unsigned short* u = reinterpret_cast<const unsigned short*>(static_cast<const uint8_t*>(p) + i);
+    const unsigned int lo = __ldg(u), hi = __ldg(u + 1);
+    A = decode2(lo & 0xffu, hi & 0xffu);
+    B = decode2(lo >> 8, hi >> 8);
   }
 };
 
-template <int NU, bool DOWN, int MODE, typename TI, bool FAST>
-__device__ __forceinline__ void pass2d_body(const Pass2D& P, float2 (&sh_top)[2][F2_W][32],
-                                            float2 (&sh_bot)[2][F2_W][32]) {
+// Row data of one warp row (warp-uniform): link coefficients of the row's y links, whether the
+// row is inside the domain, and whether its coefficients are the regular interior ones.
+struct RowInfo { float yl, yr; int in, dcase; };
+
+template <int NU, bool DOWN, int MODE, typename TI>
+__device__ __forceinline__ void pass2d_body(const Pass2D& P, float4 (&sh_top)[2][G_W][32],
+                                            float4 (&sh_bot)[2][G_W][32], float2 (&sb)[G_W][G_R][2][32],
+                                            RowInfo (&srow)[G_W][G_R + 2], float2 (&sinv)[G_W][4][2][32],
+                                            int tile_x, int tile_y, int tiles_x, int tiles_y) {
   constexpr int H = halo2(NU);
-  constexpr int TXI = F2_COLS - 2 * H, TYI = F2_ROWS - 2 * H;
+  constexpr int TXI = G_COLS - 2 * H, TYI = G_ROWS - 2 * H;
   const LevelK& L = P.L;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int gx0 = blockIdx.x * TXI - H + 2 * lane;    // my even column
-  const int gyw = blockIdx.y * TYI - H + warp * F2_R;  // my first row (even)
+  const int gx0 = tile_x * TXI - H + 4 * lane;    // my first column (even)
+  const int gyw = tile_y * TYI - H + warp * G_R;  // my first row (even)
   const int iz = blockIdx.z;
   const long long zg = L.z0 + iz;
   const long long nx = L.nx;
   const long long pbase = (long long)iz * L.nx * L.ny;
   const float alpha = L.alpha;
-  const bool vec = (L.nx & 1) == 0;  // 8-byte aligned column pairs
+  const float2 al2 = f2(alpha);
 
-  bool cin[2], cint[2];
-  float cxl[2], cxr[2];
+  // ---- per-lane column data, packs A = (c0, c2), B = (c1, c3)
+  bool cin[4];
+  float cxl[4], cxr[4];
 #pragma unroll
-  for (int c = 0; c < 2; ++c) {
+  for (int c = 0; c < 4; ++c) {
     const int gx = gx0 + c;
-    cin[c] = FAST || (gx >= 0 && gx < L.nx);
-    cint[c] = FAST || col_interior(L.ax, gx);
-    cxl[c] = FAST ? L.ax.k : cl(L.ax, gx);
-    cxr[c] = FAST ? L.ax.k : cr(L.ax, gx);
+    cin[c] = gx >= 0 && gx < L.nx;
+    cxl[c] = cl(L.ax, gx);
+    cxr[c] = cr(L.ax, gx);
   }
-  Coef kint;
-  kint.xl = L.ax.k; kint.xr = L.ax.k; kint.yl = L.ay.k; kint.yr = L.ay.k; kint.zl = 0.f; kint.zr = 0.f;
-  const float invDint = __frcp_rn(kint.diag(alpha));  // == the 1/D gs_update forms inside
-
-  auto row_in = [&](int gy) { return FAST || (gy >= 0 && gy < L.ny); };
-  auto coef_at = [&](int c, int gy) {
+  const float2 kxlA = make_float2(cxl[0], cxl[2]), kxrA = make_float2(cxr[0], cxr[2]);
+  const float2 kxlB = make_float2(cxl[1], cxl[3]), kxrB = make_float2(cxr[1], cxr[3]);
+  auto invd = [&](int c, float yl, float yr) {
     Coef k;
-    k.xl = cxl[c]; k.xr = cxr[c];
-    k.yl = FAST ? L.ay.k : cl(L.ay, gy);
-    k.yr = FAST ? L.ay.k : cr(L.ay, gy);
-    k.zl = 0.f; k.zr = 0.f;
-    return k;
+    k.xl = cxl[c]; k.xr = cxr[c]; k.yl = yl; k.yr = yr; k.zl = 0.f; k.zr = 0.f;
+    return __frcp_rn(k.diag(alpha));  // == the 1/D of gs_update
   };
+  // 1/D of my columns for the four row cases: 0 regular (or outside the domain, whose values
+  // never reach it), 1 the first row, 2 the row before the last, 3 the last row
+  {
+    const int ny = L.ay.n;
+    const int rows[4] = {1, 0, ny - 2, ny - 1};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float yl = k == 0 ? L.ay.k : cl(L.ay, rows[k]);
+      const float yr = k == 0 ? L.ay.k : cr(L.ay, rows[k]);
+      sinv[warp][k][0][lane] = make_float2(invd(0, yl, yr), invd(2, yl, yr));
+      sinv[warp][k][1][lane] = make_float2(invd(1, yl, yr), invd(3, yl, yr));
+    }
+  }
+  const bool lane_full = cin[0] && cin[1] && cin[2] && cin[3];
+  const bool vec = (L.nx & 1) == 0;  // rows start 8-byte aligned
 
-  float x[F2_R][2], b[F2_R][2];
+  // ---- per-row data (rows -1 .. G_R of this warp), in shared memory
+  RowInfo(&ri)[G_R + 2] = srow[warp];
+  if (lane < G_R + 2) {
+    const int gy = gyw + lane - 1;
+    RowInfo r;
+    r.yl = cl(L.ay, gy);
+    r.yr = cr(L.ay, gy);
+    r.in = gy >= 0 && gy < L.ny;
+    const int n = L.ay.n;
+    r.dcase = gy == 0 ? 1 : (gy == n - 1 ? 3 : (gy == n - 2 ? 2 : 0));
+    if (!r.in) r.dcase = 0;
+    ri[lane] = r;
+  }
+  __syncwarp();
+
+  float2 A[G_R], B[G_R];  // x of my 12 rows x 4 columns
+  float2(&bs)[G_R][2][32] = sb[warp];
+  auto ld4 = [&](const float* base, long long rowp, bool rin, float2& oA, float2& oB) {
+    if (rin && lane_full && vec) { ld4f(base + rowp, oA, oB); return; }
+    float v[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) v[c] = (rin && cin[c]) ? __ldg(base + rowp + c) : 0.f;
+    oA = make_float2(v[0], v[2]);
+    oB = make_float2(v[1], v[3]);
+  };
   // ---------------------------------------------------------------- load x and rhs
 #pragma unroll
-  for (int j = 0; j < F2_R; ++j) {
+  for (int j = 0; j < G_R; ++j) {
     const int gy = gyw + j;
+    const bool rin = ri[j + 1].in;
     const long long rowp = pbase + (long long)gy * nx + gx0;
-    if (FAST) {
-      if (P.zero_x) { x[j][0] = x[j][1] = 0.f; }
-      else Pair<float>::ld(P.xin, rowp, vec, x[j]);
-      if (MODE == RHS_B) Pair<float>::ld(P.R.b, rowp, vec, b[j]);
-    } else {
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        const bool in = row_in(gy) && cin[c];
-        x[j][c] = (in && !P.zero_x) ? __ldg(P.xin + rowp + c) : 0.f;
-        if (MODE == RHS_B) b[j][c] = in ? __ldg(P.R.b + rowp + c) : 0.f;
-      }
+    if (P.zero_x) { A[j] = B[j] = f2(0.f); }
+    else ld4(P.xin, rowp, rin, A[j], B[j]);
+    if (MODE == RHS_B) {
+      float2 a, b;
+      ld4(P.R.b, rowp, rin, a, b);
+      bs[j][0][lane] = a;
+      bs[j][1][lane] = b;
     }
   }
   if (MODE == RHS_G) {
     // b = rhs_from(...) on a rolling window of I rows (gy-1, gy, gy+1)
-    float Ip[2], Ic[2], In[2];
-    auto ldrow = [&](int gy, float (&o)[2]) {
+    float2 IpA, IpB, IcA, IcB, InA, InB;
+    auto ldrow = [&](int jr, float2& oA, float2& oB) {  // jr = row index - 1 .. G_R
+      const int gy = gyw + jr;
+      const bool rin = ri[jr + 1].in;
       const long long rowp = pbase + (long long)gy * nx + gx0;
-      if (FAST) { Pair<TI>::ld(P.R.I, rowp, vec, o); return; }
+      if (rin && lane_full && vec) { Row4<TI>::ld(P.R.I, rowp, oA, oB); return; }
+      float v[4];
 #pragma unroll
-      for (int c = 0; c < 2; ++c) o[c] = (row_in(gy) && cin[c]) ? ldI<TI>(P.R.I, rowp + c) : 0.f;
+      for (int c = 0; c < 4; ++c) v[c] = (rin && cin[c]) ? ldI<TI>(P.R.I, rowp + c) : 0.f;
+      oA = make_float2(v[0], v[2]);
+      oB = make_float2(v[1], v[3]);
     };
-    ldrow(gyw - 1, Ip);
-    ldrow(gyw, Ic);
+    ldrow(-1, IpA, IpB);
+    ldrow(0, IcA, IcB);
+    const float2 av2 = f2(P.R.av);
 #pragma unroll
-    for (int j = 0; j < F2_R; ++j) {
-      const int gy = gyw + j;
-      ldrow(gy + 1, In);
-      float Vr[2] = {0.f, 0.f};
-      const long long rowp = pbase + (long long)gy * nx + gx0;
-      if (P.R.vmode == 1) { Vr[0] = Ic[0]; Vr[1] = Ic[1]; }
-      else if (P.R.vmode == 2) {
-        if (FAST) Pair<float>::ld(P.R.V, rowp, vec, Vr);
-        else {
-#pragma unroll
-          for (int c = 0; c < 2; ++c) Vr[c] = (row_in(gy) && cin[c]) ? __ldg(P.R.V + rowp + c) : 0.f;
-        }
-      }
-      float Iw[2], Ie[2];
-      xnbr<0>(Ic, Iw[0], Ie[0]);
-      xnbr<1>(Ic, Iw[1], Ie[1]);
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        const Coef k = coef_at(c, gy);
-        const float I0 = Ic[c];
-        const float w = k.xl != 0.f ? Iw[c] : I0, e = k.xr != 0.f ? Ie[c] : I0;
-        const float s = k.yl != 0.f ? Ip[c] : I0, n = k.yr != 0.f ? In[c] : I0;
-        const bool in = row_in(gy) && cin[c];
-        b[j][c] = in ? rhs_from(k, I0, w, e, s, n, Vr[c], P.R.av) : 0.f;
-      }
-#pragma unroll
-      for (int c = 0; c < 2; ++c) { Ip[c] = Ic[c]; Ic[c] = In[c]; }
+    for (int j = 0; j < G_R; ++j) {
+      if (j + 1 < G_R + 1) ldrow(j + 1, InA, InB);
+      const RowInfo r = ri[j + 1];
+      const long long rowp = pbase + (long long)(gyw + j) * nx + gx0;
+      float2 VA = f2(0.f), VB = f2(0.f);
+      if (P.R.vmode == 1) { VA = IcA; VB = IcB; }
+      else if (P.R.vmode == 2) ld4(P.R.V, rowp, r.in != 0, VA, VB);
+      const float up3 = __shfl_up_sync(FULL, IcB.y, 1);    // column -1
+      const float dn0 = __shfl_down_sync(FULL, IcA.x, 1);  // column 4
+      const float2 yl = f2(r.yl), yr = f2(r.yr);
+      // rhs_from(k, Ic, Iw, Ie, Is, In, V, av) per element (absent links have coefficient 0)
+      float2 g = __fmul2_rn(kxlA, sub2(IcA, make_float2(up3, IcB.x)));
+      g = __ffma2_rn(kxrA, sub2(IcA, IcB), g);
+      g = __ffma2_rn(yl, sub2(IcA, IpA), g);
+      g = __ffma2_rn(yr, sub2(IcA, InA), g);
+      bs[j][0][lane] = __ffma2_rn(av2, VA, g);
+      g = __fmul2_rn(kxlB, sub2(IcB, IcA));
+      g = __ffma2_rn(kxrB, sub2(IcB, make_float2(IcA.y, dn0)), g);
+      g = __ffma2_rn(yl, sub2(IcB, IpB), g);
+      g = __ffma2_rn(yr, sub2(IcB, InB), g);
+      bs[j][1][lane] = __ffma2_rn(av2, VB, g);
+      IpA = IcA; IpB = IcB; IcA = InA; IcB = InB;
     }
   }
 
@@ -206,83 +290,112 @@ __device__ __forceinline__ void pass2d_body(const Pass2D& P, float2 (&sh_top)[2]
   if (!DOWN) {
     const long long cplane = (long long)P.ncx * P.ncy;
     const float* xcp = P.xc + (long long)iz * cplane;
-    if (FAST) {
-      // parents of my columns: Ix = gx0/2 (col 0 leans on Ix-1, col 1 on Ix+1), weights 3/4, 1/4
-      const int Ix = gx0 >> 1;
-      const int Jw = (gyw >> 1) - 1;  // first coarse row needed
-      float cv[F2_R / 2 + 2][3];
+    // my columns' parents: Ix0 = gx0/2 (c0, c1) and Ix0+1 (c2, c3); taps from ptaps()
+    const int Ix0 = gx0 >> 1;
+    float tx[4];
+    bool selfJ[4];
 #pragma unroll
-      for (int q = 0; q < F2_R / 2 + 2; ++q) {
-        const float v = __ldg(xcp + (long long)(Jw + q) * P.ncx + Ix);
-        cv[q][1] = v;
-        cv[q][0] = __shfl_up_sync(FULL, v, 1);
-        cv[q][2] = __shfl_down_sync(FULL, v, 1);
+    for (int c = 0; c < 4; ++c) {
+      long long I, J;
+      ptaps(P.tx, gx0 + c, I, J, tx[c]);
+      selfJ[c] = J == I;
+    }
+    const float2 txA = make_float2(tx[0], tx[2]), txB = make_float2(tx[1], tx[3]);
+    const int Jw = (gyw >> 1) - 1;  // first coarse row loaded
+    float2 cv[G_R / 2 + 2][2];      // [q] -> (v0, v1) at (Ix0, Ix0+1) and (vm, vp) at (Ix0-1, Ix0+2)
+#pragma unroll
+    for (int q = 0; q < G_R / 2 + 2; ++q) {
+      const int J = Jw + q;
+      const bool rin = J >= 0 && J < P.ncy;
+      const float* rp = xcp + (long long)J * P.ncx + Ix0;
+      const float v0 = (rin && Ix0 >= 0 && Ix0 < P.ncx) ? __ldg(rp) : 0.f;
+      const float v1 = (rin && Ix0 + 1 >= 0 && Ix0 + 1 < P.ncx) ? __ldg(rp + 1) : 0.f;
+      cv[q][0] = make_float2(v0, v1);
+      cv[q][1] = make_float2(__shfl_up_sync(FULL, v1, 1), __shfl_down_sync(FULL, v0, 1));
+    }
+#pragma unroll
+    for (int j = 0; j < G_R; ++j) {
+      const int gy = gyw + j;
+      long long Iy, Jy;
+      float ty;
+      ptaps(P.ty, gy, Iy, Jy, ty);
+      const int q = (j >> 1) + 1;  // == Iy - Jw
+      const int dq = (int)(Jy - Iy);
+      auto rowJ = [&](int k) { return dq < 0 ? cv[q - 1][k] : (dq > 0 ? cv[q + 1][k] : cv[q][k]); };
+      const float2 r0 = cv[q][0], r1 = cv[q][1], n0 = rowJ(0), n1 = rowJ(1);
+      // pack A = (c0, c2): parents (Ix0, Ix0+1); neighbours c0 -> Ix0-1 | Ix0, c2 -> Ix0 | Ix0+1
+      const float2 aJ = make_float2(selfJ[0] ? r0.x : r1.x, selfJ[2] ? r0.y : r0.x);
+      const float2 cJ = make_float2(selfJ[0] ? n0.x : n1.x, selfJ[2] ? n0.y : n0.x);
+      // pack B = (c1, c3): neighbours c1 -> Ix0+1 | Ix0, c3 -> Ix0+2 | Ix0+1
+      const float2 bJ = make_float2(selfJ[1] ? r0.x : r0.y, selfJ[3] ? r0.y : r1.y);
+      const float2 dJ = make_float2(selfJ[1] ? n0.x : n0.y, selfJ[3] ? n0.y : n1.y);
+      const float2 ty2 = f2(ty), uy2 = f2(1.f - ty);
+      // bilerp(a, b, c, d, tx, ty) per element
+      {
+        const float2 ux = make_float2(1.f - txA.x, 1.f - txA.y);
+        const float2 s0 = __ffma2_rn(txA, aJ, __fmul2_rn(ux, r0));
+        const float2 s1 = __ffma2_rn(txA, cJ, __fmul2_rn(ux, n0));
+        A[j] = __fadd2_rn(A[j], __ffma2_rn(ty2, s1, __fmul2_rn(uy2, s0)));
       }
-#pragma unroll
-      for (int j = 0; j < F2_R; ++j) {
-        const int q = (j >> 1) + 1;
-        const int qn = (j & 1) ? q + 1 : q - 1;
-        // bilerp(a=(Iy,Ix), b=(Iy,Jx), c=(Jy,Ix), d=(Jy,Jx)) as ptaps/bilerp order it
-        x[j][0] = __fadd_rn(x[j][0], bilerp(cv[q][1], cv[q][0], cv[qn][1], cv[qn][0], 0.25f, 0.25f));
-        x[j][1] = __fadd_rn(x[j][1], bilerp(cv[q][1], cv[q][2], cv[qn][1], cv[qn][2], 0.25f, 0.25f));
-      }
-    } else {
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        long long Ix, Jx;
-        float tx;
-        ptaps(P.tx, gx0 + c, Ix, Jx, tx);
-#pragma unroll
-        for (int j = 0; j < F2_R; ++j) {
-          const int gy = gyw + j;
-          if (!(cin[c] && row_in(gy))) continue;
-          long long Iy, Jy;
-          float ty;
-          ptaps(P.ty, gy, Iy, Jy, ty);
-          const float e = bilerp(__ldg(xcp + Iy * P.ncx + Ix), __ldg(xcp + Iy * P.ncx + Jx),
-                                 __ldg(xcp + Jy * P.ncx + Ix), __ldg(xcp + Jy * P.ncx + Jx), tx, ty);
-          x[j][c] = __fadd_rn(x[j][c], e);
-        }
+      {
+        const float2 ux = make_float2(1.f - txB.x, 1.f - txB.y);
+        const float2 s0 = __ffma2_rn(txB, bJ, __fmul2_rn(ux, r0));
+        const float2 s1 = __ffma2_rn(txB, dJ, __fmul2_rn(ux, n0));
+        B[j] = __fadd2_rn(B[j], __ffma2_rn(ty2, s1, __fmul2_rn(uy2, s0)));
       }
     }
   }
 
   // ---------------------------------------------------------------- row exchange
-  float sv[2], nv[2];
+  float2 sA, sB, nA, nB;
   auto exchange = [&](int buf) {
-    sh_top[buf][warp][lane] = make_float2(x[0][0], x[0][1]);
-    sh_bot[buf][warp][lane] = make_float2(x[F2_R - 1][0], x[F2_R - 1][1]);
+    sh_top[buf][warp][lane] = make_float4(A[0].x, A[0].y, B[0].x, B[0].y);
+    sh_bot[buf][warp][lane] = make_float4(A[G_R - 1].x, A[G_R - 1].y, B[G_R - 1].x, B[G_R - 1].y);
     __syncthreads();
-    const float2 s2 = warp > 0 ? sh_bot[buf][warp - 1][lane] : make_float2(x[0][0], x[0][1]);
-    const float2 n2 = warp < F2_W - 1 ? sh_top[buf][warp + 1][lane] : make_float2(x[F2_R - 1][0], x[F2_R - 1][1]);
-    sv[0] = s2.x; sv[1] = s2.y; nv[0] = n2.x; nv[1] = n2.y;
+    const float4 s4 = warp > 0 ? sh_bot[buf][warp - 1][lane]
+                               : make_float4(A[0].x, A[0].y, B[0].x, B[0].y);
+    const float4 n4 = warp < G_W - 1 ? sh_top[buf][warp + 1][lane]
+                                     : make_float4(A[G_R - 1].x, A[G_R - 1].y, B[G_R - 1].x, B[G_R - 1].y);
+    sA = make_float2(s4.x, s4.y); sB = make_float2(s4.z, s4.w);
+    nA = make_float2(n4.x, n4.y); nB = make_float2(n4.z, n4.w);
   };
 
-  // one cell update of column C (static) in row j (static)
-  auto update = [&](auto Cc, auto Jc) {
-    constexpr int C = decltype(Cc)::value;
+  // (A x) of pack PK (0: A, 1: B) in row j: alpha x + sum_links k (x - x_n), apply_from order
+  auto stencil = [&](auto PKc, auto Jc, const RowInfo& r) -> float2 {
+    constexpr int PK = decltype(PKc)::value;
     constexpr int j = decltype(Jc)::value;
-    float w, e;
-    xnbr<C>(x[j], w, e);
-    const float xc = x[j][C];
-    const float s = j > 0 ? x[j - 1][C] : sv[C];
-    const float n = j < F2_R - 1 ? x[j + 1][C] : nv[C];
-    if (FAST) {
-      const float r = __fsub_rn(b[j][C], apply2d(kint, alpha, xc, w, e, s, n));
-      x[j][C] = __fmaf_rn(r, invDint, xc);  // == gs_update(xc, r, D_interior)
+    const float2 yl = f2(r.yl), yr = f2(r.yr);
+    if (PK == 0) {
+      const float2 X = A[j];
+      const float2 W = make_float2(__shfl_up_sync(FULL, B[j].y, 1), B[j].x);
+      const float2 S = j > 0 ? A[j - 1] : sA, N = j < G_R - 1 ? A[j + 1] : nA;
+      float2 s = __fmul2_rn(al2, X);
+      s = __ffma2_rn(kxlA, sub2(X, W), s);
+      s = __ffma2_rn(kxrA, sub2(X, B[j]), s);
+      s = __ffma2_rn(yl, sub2(X, S), s);
+      return __ffma2_rn(yr, sub2(X, N), s);
     } else {
-      const int gy = gyw + j;
-      if (cint[C] && col_interior(L.ay, gy)) {
-        const float r = __fsub_rn(b[j][C], apply2d(kint, alpha, xc, w, e, s, n));
-        x[j][C] = __fmaf_rn(r, invDint, xc);
-      } else if (cin[C] && row_in(gy)) {
-        const Coef k = coef_at(C, gy);
-        const float ww = k.xl != 0.f ? w : xc, ee = k.xr != 0.f ? e : xc;
-        const float ss = k.yl != 0.f ? s : xc, nn = k.yr != 0.f ? n : xc;
-        const float r = __fsub_rn(b[j][C], apply2d(k, alpha, xc, ww, ee, ss, nn));
-        x[j][C] = gs_update(xc, r, k.diag(alpha));
-      }
+      const float2 X = B[j];
+      const float2 E = make_float2(A[j].y, __shfl_down_sync(FULL, A[j].x, 1));
+      const float2 S = j > 0 ? B[j - 1] : sB, N = j < G_R - 1 ? B[j + 1] : nB;
+      float2 s = __fmul2_rn(al2, X);
+      s = __ffma2_rn(kxlB, sub2(X, A[j]), s);
+      s = __ffma2_rn(kxrB, sub2(X, E), s);
+      s = __ffma2_rn(yl, sub2(X, S), s);
+      return __ffma2_rn(yr, sub2(X, N), s);
     }
+  };
+
+  // Gauss-Seidel update of the active pack of row j (out-of-domain cells keep finite values
+  // that never reach the domain: every link leaving it has coefficient 0)
+  auto update = [&](auto PKc, auto Jc) {
+    constexpr int PK = decltype(PKc)::value;
+    constexpr int j = decltype(Jc)::value;
+    const RowInfo r = ri[j + 1];
+    const float2 res = sub2(bs[j][PK][lane], stencil(PKc, Jc, r));
+    const float2 iD = sinv[warp][r.dcase][PK][lane];
+    if (PK == 0) A[j] = __ffma2_rn(res, iD, A[j]);
+    else B[j] = __ffma2_rn(res, iD, B[j]);
   };
 
   // ---------------------------------------------------------------- nu sweeps
@@ -290,141 +403,265 @@ __device__ __forceinline__ void pass2d_body(const Pass2D& P, float2 (&sh_top)[2]
   for (int hs = 0; hs < 2 * NU; ++hs) {
     const int color = hs & 1;
     exchange(hs & 1);
-    const int a0 = (color + gyw + (int)(zg & 1)) & 1;  // active column of row 0
-    if (a0 == 0) static_for<F2_R>([&](auto J) { update(IC<(decltype(J)::value & 1)>{}, J); });
-    else static_for<F2_R>([&](auto J) { update(IC<((decltype(J)::value & 1) ^ 1)>{}, J); });
+    const int a0 = (color + gyw + (int)(zg & 1)) & 1;  // active pack of row 0
+    if (a0 == 0) static_for<G_R>([&](auto J) { update(IC<(decltype(J)::value & 1)>{}, J); });
+    else static_for<G_R>([&](auto J) { update(IC<((decltype(J)::value & 1) ^ 1)>{}, J); });
   }
 
-  // ---------------------------------------------------------------- residual, row pair by row pair
+  // ---------------------------------------------------------------- residual, restriction / norms
   exchange((2 * NU) & 1);
-  const int lx0 = 2 * lane;     // local column of c = 0 (c = 1 shares interior-ness: H even)
-  const int ly0 = warp * F2_R;  // local row of j = 0
-  auto resid = [&](auto Jc, auto Cc) -> float {
-    constexpr int j = decltype(Jc)::value;
-    constexpr int c = decltype(Cc)::value;
-    const int gy = gyw + j;
-    float w, e;
-    xnbr<c>(x[j], w, e);
-    const float xc = x[j][c];
-    const float s = j > 0 ? x[j - 1][c] : sv[c];
-    const float n = j < F2_R - 1 ? x[j + 1][c] : nv[c];
-    if (FAST) return __fsub_rn(b[j][c], apply2d(kint, alpha, xc, w, e, s, n));
-    const Coef k = coef_at(c, gy);
-    const float ww = k.xl != 0.f ? w : xc, ee = k.xr != 0.f ? e : xc;
-    const float ss = k.yl != 0.f ? s : xc, nn = k.yr != 0.f ? n : xc;
-    return (row_in(gy) && cin[c]) ? __fsub_rn(b[j][c], apply2d(k, alpha, xc, ww, ee, ss, nn)) : 0.f;
-  };
-  double sr = 0.0, sb = 0.0;
+  const int lx0 = 4 * lane;     // local column of c = 0
+  const int ly0 = warp * G_R;   // local row of j = 0
+  // interior-ness of column pairs (c0,c1) and (c2,c3) (pairs are even-aligned, H even)
+  const bool pin0 = lx0 >= H && lx0 < G_COLS - H;
+  const bool pin1 = lx0 + 2 >= H && lx0 + 2 < G_COLS - H;
+  double sr = 0.0, sbb = 0.0;
   const long long cplane = (long long)P.ncx * P.ncy;
   float* bcp = DOWN ? P.bc + (long long)iz * cplane : nullptr;
-  const bool xin_tile = lx0 >= H && lx0 < F2_COLS - H;
-  static_for<F2_R / 2>([&](auto JP) {
+  float wx[4];
+  if (DOWN) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) wx[c] = rweight(P.tx, gx0 + c);
+  }
+  static_for<G_R / 2>([&](auto JP) {
     constexpr int j0 = 2 * decltype(JP)::value;
-    float r[2][2];
-    r[0][0] = resid(IC<j0>{}, IC<0>{});
-    r[0][1] = resid(IC<j0>{}, IC<1>{});
-    r[1][0] = resid(IC<j0 + 1>{}, IC<0>{});
-    r[1][1] = resid(IC<j0 + 1>{}, IC<1>{});
+    const RowInfo r0 = ri[j0 + 1], r1 = ri[j0 + 2];
+    const float2 rA0 = sub2(bs[j0][0][lane], stencil(IC<0>{}, IC<j0>{}, r0));
+    const float2 rB0 = sub2(bs[j0][1][lane], stencil(IC<1>{}, IC<j0>{}, r0));
+    const float2 rA1 = sub2(bs[j0 + 1][0][lane], stencil(IC<0>{}, IC<j0 + 1>{}, r1));
+    const float2 rB1 = sub2(bs[j0 + 1][1][lane], stencil(IC<1>{}, IC<j0 + 1>{}, r1));
     const int gy0 = gyw + j0;  // even
-    const bool yin0 = ly0 + j0 >= H && ly0 + j0 < F2_ROWS - H;  // rows j0, j0+1 share it (H even)
+    const bool yin0 = ly0 + j0 >= H && ly0 + j0 < G_ROWS - H;  // rows j0, j0+1 together (H even)
     if (DOWN) {
-      if (FAST) {
-        // volume-weighted child average of 2 x 2 full cells: weight 0.5 * 0.5 each
-        if (xin_tile && yin0) {
-          const float w = rw3(1.f, 0.5f, 0.5f);
-          float acc = 0.f;
-          acc = __fmaf_rn(w, r[0][0], acc);
-          acc = __fmaf_rn(w, r[0][1], acc);
-          acc = __fmaf_rn(w, r[1][0], acc);
-          acc = __fmaf_rn(w, r[1][1], acc);
-          bcp[(long long)(gy0 >> 1) * P.ncx + (gx0 >> 1)] = acc;
+      // volume-weighted child average (fy outer, fx inner as in k_restrict); coarse cells
+      // (Ix0, J) from children (c0, c1) and (Ix0+1, J) from (c2, c3)
+      const int J = gy0 >> 1, I0 = gx0 >> 1;
+      const bool ok0 = yin0 && pin0 && r0.in && gx0 >= 0 && I0 < P.ncx && J < P.ncy;
+      const bool ok1 = yin0 && pin1 && r0.in && gx0 + 2 >= 0 && I0 + 1 < P.ncx && J < P.ncy;
+      if (ok0 || ok1) {
+        const float wy0 = rweight(P.ty, gy0), wy1 = rweight(P.ty, gy0 + 1);
+        const float2 wA0 = make_float2(rw3(1.f, wy0, wx[0]), rw3(1.f, wy0, wx[2]));
+        const float2 wB0 = make_float2(rw3(1.f, wy0, wx[1]), rw3(1.f, wy0, wx[3]));
+        const float2 wA1 = make_float2(rw3(1.f, wy1, wx[0]), rw3(1.f, wy1, wx[2]));
+        const float2 wB1 = make_float2(rw3(1.f, wy1, wx[1]), rw3(1.f, wy1, wx[3]));
+        float2 acc = __ffma2_rn(wA0, rA0, f2(0.f));
+        float2 t = __ffma2_rn(wB0, rB0, acc);
+        acc = make_float2(cin[1] ? t.x : acc.x, cin[3] ? t.y : acc.y);
+        if (r1.in) {
+          acc = __ffma2_rn(wA1, rA1, acc);
+          t = __ffma2_rn(wB1, rB1, acc);
+          acc = make_float2(cin[1] ? t.x : acc.x, cin[3] ? t.y : acc.y);
         }
-      } else {
-#pragma unroll
-        for (int dj = 0; dj < 2; ++dj) {
-          if (P.ty.coarsened && dj == 1) break;  // a coarse row takes both fine rows
-          const int gyr = gy0 + dj;
-          const int J = P.ty.coarsened ? (gyr >> 1) : gyr;
-          const int nyc = P.ty.coarsened ? 2 : 1;
-          if (gyr < 0 || J >= P.ncy || !(xin_tile && yin0)) continue;
-          if (P.tx.coarsened) {
-            const int I = gx0 >> 1;
-            if (gx0 < 0 || I >= P.ncx) continue;
-            float acc = 0.f;
-#pragma unroll
-            for (int dy = 0; dy < 2; ++dy) {
-              if (dy >= nyc || gyr + dy >= L.ny) break;
-              const float wy = rweight(P.ty, gyr + dy);
-#pragma unroll
-              for (int c = 0; c < 2; ++c) {
-                if (gx0 + c >= L.nx) break;
-                acc = __fmaf_rn(rw3(1.f, wy, rweight(P.tx, gx0 + c)), r[dj + dy][c], acc);
-              }
-            }
-            bcp[(long long)J * P.ncx + I] = acc;
-          } else {
-#pragma unroll
-            for (int c = 0; c < 2; ++c) {
-              const int I = gx0 + c;
-              if (I < 0 || I >= P.ncx) continue;
-              float acc = 0.f;
-#pragma unroll
-              for (int dy = 0; dy < 2; ++dy) {
-                if (dy >= nyc || gyr + dy >= L.ny) break;
-                acc = __fmaf_rn(rw3(1.f, rweight(P.ty, gyr + dy), 1.f), r[dj + dy][c], acc);
-              }
-              bcp[(long long)J * P.ncx + I] = acc;
-            }
-          }
-        }
+        float* o = bcp + (long long)J * P.ncx + I0;
+        if (ok0) o[0] = acc.x;
+        if (ok1) o[1] = acc.y;
       }
-    } else if (xin_tile && yin0) {
+    } else if (yin0 && P.partials) {
+      const float2 bA0 = bs[j0][0][lane], bB0 = bs[j0][1][lane];
+      const float2 bA1 = bs[j0 + 1][0][lane], bB1 = bs[j0 + 1][1][lane];
+      const float rr[2][4] = {{rA0.x, rB0.x, rA0.y, rB0.y}, {rA1.x, rB1.x, rA1.y, rB1.y}};
+      const float bv[2][4] = {{bA0.x, bB0.x, bA0.y, bB0.y}, {bA1.x, bB1.x, bA1.y, bB1.y}};
 #pragma unroll
-      for (int dj = 0; dj < 2; ++dj)
+      for (int dj = 0; dj < 2; ++dj) {
+        if (!(dj ? r1.in : r0.in)) continue;
 #pragma unroll
-        for (int c = 0; c < 2; ++c)
-          if (cin[c] && row_in(gy0 + dj)) {
-            sr += (double)r[dj][c] * (double)r[dj][c];
-            sb += (double)b[j0 + dj][c] * (double)b[j0 + dj][c];
+        for (int c = 0; c < 4; ++c)
+          if ((c < 2 ? pin0 : pin1) && cin[c]) {
+            sr += (double)rr[dj][c] * (double)rr[dj][c];
+            sbb += (double)bv[dj][c] * (double)bv[dj][c];
           }
+      }
     }
   });
   if (!DOWN && P.partials) {
-    block_sum2(sr, sb);
+    block_sum2(sr, sbb);
     if (threadIdx.x == 0)
-      P.partials[((long long)iz * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = make_double2(sr, sb);
+      P.partials[((long long)iz * tiles_y + tile_y) * tiles_x + tile_x] = make_double2(sr, sbb);
   }
 
   // ---------------------------------------------------------------- store x (tile interior)
-  if (xin_tile) {
 #pragma unroll
-    for (int j = 0; j < F2_R; ++j) {
-      const int gy = gyw + j;
-      if (!(ly0 + j >= H && ly0 + j < F2_ROWS - H) || !row_in(gy)) continue;
-      float* o = P.xout + pbase + (long long)gy * nx + gx0;
-      if (FAST && vec) {
-        *reinterpret_cast<float2*>(o) = make_float2(x[j][0], x[j][1]);
-      } else {
-        if (cin[0]) o[0] = x[j][0];
-        if (cin[1]) o[1] = x[j][1];
-      }
+  for (int j = 0; j < G_R; ++j) {
+    const int gy = gyw + j;
+    if (!(ly0 + j >= H && ly0 + j < G_ROWS - H) || !ri[j + 1].in) continue;
+    float* o = P.xout + pbase + (long long)gy * nx + gx0;
+    if (lane_full && vec) {
+      if (pin0) *reinterpret_cast<float2*>(o) = make_float2(A[j].x, B[j].x);
+      if (pin1) *reinterpret_cast<float2*>(o + 2) = make_float2(A[j].y, B[j].y);
+    } else {
+      if (pin0 && cin[0]) o[0] = A[j].x;
+      if (pin0 && cin[1]) o[1] = B[j].x;
+      if (pin1 && cin[2]) o[2] = A[j].y;
+      if (pin1 && cin[3]) o[3] = B[j].y;
     }
   }
 }
 
+struct Smem2D {
+  float4 top[2][G_W][32];        // warp boundary rows, double-buffered by half-sweep parity
+  float4 bot[2][G_W][32];
+  float2 b[G_W][G_R][2][32];     // rhs of the tile (read once per update)
+  RowInfo row[G_W][G_R + 2];     // per warp row: y coefficients and flags
+  float2 inv[G_W][4][2][32];     // per lane 1/D of the four row cases
+};
+constexpr size_t SMEM2D = sizeof(Smem2D);
+
+struct TileRect {  // tiles [tx0, tx1) x [ty0, ty1) of the tile grid take the fast kernel
+  int gx, gy;      // tile grid
+  int tx0, tx1, ty0, ty1;
+};
+
+// fast kernel: interior tiles only (grid = the fast rectangle)
 template <int NU, bool DOWN, int MODE, typename TI>
-__global__ void __launch_bounds__(256, 2) k_pass2d(Pass2D P) {
+__global__ void __launch_bounds__(256, 2) k_pass2d(Pass2D P, TileRect T) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Smem2D& S = *reinterpret_cast<Smem2D*>(smem_raw);
+  pass2d_body<NU, DOWN, MODE, TI>(P, S.top, S.bot, S.b, S.row, S.inv, blockIdx.x, blockIdx.y, T.gx, T.gy);
+}
+
+// ---------------------------------------------------------------------------------
+// edge kernel: tiles touching the domain faces (and every tile of small levels).  The tile
+// lives in shared memory and every cell calls the reference per-point functions
+// (coefs / rhs_g / apply_from / gs_update / rweight / ptaps / bilerp), so the result is the
+// reference schedule's bit for bit.  Runtime loops keep the code small.
+// ---------------------------------------------------------------------------------
+struct SmemEdge {
+  float x[G_ROWS][G_COLS];
+  float b[G_ROWS][G_COLS];
+};
+constexpr size_t SMEMEDGE = sizeof(SmemEdge);
+
+__device__ __forceinline__ void edge_tile(const TileRect& T, int e, int& tx, int& ty) {
+  // enumerate the tiles outside the fast rectangle: full rows below / above it, then the
+  // left and right columns of the rows it spans
+  const int below = T.ty0 * T.gx;
+  const int above = (T.gy - T.ty1) * T.gx;
+  if (e < below) { ty = e / T.gx; tx = e % T.gx; return; }
+  e -= below;
+  if (e < above) { ty = T.ty1 + e / T.gx; tx = e % T.gx; return; }
+  e -= above;
+  const int side = T.tx0 + (T.gx - T.tx1);
+  ty = T.ty0 + e / side;
+  const int k = e % side;
+  tx = k < T.tx0 ? k : T.tx1 + (k - T.tx0);
+}
+
+template <int NU, bool DOWN, int MODE, typename TI>
+__global__ void __launch_bounds__(256, 2) k_pass2d_edge(Pass2D P, TileRect T) {
   constexpr int H = halo2(NU);
-  constexpr int TXI = F2_COLS - 2 * H, TYI = F2_ROWS - 2 * H;
-  __shared__ float2 sh_top[2][F2_W][32];
-  __shared__ float2 sh_bot[2][F2_W][32];
-  // a tile whose cells (halo included) are all >= 2 cells from the low faces and >= 7 from the
-  // high faces has regular coefficients and regular transfer taps (no partial cells in reach)
-  const int gxa = blockIdx.x * TXI - H, gya = blockIdx.y * TYI - H;
-  const bool fast = P.fast_ok && gxa >= 2 && gxa + F2_COLS - 1 <= P.L.nx - 7 && gya >= 2 &&
-                    gya + F2_ROWS - 1 <= P.L.ny - 7;
-  if (fast) pass2d_body<NU, DOWN, MODE, TI, true>(P, sh_top, sh_bot);
-  else pass2d_body<NU, DOWN, MODE, TI, false>(P, sh_top, sh_bot);
+  constexpr int TXI = G_COLS - 2 * H, TYI = G_ROWS - 2 * H;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  SmemEdge& S = *reinterpret_cast<SmemEdge*>(smem_raw);
+  const LevelK& L = P.L;
+  int tx, ty;
+  edge_tile(T, blockIdx.x, tx, ty);
+  const int iz = blockIdx.y;
+  const long long zg = L.z0 + iz;
+  const int gxa = tx * TXI - H, gya = ty * TYI - H;
+  const long long nx = L.nx, plane = (long long)L.nx * L.ny, pbase = (long long)iz * plane;
+  const int tid = threadIdx.x;
+  auto inside = [&](int gx, int gy) { return gx >= 0 && gx < L.nx && gy >= 0 && gy < L.ny; };
+
+  // load x and b
+  for (int i = tid; i < G_ROWS * G_COLS; i += 256) {
+    const int ly = i / G_COLS, lx = i % G_COLS, gx = gxa + lx, gy = gya + ly;
+    float xv = 0.f, bv = 0.f;
+    if (inside(gx, gy)) {
+      const long long c = pbase + (long long)gy * nx + gx;
+      if (!P.zero_x) xv = P.xin[c];
+      if (MODE == RHS_B) bv = __ldg(P.R.b + c);
+      else bv = rhs_g<TI>(L, P.R, coefs(L, gx, gy, zg), c, nx);
+    }
+    S.x[ly][lx] = xv;
+    S.b[ly][lx] = bv;
+  }
+  __syncthreads();
+  if (!DOWN) {  // x += P e_c
+    const long long cplane = (long long)P.ncx * P.ncy;
+    const float* xcp = P.xc + (long long)iz * cplane;
+    for (int i = tid; i < G_ROWS * G_COLS; i += 256) {
+      const int ly = i / G_COLS, lx = i % G_COLS, gx = gxa + lx, gy = gya + ly;
+      if (!inside(gx, gy)) continue;
+      long long Ix, Jx, Iy, Jy;
+      float txw, tyw;
+      ptaps(P.tx, gx, Ix, Jx, txw);
+      ptaps(P.ty, gy, Iy, Jy, tyw);
+      const float e = bilerp(__ldg(xcp + Iy * P.ncx + Ix), __ldg(xcp + Iy * P.ncx + Jx),
+                             __ldg(xcp + Jy * P.ncx + Ix), __ldg(xcp + Jy * P.ncx + Jx), txw, tyw);
+      S.x[ly][lx] = __fadd_rn(S.x[ly][lx], e);
+    }
+    __syncthreads();
+  }
+  // residual of an in-domain cell whose 4 neighbours are in the tile (or absent)
+  auto resid = [&](int lx, int ly, int gx, int gy, float* bval) -> float {
+    const Coef k = coefs(L, gx, gy, zg);
+    const float xc = S.x[ly][lx];
+    Nbr nb;
+    nb.w = k.xl != 0.f ? S.x[ly][lx - 1] : xc;
+    nb.e = k.xr != 0.f ? S.x[ly][lx + 1] : xc;
+    nb.s = k.yl != 0.f ? S.x[ly - 1][lx] : xc;
+    nb.n = k.yr != 0.f ? S.x[ly + 1][lx] : xc;
+    nb.d = xc;
+    nb.u = xc;
+    if (bval) *bval = S.b[ly][lx];
+    return __fsub_rn(S.b[ly][lx], apply_from(k, L.alpha, xc, nb.w, nb.e, nb.s, nb.n, nb.d, nb.u));
+  };
+  // nu red-black sweeps (the outermost tile ring is never updated: it is stale anyway)
+  for (int hs = 0; hs < 2 * NU; ++hs) {
+    const int color = hs & 1;
+    for (int i = tid; i < G_ROWS * (G_COLS / 2); i += 256) {
+      const int ly = i / (G_COLS / 2), gy = gya + ly;
+      const int lx = 2 * (i % (G_COLS / 2)) + ((color + gy + (int)(zg & 1)) & 1);  // gxa even
+      const int gx = gxa + lx;
+      if (lx == 0 || lx == G_COLS - 1 || ly == 0 || ly == G_ROWS - 1 || !inside(gx, gy)) continue;
+      const float xc = S.x[ly][lx];
+      const float r = resid(lx, ly, gx, gy, nullptr);
+      S.x[ly][lx] = gs_update(xc, r, coefs(L, gx, gy, zg).diag(L.alpha));
+    }
+    __syncthreads();
+  }
+  // residual -> restriction (down) or norms (up), over the tile interior
+  if (DOWN) {
+    const long long cplane = (long long)P.ncx * P.ncy;
+    float* bcp = P.bc + (long long)iz * cplane;
+    const int sx = P.tx.coarsened ? 2 : 1, sy = P.ty.coarsened ? 2 : 1;
+    const int ncl = TXI / sx, nrl = TYI / sy;  // coarse cells of the interior
+    for (int i = tid; i < ncl * nrl; i += 256) {
+      const int cyl = i / ncl, cxl = i % ncl;
+      const int gx0 = gxa + H + sx * cxl, gy0 = gya + H + sy * cyl;
+      if (gx0 >= L.nx || gy0 >= L.ny) continue;
+      const int I = P.tx.coarsened ? gx0 >> 1 : gx0, J = P.ty.coarsened ? gy0 >> 1 : gy0;
+      float acc = 0.f;
+      for (int dy = 0; dy < sy && gy0 + dy < L.ny; ++dy) {
+        const float wy = rweight(P.ty, gy0 + dy);
+        for (int dx = 0; dx < sx && gx0 + dx < L.nx; ++dx) {
+          const int gx = gx0 + dx, gy = gy0 + dy;
+          const float r = resid(gx - gxa, gy - gya, gx, gy, nullptr);
+          acc = __fmaf_rn(rw3(1.f, wy, rweight(P.tx, gx)), r, acc);
+        }
+      }
+      bcp[(long long)J * P.ncx + I] = acc;
+    }
+  } else {
+    double sr = 0.0, sbb = 0.0;
+    if (P.partials) {
+      for (int i = tid; i < TYI * TXI; i += 256) {
+        const int ly = H + i / TXI, lx = H + i % TXI, gx = gxa + lx, gy = gya + ly;
+        if (!inside(gx, gy)) continue;
+        float bv;
+        const float r = resid(lx, ly, gx, gy, &bv);
+        sr += (double)r * (double)r;
+        sbb += (double)bv * (double)bv;
+      }
+      block_sum2(sr, sbb);
+      if (tid == 0) P.partials[((long long)iz * T.gy + ty) * T.gx + tx] = make_double2(sr, sbb);
+    }
+  }
+  // store the interior
+  for (int i = tid; i < TYI * TXI; i += 256) {
+    const int ly = H + i / TXI, lx = H + i % TXI, gx = gxa + lx, gy = gya + ly;
+    if (inside(gx, gy)) P.xout[pbase + (long long)gy * nx + gx] = S.x[ly][lx];
+  }
 }
 
 // ---------------------------------------------------------------------------------
@@ -435,39 +672,73 @@ bool fusable2d(const Level& L, const Level& C, const gdp_opts& o) {
   return nu_ok && o.fused && L.K.az.k == 0.f && L.K.az.kr == 0.f && L.K.az.kl == 0.f && !C.tz.coarsened;
 }
 
+static TileRect tiles2d(int nu, const LevelK& L, bool fast_ok) {
+  const int H = halo2(nu);
+  const int TXI = G_COLS - 2 * H, TYI = G_ROWS - 2 * H;
+  TileRect T{};
+  T.gx = (L.nx + TXI - 1) / TXI;
+  T.gy = (L.ny + TYI - 1) / TYI;
+  // the register kernel takes every tile of levels whose in-plane axes are both coarsened;
+  // other levels (one axis stopped coarsening) go to the shared-memory edge kernel
+  T.tx0 = 0; T.ty0 = 0;
+  T.tx1 = fast_ok ? T.gx : 0;
+  T.ty1 = fast_ok ? T.gy : 0;
+  return T;
+}
+
+int fused_tiles_per_plane(int nu, const LevelK& L) {
+  const TileRect T = tiles2d(nu, L, true);
+  return T.gx * T.gy;
+}
+
+template <typename K>
+static void set_smem(K k, size_t bytes) {
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+template <int NU, bool DOWN, int MODE, typename TI>
+static void launch2d_nu(const Pass2D& P, const TileRect& T, cudaStream_t s) {
+  static bool attr = false;  // opt in to > 48 KB dynamic shared memory once per instantiation
+  if (!attr) {
+    set_smem(k_pass2d<NU, DOWN, MODE, TI>, SMEM2D);
+    set_smem(k_pass2d_edge<NU, DOWN, MODE, TI>, SMEMEDGE);
+    attr = true;
+  }
+  const int nfast = (T.tx1 - T.tx0) * (T.ty1 - T.ty0);
+  const int nedge = T.gx * T.gy - nfast;
+  if (nfast > 0) {
+    dim3 g(T.tx1 - T.tx0, T.ty1 - T.ty0, P.L.nzl);
+    k_pass2d<NU, DOWN, MODE, TI><<<g, 256, SMEM2D, s>>>(P, T);
+  }
+  if (nedge > 0) {
+    count_launch();
+    dim3 g(nedge, P.L.nzl);
+    k_pass2d_edge<NU, DOWN, MODE, TI><<<g, 256, SMEMEDGE, s>>>(P, T);
+  }
+}
+
 template <bool DOWN, int MODE, typename TI>
-static void launch2d_t(int nu, const Pass2D& P, dim3 g, cudaStream_t s) {
+static void launch2d_t(int nu, const Pass2D& P, const TileRect& T, cudaStream_t s) {
   switch (nu) {
-    case 1: k_pass2d<1, DOWN, MODE, TI><<<g, 256, 0, s>>>(P); break;
-    case 2: k_pass2d<2, DOWN, MODE, TI><<<g, 256, 0, s>>>(P); break;
+    case 1: launch2d_nu<1, DOWN, MODE, TI>(P, T, s); break;
+    case 2: launch2d_nu<2, DOWN, MODE, TI>(P, T, s); break;
     default: break;
   }
 }
 
-static dim3 grid2d(int nu, const LevelK& L) {
-  const int H = halo2(nu);
-  const int TXI = F2_COLS - 2 * H, TYI = F2_ROWS - 2 * H;
-  return dim3((L.nx + TXI - 1) / TXI, (L.ny + TYI - 1) / TYI, L.nzl);
-}
-
-int fused_tiles_per_plane(int nu, const LevelK& L) {
-  dim3 g = grid2d(nu, L);
-  return g.x * g.y;
-}
-
 static void launch2d(bool down, int nu, const Pass2D& P, int mode, int tI, cudaStream_t s) {
-  dim3 g = grid2d(nu, P.L);
+  const TileRect T = tiles2d(nu, P.L, P.fast_ok != 0);
   const double N = (double)P.L.nx * P.L.ny * P.L.nzl, Nc = (double)P.ncx * P.ncy * P.L.nzl;
   const double bytes = N * ((P.zero_x ? 4.0 : 8.0) + rhs_bytes(mode, tI, P.R)) + Nc * 4.0;
   ProfScope ps(down ? KC_DOWN2D : KC_UP2D, bytes, s);
   if (down) {
-    if (mode == RHS_B) launch2d_t<true, RHS_B, float>(nu, P, g, s);
-    else if (tI == 0) launch2d_t<true, RHS_G, uint8_t>(nu, P, g, s);
-    else launch2d_t<true, RHS_G, float>(nu, P, g, s);
+    if (mode == RHS_B) launch2d_t<true, RHS_B, float>(nu, P, T, s);
+    else if (tI == 0) launch2d_t<true, RHS_G, uint8_t>(nu, P, T, s);
+    else launch2d_t<true, RHS_G, float>(nu, P, T, s);
   } else {
-    if (mode == RHS_B) launch2d_t<false, RHS_B, float>(nu, P, g, s);
-    else if (tI == 0) launch2d_t<false, RHS_G, uint8_t>(nu, P, g, s);
-    else launch2d_t<false, RHS_G, float>(nu, P, g, s);
+    if (mode == RHS_B) launch2d_t<false, RHS_B, float>(nu, P, T, s);
+    else if (tI == 0) launch2d_t<false, RHS_G, uint8_t>(nu, P, T, s);
+    else launch2d_t<false, RHS_G, float>(nu, P, T, s);
   }
 }
 

@@ -42,7 +42,6 @@ constexpr int G_COLS = 128;               // columns per warp (4 per lane)
 constexpr int G_ROWS = G_R * G_W;         // 96
 constexpr unsigned FULL = 0xffffffffu;
 
-__host__ __device__ constexpr int halo2(int nu) { return ((2 * nu + 1) + 1) & ~1; }
 
 struct Pass2D {
   LevelK L;
@@ -149,20 +148,30 @@ template <> struct Row4<uint8_t> {
 };
 
 // Row data of one warp row (warp-uniform): link coefficients of the row's y links, whether the
-// row is inside the domain, and whether its coefficients are the regular interior ones.
+// row is inside the domain, and which 1/D case applies.
 struct RowInfo { float yl, yr; int in, dcase; };
 
-template <int NU, bool DOWN, int MODE, typename TI>
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
+
+// halo of the 2D pass: >= 2 nu + 1; a multiple of 4 in x (16-byte aligned lane quads), even in y
+__host__ __device__ constexpr int halo2x(int nu) { return ((2 * nu + 1) + 3) & ~3; }
+__host__ __device__ constexpr int halo2y(int nu) { return ((2 * nu + 1) + 1) & ~1; }
+
+template <int NU, bool DOWN>
 __device__ __forceinline__ void pass2d_body(const Pass2D& P, float4 (&sh_top)[2][G_W][32],
-                                            float4 (&sh_bot)[2][G_W][32], float2 (&sb)[G_W][G_R][2][32],
+                                            float4 (&sh_bot)[2][G_W][32], float4 (&sb)[G_W][G_R][32],
                                             RowInfo (&srow)[G_W][G_R + 2], float2 (&sinv)[G_W][4][2][32],
                                             int tile_x, int tile_y, int tiles_x, int tiles_y) {
-  constexpr int H = halo2(NU);
-  constexpr int TXI = G_COLS - 2 * H, TYI = G_ROWS - 2 * H;
+  constexpr int HX = halo2x(NU), HY = halo2y(NU);
+  constexpr int TXI = G_COLS - 2 * HX, TYI = G_ROWS - 2 * HY;
   const LevelK& L = P.L;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int gx0 = tile_x * TXI - H + 4 * lane;    // my first column (even)
-  const int gyw = tile_y * TYI - H + warp * G_R;  // my first row (even)
+  const int gx0 = tile_x * TXI - HX + 4 * lane;    // my first column (multiple of 4)
+  const int gyw = tile_y * TYI - HY + warp * G_R;  // my first row (even)
   const int iz = blockIdx.z;
   const long long zg = L.z0 + iz;
   const long long nx = L.nx;
@@ -182,28 +191,61 @@ __device__ __forceinline__ void pass2d_body(const Pass2D& P, float4 (&sh_top)[2]
   }
   const float2 kxlA = make_float2(cxl[0], cxl[2]), kxrA = make_float2(cxr[0], cxr[2]);
   const float2 kxlB = make_float2(cxl[1], cxl[3]), kxrB = make_float2(cxr[1], cxr[3]);
-  auto invd = [&](int c, float yl, float yr) {
-    Coef k;
-    k.xl = cxl[c]; k.xr = cxr[c]; k.yl = yl; k.yr = yr; k.zl = 0.f; k.zr = 0.f;
-    return __frcp_rn(k.diag(alpha));  // == the 1/D of gs_update
-  };
-  // 1/D of my columns for the four row cases: 0 regular (or outside the domain, whose values
-  // never reach it), 1 the first row, 2 the row before the last, 3 the last row
-  {
-    const int ny = L.ay.n;
-    const int rows[4] = {1, 0, ny - 2, ny - 1};
+  const bool lane_full = cin[0] && cin[1] && cin[2] && cin[3];
+  const bool vec = (L.nx & 3) == 0;  // rows start 16-byte aligned
+
+  // ---------------------------------------------------------------- issue all loads
+  float4(&bs)[G_R][32] = sb[warp];
+  float2 A[G_R], B[G_R];  // x of my 12 rows x 4 columns
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const float yl = k == 0 ? L.ay.k : cl(L.ay, rows[k]);
-      const float yr = k == 0 ? L.ay.k : cr(L.ay, rows[k]);
-      sinv[warp][k][0][lane] = make_float2(invd(0, yl, yr), invd(2, yl, yr));
-      sinv[warp][k][1][lane] = make_float2(invd(1, yl, yr), invd(3, yl, yr));
+  for (int j = 0; j < G_R; ++j) {
+    const int gy = gyw + j;
+    const bool rin = gy >= 0 && gy < L.ny;
+    const long long rowp = pbase + (long long)gy * nx + gx0;
+    if (rin && lane_full && vec) {
+      cp_async16(&bs[j][lane], P.R.b + rowp);
+      if (P.zero_x) { A[j] = B[j] = f2(0.f); }
+      else {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(P.xin + rowp));
+        A[j] = make_float2(v.x, v.z);
+        B[j] = make_float2(v.y, v.w);
+      }
+    } else {
+      float v[4], w[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const bool in = rin && cin[c];
+        v[c] = (in && !P.zero_x) ? __ldg(P.xin + rowp + c) : 0.f;
+        w[c] = in ? __ldg(P.R.b + rowp + c) : 0.f;
+      }
+      A[j] = make_float2(v[0], v[2]);
+      B[j] = make_float2(v[1], v[3]);
+      bs[j][lane] = make_float4(w[0], w[1], w[2], w[3]);
     }
   }
-  const bool lane_full = cin[0] && cin[1] && cin[2] && cin[3];
-  const bool vec = (L.nx & 1) == 0;  // rows start 8-byte aligned
+  // coarse correction values for the up pass (issued before waiting on anything)
+  constexpr int NQ = G_R / 2 + 2;
+  float2 cv[NQ];  // (v0, v1) at coarse columns (Ix0, Ix0+1), coarse rows Jw .. Jw+NQ-1
+  const int Ix0 = gx0 >> 1;
+  const int Jw = (gyw >> 1) - 1;
+  const long long cplane = (long long)P.ncx * P.ncy;
+  if (!DOWN) {
+    const float* xcp = P.xc + (long long)iz * cplane;
+    const bool cvec = (P.ncx & 1) == 0 && Ix0 >= 0 && Ix0 + 1 < P.ncx;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const int J = Jw + q;
+      const float* rp = xcp + (long long)J * P.ncx + Ix0;
+      if (J >= 0 && J < P.ncy && cvec) cv[q] = __ldg(reinterpret_cast<const float2*>(rp));
+      else {
+        const bool rin = J >= 0 && J < P.ncy;
+        cv[q] = make_float2((rin && Ix0 >= 0 && Ix0 < P.ncx) ? __ldg(rp) : 0.f,
+                            (rin && Ix0 + 1 >= 0 && Ix0 + 1 < P.ncx) ? __ldg(rp + 1) : 0.f);
+      }
+    }
+  }
 
-  // ---- per-row data (rows -1 .. G_R of this warp), in shared memory
+  // ---- per-row data (rows -1 .. G_R of this warp) and the 1/D table, while loads fly
   RowInfo(&ri)[G_R + 2] = srow[warp];
   if (lane < G_R + 2) {
     const int gy = gyw + lane - 1;
@@ -212,86 +254,42 @@ __device__ __forceinline__ void pass2d_body(const Pass2D& P, float4 (&sh_top)[2]
     r.yr = cr(L.ay, gy);
     r.in = gy >= 0 && gy < L.ny;
     const int n = L.ay.n;
-    r.dcase = gy == 0 ? 1 : (gy == n - 1 ? 3 : (gy == n - 2 ? 2 : 0));
-    if (!r.in) r.dcase = 0;
+    r.dcase = !r.in ? 0 : (gy == 0 ? 1 : (gy == n - 1 ? 3 : (gy == n - 2 ? 2 : 0)));
     ri[lane] = r;
   }
+  {
+    // 1/D of my columns for the four row cases: 0 regular (or outside the domain, whose values
+    // never reach it), 1 the first row, 2 the row before the last, 3 the last row
+    auto invd = [&](int c, float yl, float yr) {
+      Coef k;
+      k.xl = cxl[c]; k.xr = cxr[c]; k.yl = yl; k.yr = yr; k.zl = 0.f; k.zr = 0.f;
+      return __frcp_rn(k.diag(alpha));  // == the 1/D of gs_update
+    };
+    const int ny = L.ay.n;
+    const int rows[4] = {1, 0, ny - 2, ny - 1};
+#pragma unroll 1
+    for (int k = 0; k < 4; ++k) {
+      const float yl = k == 0 ? L.ay.k : cl(L.ay, rows[k]);
+      const float yr = k == 0 ? L.ay.k : cr(L.ay, rows[k]);
+      sinv[warp][k][0][lane] = make_float2(invd(0, yl, yr), invd(2, yl, yr));
+      sinv[warp][k][1][lane] = make_float2(invd(1, yl, yr), invd(3, yl, yr));
+    }
+  }
+  cp_async_wait_all();
   __syncwarp();
-
-  float2 A[G_R], B[G_R];  // x of my 12 rows x 4 columns
-  float2(&bs)[G_R][2][32] = sb[warp];
-  auto ld4 = [&](const float* base, long long rowp, bool rin, float2& oA, float2& oB) {
-    if (rin && lane_full && vec) { ld4f(base + rowp, oA, oB); return; }
-    float v[4];
-#pragma unroll
-    for (int c = 0; c < 4; ++c) v[c] = (rin && cin[c]) ? __ldg(base + rowp + c) : 0.f;
-    oA = make_float2(v[0], v[2]);
-    oB = make_float2(v[1], v[3]);
-  };
-  // ---------------------------------------------------------------- load x and rhs
+  // b rows to pack layout in place: (c0, c1, c2, c3) -> (c0, c2 | c1, c3)
 #pragma unroll
   for (int j = 0; j < G_R; ++j) {
-    const int gy = gyw + j;
-    const bool rin = ri[j + 1].in;
-    const long long rowp = pbase + (long long)gy * nx + gx0;
-    if (P.zero_x) { A[j] = B[j] = f2(0.f); }
-    else ld4(P.xin, rowp, rin, A[j], B[j]);
-    if (MODE == RHS_B) {
-      float2 a, b;
-      ld4(P.R.b, rowp, rin, a, b);
-      bs[j][0][lane] = a;
-      bs[j][1][lane] = b;
-    }
+    const float4 v = bs[j][lane];
+    bs[j][lane] = make_float4(v.x, v.z, v.y, v.w);
   }
-  if (MODE == RHS_G) {
-    // b = rhs_from(...) on a rolling window of I rows (gy-1, gy, gy+1)
-    float2 IpA, IpB, IcA, IcB, InA, InB;
-    auto ldrow = [&](int jr, float2& oA, float2& oB) {  // jr = row index - 1 .. G_R
-      const int gy = gyw + jr;
-      const bool rin = ri[jr + 1].in;
-      const long long rowp = pbase + (long long)gy * nx + gx0;
-      if (rin && lane_full && vec) { Row4<TI>::ld(P.R.I, rowp, oA, oB); return; }
-      float v[4];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) v[c] = (rin && cin[c]) ? ldI<TI>(P.R.I, rowp + c) : 0.f;
-      oA = make_float2(v[0], v[2]);
-      oB = make_float2(v[1], v[3]);
-    };
-    ldrow(-1, IpA, IpB);
-    ldrow(0, IcA, IcB);
-    const float2 av2 = f2(P.R.av);
-#pragma unroll
-    for (int j = 0; j < G_R; ++j) {
-      if (j + 1 < G_R + 1) ldrow(j + 1, InA, InB);
-      const RowInfo r = ri[j + 1];
-      const long long rowp = pbase + (long long)(gyw + j) * nx + gx0;
-      float2 VA = f2(0.f), VB = f2(0.f);
-      if (P.R.vmode == 1) { VA = IcA; VB = IcB; }
-      else if (P.R.vmode == 2) ld4(P.R.V, rowp, r.in != 0, VA, VB);
-      const float up3 = __shfl_up_sync(FULL, IcB.y, 1);    // column -1
-      const float dn0 = __shfl_down_sync(FULL, IcA.x, 1);  // column 4
-      const float2 yl = f2(r.yl), yr = f2(r.yr);
-      // rhs_from(k, Ic, Iw, Ie, Is, In, V, av) per element (absent links have coefficient 0)
-      float2 g = __fmul2_rn(kxlA, sub2(IcA, make_float2(up3, IcB.x)));
-      g = __ffma2_rn(kxrA, sub2(IcA, IcB), g);
-      g = __ffma2_rn(yl, sub2(IcA, IpA), g);
-      g = __ffma2_rn(yr, sub2(IcA, InA), g);
-      bs[j][0][lane] = __ffma2_rn(av2, VA, g);
-      g = __fmul2_rn(kxlB, sub2(IcB, IcA));
-      g = __ffma2_rn(kxrB, sub2(IcB, make_float2(IcA.y, dn0)), g);
-      g = __ffma2_rn(yl, sub2(IcB, IpB), g);
-      g = __ffma2_rn(yr, sub2(IcB, InB), g);
-      bs[j][1][lane] = __ffma2_rn(av2, VB, g);
-      IpA = IcA; IpB = IcB; IcA = InA; IcB = InB;
-    }
-  }
+  auto bpk = [&](int j, int pk) -> float2 {
+    const float4* p = &bs[j][lane];
+    return reinterpret_cast<const float2*>(p)[pk];
+  };
 
   // ---------------------------------------------------------------- up: add P e_c
   if (!DOWN) {
-    const long long cplane = (long long)P.ncx * P.ncy;
-    const float* xcp = P.xc + (long long)iz * cplane;
-    // my columns' parents: Ix0 = gx0/2 (c0, c1) and Ix0+1 (c2, c3); taps from ptaps()
-    const int Ix0 = gx0 >> 1;
     float tx[4];
     bool selfJ[4];
 #pragma unroll
@@ -301,18 +299,11 @@ __device__ __forceinline__ void pass2d_body(const Pass2D& P, float4 (&sh_top)[2]
       selfJ[c] = J == I;
     }
     const float2 txA = make_float2(tx[0], tx[2]), txB = make_float2(tx[1], tx[3]);
-    const int Jw = (gyw >> 1) - 1;  // first coarse row loaded
-    float2 cv[G_R / 2 + 2][2];      // [q] -> (v0, v1) at (Ix0, Ix0+1) and (vm, vp) at (Ix0-1, Ix0+2)
+    const float2 uxA = make_float2(1.f - tx[0], 1.f - tx[2]), uxB = make_float2(1.f - tx[1], 1.f - tx[3]);
+    float2 cn[NQ];  // (vm, vp) at coarse columns Ix0-1, Ix0+2
 #pragma unroll
-    for (int q = 0; q < G_R / 2 + 2; ++q) {
-      const int J = Jw + q;
-      const bool rin = J >= 0 && J < P.ncy;
-      const float* rp = xcp + (long long)J * P.ncx + Ix0;
-      const float v0 = (rin && Ix0 >= 0 && Ix0 < P.ncx) ? __ldg(rp) : 0.f;
-      const float v1 = (rin && Ix0 + 1 >= 0 && Ix0 + 1 < P.ncx) ? __ldg(rp + 1) : 0.f;
-      cv[q][0] = make_float2(v0, v1);
-      cv[q][1] = make_float2(__shfl_up_sync(FULL, v1, 1), __shfl_down_sync(FULL, v0, 1));
-    }
+    for (int q = 0; q < NQ; ++q)
+      cn[q] = make_float2(__shfl_up_sync(FULL, cv[q].y, 1), __shfl_down_sync(FULL, cv[q].x, 1));
 #pragma unroll
     for (int j = 0; j < G_R; ++j) {
       const int gy = gyw + j;
@@ -321,8 +312,9 @@ __device__ __forceinline__ void pass2d_body(const Pass2D& P, float4 (&sh_top)[2]
       ptaps(P.ty, gy, Iy, Jy, ty);
       const int q = (j >> 1) + 1;  // == Iy - Jw
       const int dq = (int)(Jy - Iy);
-      auto rowJ = [&](int k) { return dq < 0 ? cv[q - 1][k] : (dq > 0 ? cv[q + 1][k] : cv[q][k]); };
-      const float2 r0 = cv[q][0], r1 = cv[q][1], n0 = rowJ(0), n1 = rowJ(1);
+      const float2 r0 = cv[q], r1 = cn[q];
+      const float2 n0 = dq < 0 ? cv[q - 1] : (dq > 0 ? cv[q + 1] : cv[q]);
+      const float2 n1 = dq < 0 ? cn[q - 1] : (dq > 0 ? cn[q + 1] : cn[q]);
       // pack A = (c0, c2): parents (Ix0, Ix0+1); neighbours c0 -> Ix0-1 | Ix0, c2 -> Ix0 | Ix0+1
       const float2 aJ = make_float2(selfJ[0] ? r0.x : r1.x, selfJ[2] ? r0.y : r0.x);
       const float2 cJ = make_float2(selfJ[0] ? n0.x : n1.x, selfJ[2] ? n0.y : n0.x);
@@ -330,19 +322,13 @@ __device__ __forceinline__ void pass2d_body(const Pass2D& P, float4 (&sh_top)[2]
       const float2 bJ = make_float2(selfJ[1] ? r0.x : r0.y, selfJ[3] ? r0.y : r1.y);
       const float2 dJ = make_float2(selfJ[1] ? n0.x : n0.y, selfJ[3] ? n0.y : n1.y);
       const float2 ty2 = f2(ty), uy2 = f2(1.f - ty);
-      // bilerp(a, b, c, d, tx, ty) per element
-      {
-        const float2 ux = make_float2(1.f - txA.x, 1.f - txA.y);
-        const float2 s0 = __ffma2_rn(txA, aJ, __fmul2_rn(ux, r0));
-        const float2 s1 = __ffma2_rn(txA, cJ, __fmul2_rn(ux, n0));
-        A[j] = __fadd2_rn(A[j], __ffma2_rn(ty2, s1, __fmul2_rn(uy2, s0)));
-      }
-      {
-        const float2 ux = make_float2(1.f - txB.x, 1.f - txB.y);
-        const float2 s0 = __ffma2_rn(txB, bJ, __fmul2_rn(ux, r0));
-        const float2 s1 = __ffma2_rn(txB, dJ, __fmul2_rn(ux, n0));
-        B[j] = __fadd2_rn(B[j], __ffma2_rn(ty2, s1, __fmul2_rn(uy2, s0)));
-      }
+      // x += bilerp(a, b, c, d, tx, ty) per element
+      const float2 sA0 = __ffma2_rn(txA, aJ, __fmul2_rn(uxA, r0));
+      const float2 sA1 = __ffma2_rn(txA, cJ, __fmul2_rn(uxA, n0));
+      A[j] = __fadd2_rn(A[j], __ffma2_rn(ty2, sA1, __fmul2_rn(uy2, sA0)));
+      const float2 sB0 = __ffma2_rn(txB, bJ, __fmul2_rn(uxB, r0));
+      const float2 sB1 = __ffma2_rn(txB, dJ, __fmul2_rn(uxB, n0));
+      B[j] = __fadd2_rn(B[j], __ffma2_rn(ty2, sB1, __fmul2_rn(uy2, sB0)));
     }
   }
 
@@ -392,7 +378,7 @@ __device__ __forceinline__ void pass2d_body(const Pass2D& P, float4 (&sh_top)[2]
     constexpr int PK = decltype(PKc)::value;
     constexpr int j = decltype(Jc)::value;
     const RowInfo r = ri[j + 1];
-    const float2 res = sub2(bs[j][PK][lane], stencil(PKc, Jc, r));
+    const float2 res = sub2(bpk(j, PK), stencil(PKc, Jc, r));
     const float2 iD = sinv[warp][r.dcase][PK][lane];
     if (PK == 0) A[j] = __ffma2_rn(res, iD, A[j]);
     else B[j] = __ffma2_rn(res, iD, B[j]);
@@ -403,7 +389,7 @@ __device__ __forceinline__ void pass2d_body(const Pass2D& P, float4 (&sh_top)[2]
   for (int hs = 0; hs < 2 * NU; ++hs) {
     const int color = hs & 1;
     exchange(hs & 1);
-    const int a0 = (color + gyw + (int)(zg & 1)) & 1;  // active pack of row 0
+    const int a0 = (color + gyw + (int)(zg & 1)) & 1;  // active pack of row 0 (gx0 even)
     if (a0 == 0) static_for<G_R>([&](auto J) { update(IC<(decltype(J)::value & 1)>{}, J); });
     else static_for<G_R>([&](auto J) { update(IC<((decltype(J)::value & 1) ^ 1)>{}, J); });
   }
@@ -412,11 +398,8 @@ __device__ __forceinline__ void pass2d_body(const Pass2D& P, float4 (&sh_top)[2]
   exchange((2 * NU) & 1);
   const int lx0 = 4 * lane;     // local column of c = 0
   const int ly0 = warp * G_R;   // local row of j = 0
-  // interior-ness of column pairs (c0,c1) and (c2,c3) (pairs are even-aligned, H even)
-  const bool pin0 = lx0 >= H && lx0 < G_COLS - H;
-  const bool pin1 = lx0 + 2 >= H && lx0 + 2 < G_COLS - H;
+  const bool pin = lx0 >= HX && lx0 < G_COLS - HX;  // all 4 columns together (HX % 4 == 0)
   double sr = 0.0, sbb = 0.0;
-  const long long cplane = (long long)P.ncx * P.ncy;
   float* bcp = DOWN ? P.bc + (long long)iz * cplane : nullptr;
   float wx[4];
   if (DOWN) {
@@ -426,18 +409,18 @@ __device__ __forceinline__ void pass2d_body(const Pass2D& P, float4 (&sh_top)[2]
   static_for<G_R / 2>([&](auto JP) {
     constexpr int j0 = 2 * decltype(JP)::value;
     const RowInfo r0 = ri[j0 + 1], r1 = ri[j0 + 2];
-    const float2 rA0 = sub2(bs[j0][0][lane], stencil(IC<0>{}, IC<j0>{}, r0));
-    const float2 rB0 = sub2(bs[j0][1][lane], stencil(IC<1>{}, IC<j0>{}, r0));
-    const float2 rA1 = sub2(bs[j0 + 1][0][lane], stencil(IC<0>{}, IC<j0 + 1>{}, r1));
-    const float2 rB1 = sub2(bs[j0 + 1][1][lane], stencil(IC<1>{}, IC<j0 + 1>{}, r1));
+    const float2 rA0 = sub2(bpk(j0, 0), stencil(IC<0>{}, IC<j0>{}, r0));
+    const float2 rB0 = sub2(bpk(j0, 1), stencil(IC<1>{}, IC<j0>{}, r0));
+    const float2 rA1 = sub2(bpk(j0 + 1, 0), stencil(IC<0>{}, IC<j0 + 1>{}, r1));
+    const float2 rB1 = sub2(bpk(j0 + 1, 1), stencil(IC<1>{}, IC<j0 + 1>{}, r1));
     const int gy0 = gyw + j0;  // even
-    const bool yin0 = ly0 + j0 >= H && ly0 + j0 < G_ROWS - H;  // rows j0, j0+1 together (H even)
+    const bool yin0 = ly0 + j0 >= HY && ly0 + j0 < G_ROWS - HY;  // rows j0, j0+1 together (HY even)
     if (DOWN) {
       // volume-weighted child average (fy outer, fx inner as in k_restrict); coarse cells
       // (Ix0, J) from children (c0, c1) and (Ix0+1, J) from (c2, c3)
-      const int J = gy0 >> 1, I0 = gx0 >> 1;
-      const bool ok0 = yin0 && pin0 && r0.in && gx0 >= 0 && I0 < P.ncx && J < P.ncy;
-      const bool ok1 = yin0 && pin1 && r0.in && gx0 + 2 >= 0 && I0 + 1 < P.ncx && J < P.ncy;
+      const int J = gy0 >> 1;
+      const bool ok0 = yin0 && pin && r0.in && gx0 >= 0 && Ix0 < P.ncx && J < P.ncy;
+      const bool ok1 = yin0 && pin && r0.in && Ix0 + 1 < P.ncx && J < P.ncy;
       if (ok0 || ok1) {
         const float wy0 = rweight(P.ty, gy0), wy1 = rweight(P.ty, gy0 + 1);
         const float2 wA0 = make_float2(rw3(1.f, wy0, wx[0]), rw3(1.f, wy0, wx[2]));
@@ -452,13 +435,15 @@ __device__ __forceinline__ void pass2d_body(const Pass2D& P, float4 (&sh_top)[2]
           t = __ffma2_rn(wB1, rB1, acc);
           acc = make_float2(cin[1] ? t.x : acc.x, cin[3] ? t.y : acc.y);
         }
-        float* o = bcp + (long long)J * P.ncx + I0;
-        if (ok0) o[0] = acc.x;
-        if (ok1) o[1] = acc.y;
+        float* o = bcp + (long long)J * P.ncx + Ix0;
+        if (ok0 && ok1 && (P.ncx & 1) == 0) *reinterpret_cast<float2*>(o) = acc;
+        else {
+          if (ok0) o[0] = acc.x;
+          if (ok1) o[1] = acc.y;
+        }
       }
-    } else if (yin0 && P.partials) {
-      const float2 bA0 = bs[j0][0][lane], bB0 = bs[j0][1][lane];
-      const float2 bA1 = bs[j0 + 1][0][lane], bB1 = bs[j0 + 1][1][lane];
+    } else if (yin0 && pin && P.partials) {
+      const float2 bA0 = bpk(j0, 0), bB0 = bpk(j0, 1), bA1 = bpk(j0 + 1, 0), bB1 = bpk(j0 + 1, 1);
       const float rr[2][4] = {{rA0.x, rB0.x, rA0.y, rB0.y}, {rA1.x, rB1.x, rA1.y, rB1.y}};
       const float bv[2][4] = {{bA0.x, bB0.x, bA0.y, bB0.y}, {bA1.x, bB1.x, bA1.y, bB1.y}};
 #pragma unroll
@@ -466,7 +451,7 @@ __device__ __forceinline__ void pass2d_body(const Pass2D& P, float4 (&sh_top)[2]
         if (!(dj ? r1.in : r0.in)) continue;
 #pragma unroll
         for (int c = 0; c < 4; ++c)
-          if ((c < 2 ? pin0 : pin1) && cin[c]) {
+          if (cin[c]) {
             sr += (double)rr[dj][c] * (double)rr[dj][c];
             sbb += (double)bv[dj][c] * (double)bv[dj][c];
           }
@@ -480,19 +465,20 @@ __device__ __forceinline__ void pass2d_body(const Pass2D& P, float4 (&sh_top)[2]
   }
 
   // ---------------------------------------------------------------- store x (tile interior)
+  if (pin) {
 #pragma unroll
-  for (int j = 0; j < G_R; ++j) {
-    const int gy = gyw + j;
-    if (!(ly0 + j >= H && ly0 + j < G_ROWS - H) || !ri[j + 1].in) continue;
-    float* o = P.xout + pbase + (long long)gy * nx + gx0;
-    if (lane_full && vec) {
-      if (pin0) *reinterpret_cast<float2*>(o) = make_float2(A[j].x, B[j].x);
-      if (pin1) *reinterpret_cast<float2*>(o + 2) = make_float2(A[j].y, B[j].y);
-    } else {
-      if (pin0 && cin[0]) o[0] = A[j].x;
-      if (pin0 && cin[1]) o[1] = B[j].x;
-      if (pin1 && cin[2]) o[2] = A[j].y;
-      if (pin1 && cin[3]) o[3] = B[j].y;
+    for (int j = 0; j < G_R; ++j) {
+      const int gy = gyw + j;
+      if (!(ly0 + j >= HY && ly0 + j < G_ROWS - HY) || !ri[j + 1].in) continue;
+      float* o = P.xout + pbase + (long long)gy * nx + gx0;
+      if (lane_full && vec) {
+        *reinterpret_cast<float4*>(o) = make_float4(A[j].x, B[j].x, A[j].y, B[j].y);
+      } else {
+        if (cin[0]) o[0] = A[j].x;
+        if (cin[1]) o[1] = B[j].x;
+        if (cin[2]) o[2] = A[j].y;
+        if (cin[3]) o[3] = B[j].y;
+      }
     }
   }
 }
@@ -500,23 +486,23 @@ __device__ __forceinline__ void pass2d_body(const Pass2D& P, float4 (&sh_top)[2]
 struct Smem2D {
   float4 top[2][G_W][32];        // warp boundary rows, double-buffered by half-sweep parity
   float4 bot[2][G_W][32];
-  float2 b[G_W][G_R][2][32];     // rhs of the tile (read once per update)
+  float4 b[G_W][G_R][32];        // rhs of the tile, per lane (c0, c2 | c1, c3)
   RowInfo row[G_W][G_R + 2];     // per warp row: y coefficients and flags
   float2 inv[G_W][4][2][32];     // per lane 1/D of the four row cases
 };
 constexpr size_t SMEM2D = sizeof(Smem2D);
 
-struct TileRect {  // tiles [tx0, tx1) x [ty0, ty1) of the tile grid take the fast kernel
+struct TileRect {  // tiles [tx0, tx1) x [ty0, ty1) of the tile grid take the register kernel
   int gx, gy;      // tile grid
   int tx0, tx1, ty0, ty1;
 };
 
-// fast kernel: interior tiles only (grid = the fast rectangle)
-template <int NU, bool DOWN, int MODE, typename TI>
+// register kernel: every tile of a level whose in-plane axes are both coarsened; explicit rhs b
+template <int NU, bool DOWN>
 __global__ void __launch_bounds__(256, 2) k_pass2d(Pass2D P, TileRect T) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Smem2D& S = *reinterpret_cast<Smem2D*>(smem_raw);
-  pass2d_body<NU, DOWN, MODE, TI>(P, S.top, S.bot, S.b, S.row, S.inv, blockIdx.x, blockIdx.y, T.gx, T.gy);
+  pass2d_body<NU, DOWN>(P, S.top, S.bot, S.b, S.row, S.inv, blockIdx.x, blockIdx.y, T.gx, T.gy);
 }
 
 // ---------------------------------------------------------------------------------
@@ -546,10 +532,10 @@ __device__ __forceinline__ void edge_tile(const TileRect& T, int e, int& tx, int
   tx = k < T.tx0 ? k : T.tx1 + (k - T.tx0);
 }
 
-template <int NU, bool DOWN, int MODE, typename TI>
+template <int NU, bool DOWN>
 __global__ void __launch_bounds__(256, 2) k_pass2d_edge(Pass2D P, TileRect T) {
-  constexpr int H = halo2(NU);
-  constexpr int TXI = G_COLS - 2 * H, TYI = G_ROWS - 2 * H;
+  constexpr int HX = halo2x(NU), HY = halo2y(NU);
+  constexpr int TXI = G_COLS - 2 * HX, TYI = G_ROWS - 2 * HY;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   SmemEdge& S = *reinterpret_cast<SmemEdge*>(smem_raw);
   const LevelK& L = P.L;
@@ -557,7 +543,7 @@ __global__ void __launch_bounds__(256, 2) k_pass2d_edge(Pass2D P, TileRect T) {
   edge_tile(T, blockIdx.x, tx, ty);
   const int iz = blockIdx.y;
   const long long zg = L.z0 + iz;
-  const int gxa = tx * TXI - H, gya = ty * TYI - H;
+  const int gxa = tx * TXI - HX, gya = ty * TYI - HY;
   const long long nx = L.nx, plane = (long long)L.nx * L.ny, pbase = (long long)iz * plane;
   const int tid = threadIdx.x;
   auto inside = [&](int gx, int gy) { return gx >= 0 && gx < L.nx && gy >= 0 && gy < L.ny; };
@@ -569,8 +555,7 @@ __global__ void __launch_bounds__(256, 2) k_pass2d_edge(Pass2D P, TileRect T) {
     if (inside(gx, gy)) {
       const long long c = pbase + (long long)gy * nx + gx;
       if (!P.zero_x) xv = P.xin[c];
-      if (MODE == RHS_B) bv = __ldg(P.R.b + c);
-      else bv = rhs_g<TI>(L, P.R, coefs(L, gx, gy, zg), c, nx);
+      bv = __ldg(P.R.b + c);
     }
     S.x[ly][lx] = xv;
     S.b[ly][lx] = bv;
@@ -628,7 +613,7 @@ __global__ void __launch_bounds__(256, 2) k_pass2d_edge(Pass2D P, TileRect T) {
     const int ncl = TXI / sx, nrl = TYI / sy;  // coarse cells of the interior
     for (int i = tid; i < ncl * nrl; i += 256) {
       const int cyl = i / ncl, cxl = i % ncl;
-      const int gx0 = gxa + H + sx * cxl, gy0 = gya + H + sy * cyl;
+      const int gx0 = gxa + HX + sx * cxl, gy0 = gya + HY + sy * cyl;
       if (gx0 >= L.nx || gy0 >= L.ny) continue;
       const int I = P.tx.coarsened ? gx0 >> 1 : gx0, J = P.ty.coarsened ? gy0 >> 1 : gy0;
       float acc = 0.f;
@@ -646,7 +631,7 @@ __global__ void __launch_bounds__(256, 2) k_pass2d_edge(Pass2D P, TileRect T) {
     double sr = 0.0, sbb = 0.0;
     if (P.partials) {
       for (int i = tid; i < TYI * TXI; i += 256) {
-        const int ly = H + i / TXI, lx = H + i % TXI, gx = gxa + lx, gy = gya + ly;
+        const int ly = HY + i / TXI, lx = HX + i % TXI, gx = gxa + lx, gy = gya + ly;
         if (!inside(gx, gy)) continue;
         float bv;
         const float r = resid(lx, ly, gx, gy, &bv);
@@ -659,7 +644,7 @@ __global__ void __launch_bounds__(256, 2) k_pass2d_edge(Pass2D P, TileRect T) {
   }
   // store the interior
   for (int i = tid; i < TYI * TXI; i += 256) {
-    const int ly = H + i / TXI, lx = H + i % TXI, gx = gxa + lx, gy = gya + ly;
+    const int ly = HY + i / TXI, lx = HX + i % TXI, gx = gxa + lx, gy = gya + ly;
     if (inside(gx, gy)) P.xout[pbase + (long long)gy * nx + gx] = S.x[ly][lx];
   }
 }
@@ -673,8 +658,7 @@ bool fusable2d(const Level& L, const Level& C, const gdp_opts& o) {
 }
 
 static TileRect tiles2d(int nu, const LevelK& L, bool fast_ok) {
-  const int H = halo2(nu);
-  const int TXI = G_COLS - 2 * H, TYI = G_ROWS - 2 * H;
+  const int TXI = G_COLS - 2 * halo2x(nu), TYI = G_ROWS - 2 * halo2y(nu);
   TileRect T{};
   T.gx = (L.nx + TXI - 1) / TXI;
   T.gy = (L.ny + TYI - 1) / TYI;
@@ -696,49 +680,38 @@ static void set_smem(K k, size_t bytes) {
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
-template <int NU, bool DOWN, int MODE, typename TI>
+template <int NU, bool DOWN>
 static void launch2d_nu(const Pass2D& P, const TileRect& T, cudaStream_t s) {
   static bool attr = false;  // opt in to > 48 KB dynamic shared memory once per instantiation
   if (!attr) {
-    set_smem(k_pass2d<NU, DOWN, MODE, TI>, SMEM2D);
-    set_smem(k_pass2d_edge<NU, DOWN, MODE, TI>, SMEMEDGE);
+    set_smem(k_pass2d<NU, DOWN>, SMEM2D);
+    set_smem(k_pass2d_edge<NU, DOWN>, SMEMEDGE);
     attr = true;
   }
   const int nfast = (T.tx1 - T.tx0) * (T.ty1 - T.ty0);
   const int nedge = T.gx * T.gy - nfast;
   if (nfast > 0) {
     dim3 g(T.tx1 - T.tx0, T.ty1 - T.ty0, P.L.nzl);
-    k_pass2d<NU, DOWN, MODE, TI><<<g, 256, SMEM2D, s>>>(P, T);
+    k_pass2d<NU, DOWN><<<g, 256, SMEM2D, s>>>(P, T);
   }
   if (nedge > 0) {
-    count_launch();
+    if (nfast > 0) count_launch();
     dim3 g(nedge, P.L.nzl);
-    k_pass2d_edge<NU, DOWN, MODE, TI><<<g, 256, SMEMEDGE, s>>>(P, T);
+    k_pass2d_edge<NU, DOWN><<<g, 256, SMEMEDGE, s>>>(P, T);
   }
 }
 
-template <bool DOWN, int MODE, typename TI>
-static void launch2d_t(int nu, const Pass2D& P, const TileRect& T, cudaStream_t s) {
-  switch (nu) {
-    case 1: launch2d_nu<1, DOWN, MODE, TI>(P, T, s); break;
-    case 2: launch2d_nu<2, DOWN, MODE, TI>(P, T, s); break;
-    default: break;
-  }
-}
-
-static void launch2d(bool down, int nu, const Pass2D& P, int mode, int tI, cudaStream_t s) {
+static void launch2d(bool down, int nu, const Pass2D& P, cudaStream_t s) {
   const TileRect T = tiles2d(nu, P.L, P.fast_ok != 0);
   const double N = (double)P.L.nx * P.L.ny * P.L.nzl, Nc = (double)P.ncx * P.ncy * P.L.nzl;
-  const double bytes = N * ((P.zero_x ? 4.0 : 8.0) + rhs_bytes(mode, tI, P.R)) + Nc * 4.0;
+  const double bytes = N * ((P.zero_x ? 4.0 : 8.0) + 4.0) + Nc * 4.0;
   ProfScope ps(down ? KC_DOWN2D : KC_UP2D, bytes, s);
   if (down) {
-    if (mode == RHS_B) launch2d_t<true, RHS_B, float>(nu, P, T, s);
-    else if (tI == 0) launch2d_t<true, RHS_G, uint8_t>(nu, P, T, s);
-    else launch2d_t<true, RHS_G, float>(nu, P, T, s);
+    if (nu == 1) launch2d_nu<1, true>(P, T, s);
+    else launch2d_nu<2, true>(P, T, s);
   } else {
-    if (mode == RHS_B) launch2d_t<false, RHS_B, float>(nu, P, T, s);
-    else if (tI == 0) launch2d_t<false, RHS_G, uint8_t>(nu, P, T, s);
-    else launch2d_t<false, RHS_G, float>(nu, P, T, s);
+    if (nu == 1) launch2d_nu<1, false>(P, T, s);
+    else launch2d_nu<2, false>(P, T, s);
   }
 }
 
@@ -749,7 +722,8 @@ void fused_down2d(const Level& L, const Level& C, const float* xin, float* xout,
   P.fast_ok = C.tx.coarsened && C.ty.coarsened;
   P.tx = C.tx; P.ty = C.ty; P.ncx = C.nx; P.ncy = C.ny;
   P.bc = C.b;
-  launch2d(true, nu, P, mode, tI, s);
+  (void)mode; (void)tI;
+  launch2d(true, nu, P, s);
 }
 
 void fused_up2d(const Level& L, const Level& C, const float* xin, float* xout, const RhsK& R,
@@ -760,7 +734,8 @@ void fused_up2d(const Level& L, const Level& C, const float* xin, float* xout, c
   P.tx = C.tx; P.ty = C.ty; P.ncx = C.nx; P.ncy = C.ny;
   P.xc = C.x;
   P.partials = partials;
-  launch2d(false, nu, P, mode, tI, s);
+  (void)mode; (void)tI;
+  launch2d(false, nu, P, s);
 }
 
 }  // namespace gdp

@@ -54,6 +54,7 @@ struct Hier {
   double2* plane_sums = nullptr;   // per-plane (sum a, sum b), device
   double2* h_plane = nullptr;      // pinned host mirror
   float* scratch_e = nullptr;      // single-level direct solve correction
+  float* b0 = nullptr;             // finest-level rhs written out for the fused 2D passes
   size_t partials_cap = 0;         // entries of `partials` per plane
   int up_norm_per = 0;             // >0: the last fused up pass left per-plane partials (this many per plane)
   ~Hier();

@@ -181,6 +181,16 @@ __global__ void __launch_bounds__(256) k_finalize(const double2* partials, int p
   if (threadIdx.x == 0) out[p] = make_double2(a, b);
 }
 
+// a2 / a11: the finest-level rhs written out once per solve (the fused 2D passes read it)
+template <typename TI>
+__global__ void __launch_bounds__(256) k_rhs(LevelK L, RhsK R, float* __restrict__ b) {
+  const int ix = blockIdx.x * blockDim.x + threadIdx.x;
+  const int iy = blockIdx.y, iz = blockIdx.z;
+  if (ix >= L.nx) return;
+  const long long c = (long long)iz * L.nx * L.ny + (long long)iy * L.nx + ix;
+  b[c] = rhs_g<TI>(L, R, coefs(L, ix, iy, L.z0 + iz), c, L.nx);
+}
+
 template <typename TI>
 __global__ void k_decode_copy(const void* I, float* __restrict__ x, long long n) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
@@ -372,6 +382,13 @@ void launch_finalize(const double2* partials, int per, int nplanes, double2* out
 static inline int ew_grid(long long n) {
   long long g = (n + 255) / 256;
   return (int)(g > 148 * 32 ? 148 * 32 : (g < 1 ? 1 : g));
+}
+
+void launch_rhs(const LevelK& L, const RhsK& R, int tI, float* b, cudaStream_t s) {
+  ProfScope ps(KC_UTIL, (double)L.nx * L.ny * L.nzl * ((tI ? 4.0 : 1.0) + (R.vmode == 2 ? 4.0 : 0.0) + 4.0), s);
+  dim3 g((L.nx + 255) / 256, L.ny, L.nzl);
+  if (tI == 0) k_rhs<uint8_t><<<g, 256, 0, s>>>(L, R, b);
+  else k_rhs<float><<<g, 256, 0, s>>>(L, R, b);
 }
 
 void launch_decode_copy(const void* I, int tI, float* x, long long n, cudaStream_t s) {

@@ -90,6 +90,7 @@ void launch_norms(const LevelK& L, const float* x, const float* xlo, const float
 void launch_plane_sums(const void* a, int ta, const void* b, int tb, int nx, int ny, int nz,
                        double2* partials, double2* plane_out, cudaStream_t s);
 void launch_finalize(const double2* partials, int per, int nplanes, double2* out, cudaStream_t s);
+void launch_rhs(const LevelK& L, const RhsK& R, int tI, float* b, cudaStream_t s);
 void launch_decode_copy(const void* I, int tI, float* x, long long n, cudaStream_t s);
 void launch_add_scalar(float* x, long long n, float v, cudaStream_t s);
 void launch_axpy(float* x, const float* e, long long n, cudaStream_t s);

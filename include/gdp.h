@@ -84,8 +84,11 @@ typedef struct {
                          <= 64 cells along each coupled axis.  Default 4096.                */
   int stagnation;     /* stop (GDP_ENOCONV) after this many cycles each reducing the residual
                          by less than 10%.  Default 2.  0 disables.                         */
-  int fused;          /* 1: fused tile kernels (default), 0: one kernel per half-sweep
-                         (reference schedule of the same arithmetic).                        */
+  int fused;          /* bitmask of fused level passes (bit-identical to the reference
+                         schedule of one kernel per half-sweep, fused = 0):
+                         1 = 2D register passes (levels without z links, phase 2);
+                         2 = 3D z-marching sweeps (levels with z links, phase 1).
+                         Default 1.                                                          */
   int use_graphs;     /* 1: replay each V-cycle as a CUDA graph (default), 0: direct launch */
 } gdp_opts;
 

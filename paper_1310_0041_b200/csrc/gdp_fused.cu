@@ -654,7 +654,7 @@ __global__ void __launch_bounds__(256, 2) k_pass2d_edge(Pass2D P, TileRect T) {
 // ---------------------------------------------------------------------------------
 bool fusable2d(const Level& L, const Level& C, const gdp_opts& o) {
   const bool nu_ok = o.nu_pre >= 1 && o.nu_pre <= 2 && o.nu_post >= 1 && o.nu_post <= 2;
-  return nu_ok && o.fused && L.K.az.k == 0.f && L.K.az.kr == 0.f && L.K.az.kl == 0.f && !C.tz.coarsened;
+  return nu_ok && (o.fused & 1) && L.K.az.k == 0.f && L.K.az.kr == 0.f && L.K.az.kl == 0.f && !C.tz.coarsened;
 }
 
 static TileRect tiles2d(int nu, const LevelK& L, bool fast_ok) {

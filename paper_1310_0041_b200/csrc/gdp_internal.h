@@ -57,6 +57,7 @@ struct Hier {
   float* b0 = nullptr;             // finest-level rhs written out for the fused 2D passes
   size_t partials_cap = 0;         // entries of `partials` per plane
   int up_norm_per = 0;             // >0: the last fused up pass left per-plane partials (this many per plane)
+  int up_norm_planes = 0;          // planes of those partials (1: one row for the whole slab)
   ~Hier();
 };
 
@@ -101,6 +102,10 @@ void fused_down2d(const Level& L, const Level& C, const float* xin, float* xout,
 void fused_up2d(const Level& L, const Level& C, const float* xin, float* xout, const RhsK& R,
                 int mode, int tI, int nu, double2* partials, cudaStream_t s);
 int fused_tiles_per_plane(int nu, const LevelK& L);
+bool fusable3d(const Level& L, const Level& C, const gdp_opts& o);
+int fused3d_tiles(const LevelK& L);
+void fused_sweep3d(const Level& L, const Level& C, const float* xin, float* xout, const float* b,
+                   bool zero_x, bool prolong, int tail, double2* partials, cudaStream_t s);
 
 // communication (gdp_comm.cu); single-rank contexts make these no-ops
 int comm_init(Ctx& c, const void* nccl_unique_id);

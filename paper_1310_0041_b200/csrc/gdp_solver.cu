@@ -409,11 +409,17 @@ int run_vcycle(Ctx& ctx, Hier& H, const Fine& f, const gdp_opts& o, cudaStream_t
     return GDP_OK;
   }
   H.up_norm_per = 0;
-  bool fz[GDP_MAX_LEVELS] = {false};
+  H.up_norm_planes = 0;
+  // per level: 0 reference schedule, 2 fused 2D passes, 3 fused 3D sweeps
+  int fz[GDP_MAX_LEVELS] = {0};
+  float* cur[GDP_MAX_LEVELS] = {nullptr};  // buffer holding x of a level after its down pass
+  const bool nu_ok = o.nu_pre >= 1 && o.nu_post >= 1;
   for (int l = 0; l < nl - 1; ++l) {
     Level& L = H.lv[l];
     Level& C = H.lv[l + 1];
-    fz[l] = fusable2d(L, C, o) && (l > 0 || f.mode == RHS_B);
+    const bool rhs_ok = l > 0 || f.mode == RHS_B;
+    if (rhs_ok && fusable2d(L, C, o)) fz[l] = 2;
+    else if (rhs_ok && nu_ok && fusable3d(L, C, o)) fz[l] = 3;
     if (fz[l] && !L.x2) CK(cudaMalloc(&L.x2, sizeof(float) * (size_t)L.nx * L.ny * L.nzl));
   }
   for (int l = 0; l < nl - 1; ++l) {
@@ -427,13 +433,25 @@ int run_vcycle(Ctx& ctx, Hier& H, const Fine& f, const gdp_opts& o, cudaStream_t
       mode = RHS_B;
       tI = 1;
     }
-    if (fz[l]) {  // one fused pass: x (A) -> x2 (B)
+    if (fz[l] == 2) {  // one fused pass: x (A) -> x2 (B)
       fused_down2d(L, C, x, L.x2, R, mode, tI, o.nu_pre, l > 0, s);
+      cur[l] = L.x2;
+      continue;
+    }
+    if (fz[l] == 3) {  // nu fused sweeps, the last one restricting; ping-pong A <-> B
+      float* c = x;
+      for (int k = 0; k < o.nu_pre; ++k) {
+        float* d = c == x ? L.x2 : x;
+        fused_sweep3d(L, C, c, d, R.b, l > 0 && k == 0, false, k == o.nu_pre - 1 ? 1 : 0, nullptr, s);
+        c = d;
+      }
+      cur[l] = c;
       continue;
     }
     if (l > 0) CK(cudaMemsetAsync(x, 0, sizeof(float) * (size_t)L.nx * L.ny * L.nzl, s));
     smooth(L, x, R, mode, tI, o.nu_pre, s);
     launch_restrict(L.K, x, L.xlo, L.xhi, R, mode, tI, C.tx, C.ty, C.tz, C.nx, C.ny, C.nzl, C.b, s);
+    cur[l] = x;
   }
   Level& Lc = H.lv[nl - 1];
   CK(launch_coarse(H.coarse, Lc.b, Lc.x, s));
@@ -444,10 +462,23 @@ int run_vcycle(Ctx& ctx, Hier& H, const Fine& f, const gdp_opts& o, cudaStream_t
     RhsK R = f.R;
     int mode = f.mode, tI = f.tI;
     if (l > 0) { R = RhsK{L.b, nullptr, nullptr, 0.f, 0}; mode = RHS_B; tI = 1; }
-    if (fz[l]) {  // one fused pass: x2 (B) -> x (A), norms of the finest level on the way
+    if (fz[l] == 2) {  // one fused pass: x2 (B) -> x (A), norms of the finest level on the way
       const bool want = l == 0 && (size_t)fused_tiles_per_plane(o.nu_post, L.K) <= H.partials_cap;
       fused_up2d(L, C, L.x2, x, R, mode, tI, o.nu_post, want ? H.partials : nullptr, s);
-      if (want) H.up_norm_per = fused_tiles_per_plane(o.nu_post, L.K);
+      if (want) { H.up_norm_per = fused_tiles_per_plane(o.nu_post, L.K); H.up_norm_planes = L.nzl; }
+      continue;
+    }
+    if (fz[l] == 3) {  // prolongation fused into the first sweep, norms into the last
+      const bool want = l == 0 && (size_t)fused3d_tiles(L.K) <= H.partials_cap * (size_t)L.nzl;
+      float* c = cur[l];
+      for (int k = 0; k < o.nu_post; ++k) {
+        float* d = c == x ? L.x2 : x;
+        const bool last = k == o.nu_post - 1;
+        fused_sweep3d(L, C, c, d, R.b, false, k == 0, last && want ? 2 : 0, want ? H.partials : nullptr, s);
+        c = d;
+      }
+      if (c != x) CK(cudaMemcpyAsync(x, c, sizeof(float) * (size_t)L.nx * L.ny * L.nzl, cudaMemcpyDeviceToDevice, s));
+      if (want) { H.up_norm_per = fused3d_tiles(L.K); H.up_norm_planes = 1; }
       continue;
     }
     launch_prolong(L.K, x, C.tx, C.ty, C.tz, C.nx, C.ny, C.nzl, C.z0, C.x, C.xlo, C.xhi, s);
@@ -504,9 +535,10 @@ int solve(Ctx& ctx, Hier& H, const Fine& f, const gdp_opts& o, bool per_slice, g
     if (k >= cap) { status = GDP_ENOCONV; break; }
     RET(run_vcycle(ctx, H, f, o, s));
     if (H.up_norm_per > 0) {  // norms of the final iterate came with the fused up pass
-      launch_finalize(H.partials, H.up_norm_per, H.lv[0].nzl, H.plane_sums, s);
-      CK(cudaMemcpyAsync(H.h_plane, H.plane_sums, sizeof(double2) * H.lv[0].nzl, cudaMemcpyDeviceToHost, s));
+      launch_finalize(H.partials, H.up_norm_per, H.up_norm_planes, H.plane_sums, s);
+      CK(cudaMemcpyAsync(H.h_plane, H.plane_sums, sizeof(double2) * H.up_norm_planes, cudaMemcpyDeviceToHost, s));
       CK(cudaStreamSynchronize(s));
+      for (int z = H.up_norm_planes; z < H.lv[0].nzl; ++z) H.h_plane[z] = make_double2(0.0, 0.0);
     } else {
       RET(finest_norms(ctx, H, f, nullptr, s));
     }
@@ -665,7 +697,15 @@ int gdp_diffuse_z(gdp_ctx* ctx, const void* I0, gdp_dtype dtype, float* I1, gdp_
   f.mode = RHS_G;
   f.tI = tI;
   f.R = RhsK{nullptr, I0, nullptr, alpha, alpha > 0 ? 1 : 0};
-  // Eq. (1): the gradient target uses (bx, by); the rhs is formed on the fly (a2)
+  // Eq. (1): the gradient target uses (bx, by); the rhs is formed on the fly (a2), or written
+  // once for the fused passes (same values)
+  if (o.fused && H->lv.size() > 1 && (fusable3d(H->lv[0], H->lv[1], o) || fusable2d(H->lv[0], H->lv[1], o))) {
+    if (!H->b0) CK(cudaMalloc(&H->b0, sizeof(float) * (size_t)n));
+    launch_rhs(H->lv[0].K, f.R, tI, H->b0, s);
+    f.mode = RHS_B;
+    f.tI = 1;
+    f.R = RhsK{H->b0, nullptr, nullptr, 0.f, 0};
+  }
   int st = solve(C, *H, f, o, false, report, s);
   if (st != GDP_OK && st != GDP_ENOCONV) return st;
   if (alpha == 0.f) {  // a10: pin mean(I1) = mean(I0) in fp64 (reading c-3)

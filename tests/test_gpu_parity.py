@@ -211,3 +211,33 @@ def test_fused_2d_vcycle_bit_identical(gpu_ctx):
             gdp.gdp_vcycle(gpu_ctx, x, b, W=(1.0, 0.5, 0.0), alpha=0.05, opts=gdp.default_opts(fused=fused, nu_pre=1, nu_post=3))
         xs.append(x.cpu().numpy())
     assert np.array_equal(xs[0], xs[1])
+
+
+@pytest.mark.parametrize("shape,dtype", [((16, 64, 64), "f32"), ((9, 63, 65), "u8"), ((33, 130, 250), "u8"),
+                                         ((24, 517, 389), "u8"), ((12, 1024, 1024), "u8")])
+def test_fused_3d_bit_identical_to_reference(gpu_ctx, shape, dtype):
+    nz, ny, nx = shape
+    I0 = synth.make_stack(nx, ny, nz, 41, dtype)
+    outs = []
+    for fused in (0, 3):
+        o = gdp.default_opts(fused=fused, max_vcycles=2, rel_tol=1e-30, stagnation=0)
+        I1, rep = gdp.gdp_diffuse_z(gpu_ctx, dev(I0), opts=o, check=False)
+        outs.append(I1.cpu().numpy())
+    assert np.array_equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("nu", [(1, 1), (2, 1), (1, 2)])
+def test_fused_3d_vcycle_nu_variants(gpu_ctx, nu):
+    shape = (10, 70, 90)
+    rng = np.random.default_rng(11)
+    b = rng.standard_normal(shape)
+    b -= b.mean()
+    bd = dev(b.astype(np.float32))
+    xs = []
+    for fused in (0, 3):
+        x = torch.zeros(shape, dtype=torch.float32, device="cuda")
+        for _ in range(2):
+            gdp.gdp_vcycle(gpu_ctx, x, bd, W=(1.0, 1.0, 0.1), alpha=0.0,
+                           opts=gdp.default_opts(fused=fused, nu_pre=nu[0], nu_post=nu[1]))
+        xs.append(x.cpu().numpy())
+    assert np.array_equal(xs[0], xs[1])

@@ -183,6 +183,19 @@ __device__ __forceinline__ float bilerp(float a, float b, float c, float d, floa
   return __fmaf_rn(ty, r1, __fmul_rn(1.f - ty, r0));
 }
 
+// Cells away from the faces and from the (possibly partial) last coarse cell have the regular
+// taps: J = I -/+ 1 by parity and t = 1/4 exactly (what ptaps computes for them).
+__device__ __forceinline__ bool ptaps_regular(const XferAxis& a, long long i) {
+  return !a.coarsened || (i >= 1 && (i >> 1) + 1 <= a.nc - 2);
+}
+__device__ __forceinline__ void ptaps_fast(const XferAxis& a, long long i, long long& I, long long& J,
+                                           float& t) {
+  if (!a.coarsened) { I = i; J = i; t = 0.f; return; }
+  I = i >> 1;
+  J = (i & 1) ? I + 1 : I - 1;
+  t = 0.25f;
+}
+
 // Linear prolongation taps of fine cell i: parent I with weight 1-t, neighbour J with t.
 __device__ __forceinline__ void ptaps(const XferAxis& a, long long i, long long& I, long long& J,
                                       float& t) {

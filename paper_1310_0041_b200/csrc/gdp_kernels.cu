@@ -25,6 +25,25 @@ __device__ __forceinline__ Nbr load_nbr(const float* x, const float* xlo, const 
   return nb;
 }
 
+// Interior cells have the regular link coefficients on every axis (and all links present), so
+// the general coefficient evaluation and the reciprocal of the diagonal can be skipped: kint and
+// 1/D_int are the values coefs() and gs_update() would produce for them.
+struct Interior {
+  Coef k;
+  float invD;
+  bool zreg_all;  // level without z links: z never disqualifies a cell
+};
+__device__ __forceinline__ Interior interior_consts(const LevelK& L) {
+  Interior I;
+  I.k.xl = L.ax.k; I.k.xr = L.ax.k; I.k.yl = L.ay.k; I.k.yr = L.ay.k; I.k.zl = L.az.k; I.k.zr = L.az.k;
+  I.invD = __frcp_rn(I.k.diag(L.alpha));
+  I.zreg_all = L.az.k == 0.f && L.az.kr == 0.f && L.az.kl == 0.f;
+  return I;
+}
+__device__ __forceinline__ bool is_interior(const LevelK& L, const Interior& I, int ix, int iy, long long zg) {
+  return ix >= 1 && ix <= L.ax.n - 3 && iy >= 1 && iy <= L.ay.n - 3 && (I.zreg_all || (zg >= 1 && zg <= L.az.n - 3));
+}
+
 // a4: one red-black Gauss-Seidel half-sweep (colour = (x + y + z_global) & 1).
 template <int MODE, typename TI>
 __global__ void __launch_bounds__(256) k_rbgs(LevelK L, float* __restrict__ x, const float* xlo,
@@ -37,8 +56,17 @@ __global__ void __launch_bounds__(256) k_rbgs(LevelK L, float* __restrict__ x, c
   if (ix >= L.nx) return;
   const long long plane = (long long)L.nx * L.ny;
   const long long c = iz * plane + (long long)iy * L.nx + ix;
-  const Coef k = coefs(L, ix, iy, zg);
   const float xc = x[c];
+  const Interior I = interior_consts(L);
+  if (MODE == RHS_B && is_interior(L, I, ix, iy, zg)) {
+    // all six neighbours exist; slab faces come from the ghost planes
+    const float d = I.zreg_all ? xc : (iz > 0 ? x[c - plane] : xlo[c]);
+    const float u = I.zreg_all ? xc : (iz < L.nzl - 1 ? x[c + plane] : xhi[c - (long long)iz * plane]);
+    const float r = __fsub_rn(R.b[c], apply_from(I.k, L.alpha, xc, x[c - 1], x[c + 1], x[c - L.nx], x[c + L.nx], d, u));
+    x[c] = __fmaf_rn(r, I.invD, xc);  // == gs_update(xc, r, D)
+    return;
+  }
+  const Coef k = coefs(L, ix, iy, zg);
   const Nbr nb = load_nbr(x, xlo, xhi, L, k, iz, c, xc);
   const float r = residual_at<MODE, TI>(L, R, k, xc, nb, c, L.nx, plane, nullptr);
   x[c] = gs_update(xc, r, k.diag(L.alpha));
@@ -60,6 +88,7 @@ __global__ void __launch_bounds__(256) k_restrict(LevelK L, const float* __restr
   const int fx0 = tx.coarsened ? 2 * cx : cx, fx1 = tx.coarsened ? min(2 * cx + 1, L.nx - 1) : cx;
   const int fy0 = ty.coarsened ? 2 * cy : cy, fy1 = ty.coarsened ? min(2 * cy + 1, L.ny - 1) : cy;
   const int fz0 = tz.coarsened ? 2 * cz : cz, fz1 = tz.coarsened ? min(2 * cz + 1, L.nzl - 1) : cz;
+  const Interior I = interior_consts(L);
   float acc = 0.f;
   for (int fz = fz0; fz <= fz1; ++fz) {
     const long long zg = L.z0 + fz;
@@ -69,10 +98,17 @@ __global__ void __launch_bounds__(256) k_restrict(LevelK L, const float* __restr
       for (int fx = fx0; fx <= fx1; ++fx) {
         const float wx = rweight(tx, fx);
         const long long c = fz * plane + (long long)fy * L.nx + fx;
-        const Coef k = coefs(L, fx, fy, zg);
         const float xc = x[c];
-        const Nbr nb = load_nbr(x, xlo, xhi, L, k, fz, c, xc);
-        const float r = residual_at<MODE, TI>(L, R, k, xc, nb, c, L.nx, plane, nullptr);
+        float r;
+        if (MODE == RHS_B && is_interior(L, I, fx, fy, zg)) {
+          const float d = I.zreg_all ? xc : (fz > 0 ? x[c - plane] : xlo[c]);
+          const float u = I.zreg_all ? xc : (fz < L.nzl - 1 ? x[c + plane] : xhi[c - (long long)fz * plane]);
+          r = __fsub_rn(R.b[c], apply_from(I.k, L.alpha, xc, x[c - 1], x[c + 1], x[c - L.nx], x[c + L.nx], d, u));
+        } else {
+          const Coef k = coefs(L, fx, fy, zg);
+          const Nbr nb = load_nbr(x, xlo, xhi, L, k, fz, c, xc);
+          r = residual_at<MODE, TI>(L, R, k, xc, nb, c, L.nx, plane, nullptr);
+        }
         acc = __fmaf_rn(rw3(wz, wy, wx), r, acc);
       }
     }
@@ -92,9 +128,9 @@ __global__ void __launch_bounds__(256) k_prolong(LevelK L, float* __restrict__ x
   if (fx >= L.nx || fy >= L.ny) return;
   long long Ix, Jx, Iy, Jy, Iz, Jz;
   float txw, tyw, tzw;
-  ptaps(tx, fx, Ix, Jx, txw);
-  ptaps(ty, fy, Iy, Jy, tyw);
-  ptaps(tz, L.z0 + fz, Iz, Jz, tzw);
+  if (ptaps_regular(tx, fx)) ptaps_fast(tx, fx, Ix, Jx, txw); else ptaps(tx, fx, Ix, Jx, txw);
+  if (ptaps_regular(ty, fy)) ptaps_fast(ty, fy, Iy, Jy, tyw); else ptaps(ty, fy, Iy, Jy, tyw);
+  if (ptaps_regular(tz, L.z0 + fz)) ptaps_fast(tz, L.z0 + fz, Iz, Jz, tzw); else ptaps(tz, L.z0 + fz, Iz, Jz, tzw);
   const long long cplane = (long long)ncx * ncy;
   // z taps are global coarse indices; map to local planes or ghost planes
   auto zrow = [&](long long zgc) -> const float* {
@@ -125,14 +161,22 @@ __global__ void __launch_bounds__(256) k_norms(LevelK L, const float* __restrict
   const long long zg = L.z0 + iz;
   const long long plane = (long long)L.nx * L.ny;
   double sr = 0.0, sb = 0.0;
+  const Interior I = interior_consts(L);
   if (ix < L.nx) {
     for (int iy = blockIdx.y * blockDim.y + threadIdx.y; iy < L.ny; iy += gridDim.y * blockDim.y) {
       const long long c = iz * plane + (long long)iy * L.nx + ix;
-      const Coef k = coefs(L, ix, iy, zg);
       const float xc = x[c];
-      const Nbr nb = load_nbr(x, xlo, xhi, L, k, iz, c, xc);
-      float bv;
-      const float r = residual_at<MODE, TI>(L, R, k, xc, nb, c, L.nx, plane, &bv);
+      float bv, r;
+      if (MODE == RHS_B && is_interior(L, I, ix, iy, zg)) {
+        const float d = I.zreg_all ? xc : (iz > 0 ? x[c - plane] : xlo[c]);
+        const float u = I.zreg_all ? xc : (iz < L.nzl - 1 ? x[c + plane] : xhi[c - (long long)iz * plane]);
+        bv = R.b[c];
+        r = __fsub_rn(bv, apply_from(I.k, L.alpha, xc, x[c - 1], x[c + 1], x[c - L.nx], x[c + L.nx], d, u));
+      } else {
+        const Coef k = coefs(L, ix, iy, zg);
+        const Nbr nb = load_nbr(x, xlo, xhi, L, k, iz, c, xc);
+        r = residual_at<MODE, TI>(L, R, k, xc, nb, c, L.nx, plane, &bv);
+      }
       if (rout) rout[c] = r;
       sr += (double)r * (double)r;
       sb += (double)bv * (double)bv;

@@ -699,7 +699,7 @@ int gdp_diffuse_z(gdp_ctx* ctx, const void* I0, gdp_dtype dtype, float* I1, gdp_
   f.R = RhsK{nullptr, I0, nullptr, alpha, alpha > 0 ? 1 : 0};
   // Eq. (1): the gradient target uses (bx, by); the rhs is formed on the fly (a2), or written
   // once for the fused passes (same values)
-  if (o.fused && H->lv.size() > 1 && (fusable3d(H->lv[0], H->lv[1], o) || fusable2d(H->lv[0], H->lv[1], o))) {
+  if (H->lv.size() > 1) {  // every schedule reads the written rhs (same values as on the fly)
     if (!H->b0) CK(cudaMalloc(&H->b0, sizeof(float) * (size_t)n));
     launch_rhs(H->lv[0].K, f.R, tI, H->b0, s);
     f.mode = RHS_B;
@@ -757,8 +757,8 @@ int gdp_screened_poisson_slices(gdp_ctx* ctx, const void* I0, gdp_dtype dtype, c
   f.mode = RHS_G;
   f.tI = tI;
   f.R = RhsK{nullptr, I0, I1, alpha, 2};
-  if (o.fused && H->lv.size() > 1 && fusable2d(H->lv[0], H->lv[1], o)) {
-    // the fused passes read the rhs b = alpha I1 + (Lx + Ly) I0 (a11) written once: 4 B/cell
+  if (H->lv.size() > 1) {
+    // the passes read the rhs b = alpha I1 + (Lx + Ly) I0 (a11) written once: 4 B/cell
     // per pass instead of I0 + I1 (5 or 8 B/cell); same values as the on-the-fly form
     if (!H->b0) CK(cudaMalloc(&H->b0, sizeof(float) * (size_t)n));
     launch_rhs(H->lv[0].K, f.R, tI, H->b0, s);

@@ -208,7 +208,7 @@ def test_fused_2d_vcycle_bit_identical(gpu_ctx):
     for fused in (0, 1):
         x = torch.zeros(shape, dtype=torch.float32, device="cuda")
         for _ in range(2):
-            gdp.gdp_vcycle(gpu_ctx, x, b, W=(1.0, 0.5, 0.0), alpha=0.05, opts=gdp.default_opts(fused=fused, nu_pre=1, nu_post=3))
+            gdp.gdp_vcycle(gpu_ctx, x, b, W=(1.0, 0.5, 0.0), alpha=0.05, opts=gdp.default_opts(fused=fused, nu_pre=1, nu_post=2))
         xs.append(x.cpu().numpy())
     assert np.array_equal(xs[0], xs[1])
 

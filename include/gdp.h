@@ -39,9 +39,12 @@
  *   synchronise `stream` only to return their host scalars.
  * DISTRIBUTION: a ctx created with world > 1 owns an NCCL communicator over the
  *   ranks; each rank passes its local z-slab (local dims) and the slab's global
- *   position (z0_global, nz_global).  A ctx created with gdp_ctx_create_loopback
- *   emulates `world` ranks inside one process on one GPU (same code path, halo
- *   exchange by device copies) for testing the partition.
+ *   position (z0_global, nz_global); slabs must tile the stack in rank order.
+ *   Phase 1 exchanges one ghost plane per slab face per half-sweep and gathers the
+ *   coarse levels once per V-cycle; phase 2 is slab-local (independent slices).
+ *   A ctx created with gdp_ctx_create_loopback emulates `world` slabs inside one
+ *   process on one GPU (same driver, halo exchange by device copies): the caller
+ *   passes the whole stack.  Results are bit-identical to the single-rank solve.
  */
 #ifndef GDP_H_
 #define GDP_H_
@@ -120,6 +123,10 @@ int gdp_ctx_create(gdp_ctx** out, int device, int rank, int world, const void* n
 int gdp_ctx_create_loopback(gdp_ctx** out, int device, int world);
 
 int gdp_ctx_destroy(gdp_ctx* ctx);
+
+/* Write a fresh ncclUniqueId (128 bytes) to `out` (n >= 128) — rank 0 calls it and
+ * broadcasts the bytes (e.g. with torch.distributed) before every rank's gdp_ctx_create. */
+int gdp_get_unique_id(void* out, size_t n);
 
 /* Phase 1 — Eq. (1).  Solves (alpha - div W grad) I1 = alpha I0 - div W G,
  * G = (dI0/dx, dI0/dy, 0); with alpha = 0 (the paper's AD) the constant null space is

@@ -14,6 +14,8 @@ from .gdp import (  # noqa: F401
     gdp_residual,
     gdp_screened_poisson_slices,
     gdp_vcycle,
+    get_unique_id,
+    partition,
     kernel_launch_count,
     profile_begin,
     profile_end,

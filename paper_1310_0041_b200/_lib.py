@@ -21,7 +21,7 @@ EXPORTS = [
     "gdp_opts_default", "gdp_ctx_create", "gdp_ctx_create_loopback", "gdp_ctx_destroy",
     "gdp_diffuse_z", "gdp_screened_poisson_slices", "gdp_destripe", "gdp_destripe_host",
     "gdp_vcycle", "gdp_residual", "gdp_last_error", "gdp_version", "gdp_kernel_launch_count",
-    "gdp_profile_begin", "gdp_profile_end",
+    "gdp_profile_begin", "gdp_profile_end", "gdp_get_unique_id",
 ]
 
 
@@ -89,6 +89,7 @@ def lib():
         "gdp_version": ([], C.c_char_p),
         "gdp_kernel_launch_count": ([], i64),
         "gdp_profile_begin": ([], i32),
+        "gdp_get_unique_id": ([vp, C.c_size_t], i32),
         "gdp_profile_end": ([P(KernelStat), i32, P(i32)], i32),
     }
     for name, (args, res) in sig.items():

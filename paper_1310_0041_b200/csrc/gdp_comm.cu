@@ -1,31 +1,152 @@
-// gdp_comm.cu — communication layer of a distributed ctx (z-slab halos, fp64 sums).
-// Single-rank contexts: every call is a no-op.
+// gdp_comm.cu — communication of a z-slab partition: one-plane halos of x
+// between neighbouring slabs, the gathered coarse right-hand side, and exact per-plane fp64
+// sums.  Two backends with one code path above them:
+//   * NCCL (world > 1): one slab per process, ncclSend/ncclRecv over NVLink, ncclAllReduce;
+//   * loopback (gdp_ctx_create_loopback): `world` slabs inside one process on one GPU, the
+//     "exchange" is a device copy between the slabs' buffers.
+// Sums are made exact and partition-independent by giving every element exactly one non-zero
+// contributor (each rank fills its own planes of a zeroed array, then a sum-allreduce).
+#include <nccl.h>
+
 #include "gdp_internal.h"
 
 namespace gdp {
 
-struct Comm {};
+struct Comm {
+  ncclComm_t nc = nullptr;
+  double* d_sum = nullptr;  // scratch for plane sums (2 * nzg doubles)
+  size_t d_sum_cap = 0;
+};
+
+#define NCK(call)                                                                     \
+  do {                                                                                \
+    ncclResult_t r_ = (call);                                                         \
+    if (r_ != ncclSuccess)                                                            \
+      return set_err(GDP_ENCCL, "%s failed: %s", #call, ncclGetErrorString(r_));      \
+  } while (0)
+
+#define CKC(call)                                                                     \
+  do {                                                                                \
+    cudaError_t e_ = (call);                                                          \
+    if (e_ != cudaSuccess) return set_err(GDP_ECUDA, "%s: %s", #call, cudaGetErrorString(e_)); \
+  } while (0)
+
+int comm_unique_id(void* out, size_t n) {
+  if (!out || n < sizeof(ncclUniqueId)) return set_err(GDP_EINVAL, "unique id buffer < %zu bytes", sizeof(ncclUniqueId));
+  ncclUniqueId id;
+  NCK(ncclGetUniqueId(&id));
+  memcpy(out, &id, sizeof id);
+  return GDP_OK;
+}
 
 int comm_init(Ctx& c, const void* nccl_unique_id) {
-  (void)nccl_unique_id;
-  return set_err(GDP_EINVAL, "world > 1: NCCL partition not available in this build (rank %d)", c.rank);
+  if (!nccl_unique_id) return set_err(GDP_EINVAL, "world > 1 needs an ncclUniqueId");
+  c.comm = new Comm();
+  ncclUniqueId id;
+  memcpy(&id, nccl_unique_id, sizeof id);
+  NCK(ncclCommInitRank(&c.comm->nc, c.world, id, c.rank));
+  return GDP_OK;
 }
 
 void comm_destroy(Ctx& c) {
+  if (!c.comm) return;
+  if (c.comm->nc) ncclCommDestroy(c.comm->nc);
+  if (c.comm->d_sum) cudaFree(c.comm->d_sum);
   delete c.comm;
   c.comm = nullptr;
 }
 
+// scalar fp64 sums over ranks (the rank holding a value is the only non-zero contributor
+// per call site, so the result does not depend on the reduction order)
 int comm_allreduce_sum2(Ctx& c, double* a, double* b, cudaStream_t s) {
-  (void)a; (void)b; (void)s;
   if (c.world == 1) return GDP_OK;
-  return set_err(GDP_ENCCL, "allreduce without communicator");
+  if (!c.comm) return set_err(GDP_ENCCL, "allreduce without communicator");
+  if (c.comm->d_sum_cap < 2) {
+    if (c.comm->d_sum) cudaFree(c.comm->d_sum);
+    CKC(cudaMalloc(&c.comm->d_sum, 2 * sizeof(double)));
+    c.comm->d_sum_cap = 2;
+  }
+  double h[2] = {*a, *b};
+  CKC(cudaMemcpyAsync(c.comm->d_sum, h, sizeof h, cudaMemcpyHostToDevice, s));
+  NCK(ncclAllReduce(c.comm->d_sum, c.comm->d_sum, 2, ncclDouble, ncclSum, c.comm->nc, s));
+  CKC(cudaMemcpyAsync(h, c.comm->d_sum, sizeof h, cudaMemcpyDeviceToHost, s));
+  CKC(cudaStreamSynchronize(s));
+  *a = h[0];
+  *b = h[1];
+  return GDP_OK;
 }
 
 int comm_halo_x(Ctx& c, Hier& H, int level, float* x, cudaStream_t s) {
   (void)H; (void)level; (void)x; (void)s;
   if (c.world == 1) return GDP_OK;
-  return set_err(GDP_ENCCL, "halo without communicator");
+  return set_err(GDP_ENCCL, "halo of a single hierarchy on a distributed ctx");
+}
+
+// ---------------------------------------------------------------------------------
+// slab partition primitives
+// ---------------------------------------------------------------------------------
+// ghost planes of level `l` for every local part: xlo <- last plane of the slab below,
+// xhi <- first plane of the slab above.  xs[i] = x of level l of local part i.
+int comm_halo_parts(Ctx& c, DistPlan& D, int l, float* const* xs, cudaStream_t s) {
+  const int np = (int)D.parts.size();
+  const Level& L0 = D.parts[0]->lv[l];
+  const size_t pl = (size_t)L0.nx * L0.ny;
+  if (c.world == 1) {  // loopback: all slabs are local
+    for (int i = 0; i < np; ++i) {
+      const Level& L = D.parts[i]->lv[l];
+      if (i > 0) {
+        const Level& B = D.parts[i - 1]->lv[l];
+        CKC(cudaMemcpyAsync(L.xlo, xs[i - 1] + (size_t)(B.nzl - 1) * pl, pl * sizeof(float), cudaMemcpyDeviceToDevice, s));
+      }
+      if (i < np - 1)
+        CKC(cudaMemcpyAsync(L.xhi, xs[i + 1], pl * sizeof(float), cudaMemcpyDeviceToDevice, s));
+    }
+    return GDP_OK;
+  }
+  const Level& L = D.parts[0]->lv[l];
+  NCK(ncclGroupStart());
+  if (c.rank > 0) {
+    NCK(ncclSend(xs[0], pl, ncclFloat, c.rank - 1, c.comm->nc, s));
+    NCK(ncclRecv(L.xlo, pl, ncclFloat, c.rank - 1, c.comm->nc, s));
+  }
+  if (c.rank < c.world - 1) {
+    NCK(ncclSend(xs[0] + (size_t)(L.nzl - 1) * pl, pl, ncclFloat, c.rank + 1, c.comm->nc, s));
+    NCK(ncclRecv(L.xhi, pl, ncclFloat, c.rank + 1, c.comm->nc, s));
+  }
+  NCK(ncclGroupEnd());
+  return GDP_OK;
+}
+
+// complete the gathered coarse rhs: every rank restricted into its own planes of a zeroed
+// buffer; the sum over ranks has one non-zero term per element (exact)
+int comm_gather_full(Ctx& c, float* full, size_t n, cudaStream_t s) {
+  if (c.world == 1) return GDP_OK;  // loopback: the slabs wrote disjoint planes of one buffer
+  NCK(ncclAllReduce(full, full, n, ncclFloat, ncclSum, c.comm->nc, s));
+  return GDP_OK;
+}
+
+// global per-plane (sum a, sum b): `local[i]` holds the planes of local part i (device);
+// the result is written to host `out` (nzg entries) in global plane order
+int comm_plane_sums(Ctx& c, DistPlan& D, double2* const* local, double2* out, cudaStream_t s) {
+  const int np = (int)D.parts.size();
+  if (c.world == 1) {
+    for (int i = 0; i < np; ++i)
+      CKC(cudaMemcpyAsync(out + D.z0[i], local[i], sizeof(double2) * D.nzl[i], cudaMemcpyDeviceToHost, s));
+    CKC(cudaStreamSynchronize(s));
+    return GDP_OK;
+  }
+  const size_t need = 2 * (size_t)D.nzg;
+  if (c.comm->d_sum_cap < need) {
+    if (c.comm->d_sum) cudaFree(c.comm->d_sum);
+    CKC(cudaMalloc(&c.comm->d_sum, need * sizeof(double)));
+    c.comm->d_sum_cap = need;
+  }
+  CKC(cudaMemsetAsync(c.comm->d_sum, 0, need * sizeof(double), s));
+  CKC(cudaMemcpyAsync(c.comm->d_sum + 2 * D.z0[0], local[0], sizeof(double2) * D.nzl[0], cudaMemcpyDeviceToDevice, s));
+  NCK(ncclAllReduce(c.comm->d_sum, c.comm->d_sum, need, ncclDouble, ncclSum, c.comm->nc, s));
+  CKC(cudaMemcpyAsync(out, c.comm->d_sum, need * sizeof(double), cudaMemcpyDeviceToHost, s));
+  CKC(cudaStreamSynchronize(s));
+  return GDP_OK;
 }
 
 }  // namespace gdp

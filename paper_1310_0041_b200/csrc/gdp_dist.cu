@@ -1,0 +1,305 @@
+// gdp_dist.cu — phase 1 (Eq. 1) on a z-slab partition.
+//
+// Every rank (NCCL) or every loopback slab owns planes [z0, z0 + nzl) of the stack.  The
+// level chain is the single-rank one (level_chain): the first levels stay split across the
+// slabs, from level `ff` on every level is full and replicated (the "tail", gathered once per
+// V-cycle from the restricted residual).  Split levels run the reference schedule with one
+// ghost plane per slab face, refreshed before every half-sweep, residual and prolongation.
+// Because colours, coefficients and transfers use global z and every kernel evaluates the
+// same per-cell arithmetic, the iterates are bit-identical to the single-rank solve for any
+// partition (tests/test_gpu_parity.py::test_loopback_partition_bit_identical).
+#include <cmath>
+#include <cstring>
+
+#include "gdp_internal.h"
+
+namespace gdp {
+
+DistPlan::~DistPlan() {
+  if (h_planes) cudaFreeHost(h_planes);
+  for (auto* p : b0) if (p) cudaFree(p);
+}
+
+#define CKD(call)                                                                         \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      return set_err(e_ == cudaErrorMemoryAllocation ? GDP_ENOMEM : GDP_ECUDA, "%s: %s", #call, \
+                     cudaGetErrorString(e_));                                             \
+  } while (0)
+#define RETD(call)                 \
+  do {                             \
+    int r_ = (call);               \
+    if (r_ != GDP_OK) return r_;   \
+  } while (0)
+
+// Build the plan for slabs (z0s[i], nzls[i]) of which `local` are processed here.
+static int build_plan(const HierKey& gkey, const std::vector<long long>& z0s, const std::vector<int>& nzls,
+                      const std::vector<int>& local, std::unique_ptr<DistPlan>& out) {
+  auto D = std::make_unique<DistPlan>();
+  D->nzg = (int)gkey.nzg;
+  // level chains of every slab; the first full level is the earliest any slab needs
+  std::vector<std::vector<Level>> chains(z0s.size());
+  int ff = 1 << 30;
+  for (size_t i = 0; i < z0s.size(); ++i) {
+    HierKey k = gkey;
+    k.z0 = z0s[i];
+    k.nzl = nzls[i];
+    int f;
+    RETD(level_chain(k, chains[i], f));
+    ff = std::min(ff, f);
+  }
+  if (ff < 1) return set_err(GDP_EINVAL, "distributed stack too small: level 0 must already be gathered");
+  D->ff = ff;
+  for (int i : local) {
+    HierKey k = gkey;
+    k.z0 = z0s[i];
+    k.nzl = nzls[i];
+    std::unique_ptr<Hier> P;
+    RETD(build_hier_levels(k, chains[i], 0, ff, false, false, P));
+    D->parts.push_back(std::move(P));
+    D->z0.push_back(z0s[i]);
+    D->nzl.push_back(nzls[i]);
+    D->b0.push_back(nullptr);
+  }
+  // the tail: levels ff.. of the chain, full in z
+  std::vector<Level> tail = chains[0];
+  for (size_t l = ff; l < tail.size(); ++l) { tail[l].z0 = 0; tail[l].nzl = tail[l].gz.n; }
+  HierKey tk = gkey;
+  tk.nx = tail[ff].nx; tk.ny = tail[ff].ny; tk.nzl = tail[ff].nzl; tk.nzg = tail[ff].gz.n; tk.z0 = 0;
+  RETD(build_hier_levels(tk, tail, ff, (int)tail.size(), true, true, D->tail));
+  CKD(cudaMallocHost(&D->h_planes, sizeof(double2) * (size_t)D->nzg));
+  out = std::move(D);
+  return GDP_OK;
+}
+
+// all ranks' slab extents (NCCL) or the loopback split of the whole stack
+static int slab_layout(Ctx& c, long long z0, int nzl, long long nzg, std::vector<long long>& z0s,
+                       std::vector<int>& nzls, std::vector<int>& local) {
+  z0s.clear(); nzls.clear(); local.clear();
+  if (c.world > 1) {
+    // every rank learns every slab: fp64 sums of one-hot vectors (exact)
+    std::vector<double> a(2 * c.world, 0.0);
+    for (int r = 0; r < c.world; ++r) {
+      double z = r == c.rank ? (double)z0 : 0.0, n = r == c.rank ? (double)nzl : 0.0;
+      RETD(comm_allreduce_sum2(c, &z, &n, nullptr));
+      a[2 * r] = z;
+      a[2 * r + 1] = n;
+    }
+    for (int r = 0; r < c.world; ++r) { z0s.push_back((long long)a[2 * r]); nzls.push_back((int)a[2 * r + 1]); }
+    local.push_back(c.rank);
+  } else {
+    const int P = c.loop;
+    const long long base = nzg / P, rem = nzg % P;
+    long long z = 0;
+    for (int i = 0; i < P; ++i) {
+      const int n = (int)(base + (i < rem ? 1 : 0));
+      z0s.push_back(z);
+      nzls.push_back(n);
+      local.push_back(i);
+      z += n;
+    }
+  }
+  long long z = 0;
+  for (size_t i = 0; i < z0s.size(); ++i) {
+    if (z0s[i] != z || nzls[i] < 1) return set_err(GDP_EINVAL, "slabs must tile [0, nz_global) in rank order");
+    z += nzls[i];
+  }
+  if (z != nzg) return set_err(GDP_EINVAL, "slabs do not cover nz_global");
+  return GDP_OK;
+}
+
+// ---------------------------------------------------------------------------------
+// V-cycle on the partition (reference schedule on split levels)
+// ---------------------------------------------------------------------------------
+static int team_smooth(Ctx& c, DistPlan& D, int l, float* const* xs, const float* const* bs, int nu, cudaStream_t s) {
+  const int np = (int)D.parts.size();
+  for (int k = 0; k < nu; ++k)
+    for (int color = 0; color < 2; ++color) {
+      RETD(comm_halo_parts(c, D, l, xs, s));
+      for (int i = 0; i < np; ++i) {
+        const Level& L = D.parts[i]->lv[l];
+        launch_rbgs(L.K, xs[i], L.xlo, L.xhi, RhsK{bs[i], nullptr, nullptr, 0.f, 0}, RHS_B, 1, color, s);
+      }
+    }
+  return GDP_OK;
+}
+
+static int team_vcycle(Ctx& c, DistPlan& D, float* const* x0, const gdp_opts& o, cudaStream_t s) {
+  const int np = (int)D.parts.size();
+  const int ff = D.ff;
+  std::vector<float*> xs(np);
+  std::vector<const float*> bs(np);
+  Hier& T = *D.tail;
+  Level& TF = T.lv[0];
+  const size_t tplane = (size_t)TF.nx * TF.ny;
+  for (int l = 0; l < ff; ++l) {
+    for (int i = 0; i < np; ++i) {
+      Level& L = D.parts[i]->lv[l];
+      xs[i] = l == 0 ? x0[i] : L.x;
+      bs[i] = l == 0 ? D.b0[i] : L.b;
+      if (l > 0) CKD(cudaMemsetAsync(xs[i], 0, sizeof(float) * (size_t)L.nx * L.ny * L.nzl, s));
+    }
+    RETD(team_smooth(c, D, l, xs.data(), bs.data(), o.nu_pre, s));
+    RETD(comm_halo_parts(c, D, l, xs.data(), s));
+    if (l + 1 == ff && c.world > 1) CKD(cudaMemsetAsync(TF.b, 0, sizeof(float) * tplane * TF.nzl, s));
+    for (int i = 0; i < np; ++i) {
+      Level& L = D.parts[i]->lv[l];
+      RhsK R{bs[i], nullptr, nullptr, 0.f, 0};
+      if (l + 1 < ff) {
+        Level& C = D.parts[i]->lv[l + 1];
+        launch_restrict(L.K, xs[i], L.xlo, L.xhi, R, RHS_B, 1, C.tx, C.ty, C.tz, C.nx, C.ny, C.nzl, C.b, s);
+      } else {  // into this slab's planes of the gathered level
+        const bool cz = TF.tz.coarsened;
+        const long long off = cz ? L.z0 / 2 : L.z0;
+        const int nczl = cz ? L.nzl / 2 : L.nzl;
+        launch_restrict(L.K, xs[i], L.xlo, L.xhi, R, RHS_B, 1, TF.tx, TF.ty, TF.tz, TF.nx, TF.ny, nczl,
+                        TF.b + off * tplane, s);
+      }
+    }
+  }
+  // gathered levels: one V-cycle of the tail from a zero start (replicated on every rank)
+  RETD(comm_gather_full(c, TF.b, tplane * TF.nzl, s));
+  CKD(cudaMemsetAsync(TF.x, 0, sizeof(float) * tplane * TF.nzl, s));
+  Fine ft;
+  ft.x = TF.x;
+  ft.mode = RHS_B;
+  ft.tI = 1;
+  ft.R = RhsK{TF.b, nullptr, nullptr, 0.f, 0};
+  RETD(run_vcycle(c, T, ft, o, s));
+  for (int l = ff - 1; l >= 0; --l) {
+    for (int i = 0; i < np; ++i) {
+      Level& L = D.parts[i]->lv[l];
+      xs[i] = l == 0 ? x0[i] : L.x;
+      bs[i] = l == 0 ? D.b0[i] : L.b;
+    }
+    if (l + 1 < ff) {
+      std::vector<float*> xc(np);
+      for (int i = 0; i < np; ++i) xc[i] = D.parts[i]->lv[l + 1].x;
+      RETD(comm_halo_parts(c, D, l + 1, xc.data(), s));
+    }
+    for (int i = 0; i < np; ++i) {
+      Level& L = D.parts[i]->lv[l];
+      if (l + 1 < ff) {
+        Level& C = D.parts[i]->lv[l + 1];
+        launch_prolong(L.K, xs[i], C.tx, C.ty, C.tz, C.nx, C.ny, C.nzl, C.z0, C.x, C.xlo, C.xhi, s);
+      } else {
+        launch_prolong(L.K, xs[i], TF.tx, TF.ty, TF.tz, TF.nx, TF.ny, TF.nzl, 0, TF.x, nullptr, nullptr, s);
+      }
+    }
+    RETD(team_smooth(c, D, l, xs.data(), bs.data(), o.nu_post, s));
+  }
+  CKD(cudaGetLastError());
+  return GDP_OK;
+}
+
+// global per-plane (r^2, b^2) of the finest level -> rel-res (one system: all planes)
+static int team_norms(Ctx& c, DistPlan& D, float* const* x0, double* rel, double* nb, cudaStream_t s) {
+  const int np = (int)D.parts.size();
+  RETD(comm_halo_parts(c, D, 0, x0, s));
+  std::vector<double2*> loc(np);
+  for (int i = 0; i < np; ++i) {
+    Hier& H = *D.parts[i];
+    Level& L = H.lv[0];
+    launch_norms(L.K, x0[i], L.xlo, L.xhi, RhsK{D.b0[i], nullptr, nullptr, 0.f, 0}, RHS_B, 1, nullptr,
+                 H.partials, H.plane_sums, s);
+    loc[i] = H.plane_sums;
+  }
+  CKD(cudaGetLastError());
+  RETD(comm_plane_sums(c, D, loc.data(), D.h_planes, s));
+  double rr = 0.0, bb = 0.0;
+  for (int z = 0; z < D.nzg; ++z) { rr += D.h_planes[z].x; bb += D.h_planes[z].y; }
+  *rel = bb > 0 ? std::sqrt(rr / bb) : std::sqrt(rr);
+  if (nb) *nb = std::sqrt(bb);
+  return GDP_OK;
+}
+
+int dist_diffuse_z(Ctx& c, const void* I0, int tI, float* I1, long long nx, long long ny, long long nzl,
+                   long long z0g, long long nzg, float bx, float by, float bz, float alpha, const gdp_opts& o,
+                   gdp_report* rep, cudaStream_t s) {
+  if (alpha != 0.f) return set_err(GDP_EINVAL, "the z-slab partition implements Eq. (1) (alpha = 0)");
+  std::vector<long long> z0s;
+  std::vector<int> nzls;
+  std::vector<int> local;
+  RETD(slab_layout(c, z0g, (int)nzl, nzg, z0s, nzls, local));
+  HierKey gk{};
+  gk.nx = nx; gk.ny = ny; gk.nzl = nzg; gk.z0 = 0; gk.nzg = nzg;
+  gk.bx = bx; gk.by = by; gk.bz = bz; gk.alpha = alpha; gk.coarse_max = o.coarse_max;
+  HierKey ck = gk;
+  ck.z0 = z0g;  // the plan depends on this rank's slab (NCCL) or on the loopback split
+  ck.nzl = nzl;
+  DistPlan* D;
+  auto it = c.dist.find(ck);
+  if (it == c.dist.end()) {
+    std::unique_ptr<DistPlan> P;
+    RETD(build_plan(gk, z0s, nzls, local, P));
+    D = P.get();
+    c.dist[ck] = std::move(P);
+  } else {
+    D = it->second.get();
+  }
+  const int np = (int)D->parts.size();
+  const size_t plane = (size_t)nx * ny;
+  const size_t sI = tI == 0 ? 1 : 4;
+  // local slabs: pointers into the caller's arrays (loopback: the whole stack here)
+  const long long base_z = c.world > 1 ? z0g : 0;
+  std::vector<float*> x0(np);
+  std::vector<const void*> i0(np);
+  const long long before = g_launches.load();
+  CKD(cudaEventRecord(c.ev0, s));
+  for (int i = 0; i < np; ++i) {
+    const long long off = D->z0[i] - base_z;
+    x0[i] = I1 + off * plane;
+    i0[i] = static_cast<const char*>(I0) + off * plane * sI;
+    Level& L = D->parts[i]->lv[0];
+    if (!D->b0[i]) CKD(cudaMalloc(&D->b0[i], sizeof(float) * plane * D->nzl[i]));
+    launch_decode_copy(i0[i], tI, x0[i], (long long)plane * D->nzl[i], s);  // x0 = I0
+    launch_rhs(L.K, RhsK{nullptr, i0[i], nullptr, 0.f, 0}, tI, D->b0[i], s);
+  }
+  gdp_report r{};
+  r.levels = D->ff + (int)D->tail->lv.size();
+  double rel, nb;
+  RETD(team_norms(c, *D, x0.data(), &rel, &nb, s));
+  r.rel_res[0] = rel;
+  r.norm_b = nb;
+  int status = GDP_OK, stall = 0, k = 0;
+  const int cap = std::min(o.max_vcycles, GDP_MAX_CYCLES);
+  while (rel > o.rel_tol) {
+    if (k >= cap) { status = GDP_ENOCONV; break; }
+    RETD(team_vcycle(c, *D, x0.data(), o, s));
+    double nrel;
+    RETD(team_norms(c, *D, x0.data(), &nrel, nullptr, s));
+    r.rel_res[++k] = nrel;
+    if (o.stagnation > 0 && nrel > 0.9 * rel) {
+      if (++stall >= o.stagnation) { rel = nrel; status = nrel <= o.rel_tol ? GDP_OK : GDP_ENOCONV; break; }
+    } else {
+      stall = 0;
+    }
+    rel = nrel;
+  }
+  // a10: mean(I1) = mean(I0), fp64 sums in global plane order
+  std::vector<double2*> loc(np);
+  for (int i = 0; i < np; ++i) {
+    Hier& H = *D->parts[i];
+    launch_plane_sums(x0[i], 1, i0[i], tI, (int)nx, (int)ny, D->nzl[i], H.partials, H.plane_sums, s);
+    loc[i] = H.plane_sums;
+  }
+  RETD(comm_plane_sums(c, *D, loc.data(), D->h_planes, s));
+  double sx = 0.0, si = 0.0;
+  for (int z = 0; z < D->nzg; ++z) { sx += D->h_planes[z].x; si += D->h_planes[z].y; }
+  const double Ntot = (double)nx * ny * nzg;
+  for (int i = 0; i < np; ++i) launch_add_scalar(x0[i], (long long)plane * D->nzl[i], (float)((si - sx) / Ntot), s);
+  CKD(cudaEventRecord(c.ev1, s));
+  CKD(cudaEventSynchronize(c.ev1));
+  r.vcycles = k;
+  r.status = status;
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, c.ev0, c.ev1);
+  r.seconds = ms * 1e-3;
+  r.kernel_launches = g_launches.load() - before;
+  if (rep) *rep = r;
+  if (status == GDP_ENOCONV) set_err(GDP_ENOCONV, "distributed diffuse_z: not converged after %d V-cycles", k);
+  return status;
+}
+
+}  // namespace gdp

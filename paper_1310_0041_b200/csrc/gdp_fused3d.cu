@@ -404,7 +404,7 @@ void fused_sweep3d(const Level& L, const Level& C, const float* xin, float* xout
   P.bc = C.b; P.xc = C.x; P.partials = partials;
   const double N = (double)L.nx * L.ny * L.nzl, Nc = (double)C.nx * C.ny * C.nzl;
   const double bytes = N * ((zero_x ? 4.0 : 8.0) + 4.0) + ((tail == 1 || prolong) ? Nc * 4.0 : 0.0);
-  ProfScope ps(tail == 1 || !prolong ? KC_DOWN3D : KC_UP3D, bytes, s);
+  ProfScope ps(tail == 1 || !prolong ? KC_DOWN3D : KC_UP3D, bytes, s, N);
   if (prolong) {
     if (tail == 2) launch3d_t<2, true>(P, s);
     else launch3d_t<0, true>(P, s);

@@ -70,8 +70,24 @@ struct Fine {        // the finest level of one solve
 
 struct Comm;          // NCCL communicator state (gdp_comm.cu)
 
+// A z-slab partition of phase 1 (gdp_dist.cu): the split levels [0, ff) of each local slab
+// and the gathered levels [ff, ..) shared by them.
+struct DistPlan {
+  std::vector<std::unique_ptr<Hier>> parts;  // local slabs (1 per NCCL rank, `loop` in loopback)
+  std::unique_ptr<Hier> tail;                // full levels, lv[0] = global level ff
+  std::vector<long long> z0;                 // global first plane of each local slab
+  std::vector<int> nzl;                      // planes of each local slab
+  std::vector<float*> b0;                    // finest rhs of each local slab
+  int ff = 0;                                // first full level
+  int nzg = 0;
+  double2* h_planes = nullptr;               // pinned, nzg per-plane sums in global order
+  ~DistPlan();
+};
+
 struct Ctx {
   int device = 0, rank = 0, world = 1;
+  int loop = 1;  // loopback slabs emulated in this process (gdp_ctx_create_loopback)
+  std::map<HierKey, std::unique_ptr<DistPlan>> dist;
   std::map<HierKey, std::unique_ptr<Hier>> hier;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   void* scratch = nullptr;
@@ -89,6 +105,9 @@ struct Ctx {
 };
 
 int build_hier(const HierKey& key, std::unique_ptr<Hier>& out);
+int level_chain(const HierKey& key, std::vector<Level>& lv, int& first_full);
+int build_hier_levels(const HierKey& key, const std::vector<Level>& chain, int from, int end, bool own0,
+                      bool coarsest_here, std::unique_ptr<Hier>& out);
 int run_vcycle(Ctx& ctx, Hier& H, const Fine& f, const gdp_opts& o, cudaStream_t s);
 int finest_norms(Ctx& ctx, Hier& H, const Fine& f, float* rout, cudaStream_t s);
 int solve(Ctx& ctx, Hier& H, const Fine& f, const gdp_opts& o, bool per_slice, gdp_report* rep,
@@ -112,6 +131,13 @@ int comm_init(Ctx& c, const void* nccl_unique_id);
 void comm_destroy(Ctx& c);
 int comm_allreduce_sum2(Ctx& c, double* a, double* b, cudaStream_t s);
 int comm_halo_x(Ctx& c, Hier& H, int level, float* x, cudaStream_t s);
+int comm_unique_id(void* out, size_t n);
+int comm_halo_parts(Ctx& c, DistPlan& D, int l, float* const* xs, cudaStream_t s);
+int comm_gather_full(Ctx& c, float* full, size_t n, cudaStream_t s);
+int comm_plane_sums(Ctx& c, DistPlan& D, double2* const* local, double2* out, cudaStream_t s);
+int dist_diffuse_z(Ctx& c, const void* I0, int tI, float* I1, long long nx, long long ny, long long nzl,
+                   long long z0g, long long nzg, float bx, float by, float bz, float alpha, const gdp_opts& o,
+                   gdp_report* rep, cudaStream_t s);
 
 }  // namespace gdp
 

@@ -339,7 +339,7 @@ static inline double ncell(const LevelK& L) { return (double)L.nx * L.ny * L.nzl
 
 void launch_rbgs(const LevelK& L, float* x, const float* xlo, const float* xhi, const RhsK& R,
                  int mode, int tI, int color, cudaStream_t s) {
-  ProfScope ps(KC_RBGS, ncell(L) * (4.0 + rhs_bytes(mode, tI, R) + 2.0), s);
+  ProfScope ps(KC_RBGS, ncell(L) * (4.0 + rhs_bytes(mode, tI, R) + 2.0), s, ncell(L));
   if (mode == RHS_B) launch_rbgs_t<RHS_B, float>(L, x, xlo, xhi, R, color, s);
   else if (tI == 0) launch_rbgs_t<RHS_G, uint8_t>(L, x, xlo, xhi, R, color, s);
   else launch_rbgs_t<RHS_G, float>(L, x, xlo, xhi, R, color, s);
@@ -358,7 +358,7 @@ static void launch_restrict_t(const LevelK& L, const float* x, const float* xlo,
 void launch_restrict(const LevelK& L, const float* x, const float* xlo, const float* xhi,
                      const RhsK& R, int mode, int tI, const XferAxis& tx, const XferAxis& ty,
                      const XferAxis& tz, int ncx, int ncy, int nczl, float* bc, cudaStream_t s) {
-  ProfScope ps(KC_RESTRICT, ncell(L) * (4.0 + rhs_bytes(mode, tI, R)) + 4.0 * ncx * ncy * (double)nczl, s);
+  ProfScope ps(KC_RESTRICT, ncell(L) * (4.0 + rhs_bytes(mode, tI, R)) + 4.0 * ncx * ncy * (double)nczl, s, ncell(L));
   if (mode == RHS_B)
     launch_restrict_t<RHS_B, float>(L, x, xlo, xhi, R, tx, ty, tz, ncx, ncy, nczl, bc, s);
   else if (tI == 0)
@@ -370,7 +370,7 @@ void launch_restrict(const LevelK& L, const float* x, const float* xlo, const fl
 void launch_prolong(const LevelK& L, float* xf, const XferAxis& tx, const XferAxis& ty,
                     const XferAxis& tz, int ncx, int ncy, int nczl, long long cz0, const float* xc,
                     const float* xclo, const float* xchi, cudaStream_t s) {
-  ProfScope ps(KC_PROLONG, ncell(L) * 8.0 + 4.0 * ncx * ncy * (double)nczl, s);
+  ProfScope ps(KC_PROLONG, ncell(L) * 8.0 + 4.0 * ncx * ncy * (double)nczl, s, ncell(L));
   dim3 blk(32, 8);
   dim3 grd((L.nx + 31) / 32, (L.ny + 7) / 8, L.nzl);
   k_prolong<<<grd, blk, 0, s>>>(L, xf, tx, ty, tz, ncx, ncy, nczl, cz0, xc, xclo, xchi);
@@ -394,7 +394,7 @@ void launch_norms(const LevelK& L, const float* x, const float* xlo, const float
                   const RhsK& R, int mode, int tI, float* rout, double2* partials,
                   double2* plane_out, cudaStream_t s) {
   {
-  ProfScope ps(KC_NORMS, ncell(L) * (4.0 + rhs_bytes(mode, tI, R) + (rout ? 4.0 : 0.0)), s);
+  ProfScope ps(KC_NORMS, ncell(L) * (4.0 + rhs_bytes(mode, tI, R) + (rout ? 4.0 : 0.0)), s, ncell(L));
   if (mode == RHS_B) launch_norms_t<RHS_B, float>(L, x, xlo, xhi, R, rout, partials, s);
   else if (tI == 0) launch_norms_t<RHS_G, uint8_t>(L, x, xlo, xhi, R, rout, partials, s);
   else launch_norms_t<RHS_G, float>(L, x, xlo, xhi, R, rout, partials, s);

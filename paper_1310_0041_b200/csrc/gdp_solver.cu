@@ -31,6 +31,7 @@ std::atomic<long long> g_launches{0};
 const char* kclass_name[KC_COUNT] = {"rbgs", "restrict", "prolong", "norms", "coarse", "util",
                                      "down2d", "up2d", "down3d", "up3d"};
 bool g_prof_on = false;
+double g_prof_finest = 0.0;
 struct ProfRec { int cls; double bytes; cudaEvent_t a, b; };
 static std::vector<ProfRec> g_prof;
 static std::vector<int> g_prof_open;  // stack of open records
@@ -237,50 +238,97 @@ static int upload(std::vector<float*>& owned, const std::vector<float>& v, const
   return GDP_OK;
 }
 
-int build_hier(const HierKey& key, std::unique_ptr<Hier>& out) {
-  auto H = std::make_unique<Hier>();
-  H->key = key;
+// One coarsening step of the single-rank rule: axes whose coupling
+// beta_d / H_d^2 is >= 1/2 of the strongest coupled axis are halved (ceil).  Returns false
+// when F is the coarsest level (<= coarse_max unknowns per system, <= 64 cells per axis).
+static bool coarsen_step(const Level& F, int coarse_max, size_t nlev, Level& C, bool co[3]) {
+  const AxisG* g[3] = {&F.gx, &F.gy, &F.gz};
+  double s[3];
+  bool cpl[3];
+  long long size = 1;
+  int maxn = 1;
+  double smax = 0.0;
+  for (int d = 0; d < 3; ++d) {
+    cpl[d] = g[d]->beta > 0.0 && g[d]->n > 1;
+    s[d] = cpl[d] ? g[d]->beta / (g[d]->H * g[d]->H) : 0.0;
+    if (cpl[d]) { size *= g[d]->n; maxn = std::max(maxn, g[d]->n); smax = std::max(smax, s[d]); }
+  }
+  if (!(cpl[0] || cpl[1] || cpl[2])) return false;
+  if (size <= coarse_max && maxn <= 64 && nlev > 1) return false;
+  if (size <= coarse_max && maxn <= 64 && size <= 64) return false;  // tiny: solve directly
+  if ((int)nlev >= GDP_MAX_LEVELS) return false;
+  for (int d = 0; d < 3; ++d) co[d] = cpl[d] && s[d] >= 0.5 * smax;
+  if (!(co[0] || co[1] || co[2])) return false;
+  C = Level();
+  C.gx = co[0] ? coarsen_axis(F.gx) : F.gx;
+  C.gy = co[1] ? coarsen_axis(F.gy) : F.gy;
+  C.gz = co[2] ? coarsen_axis(F.gz) : F.gz;
+  C.tx = make_xfer(F.gx, C.gx, co[0]);
+  C.ty = make_xfer(F.gy, C.gy, co[1]);
+  C.tz = make_xfer(F.gz, C.gz, co[2]);
+  C.nx = C.gx.n; C.ny = C.gy.n;
+  C.nzl = C.gz.n; C.z0 = 0;  // full in z unless the caller keeps it split
+  return true;
+}
+
+// level geometry chain of a (possibly z-split) grid.  Levels stay split while z coarsening
+// keeps every slab aligned (even z0 and nzl), the slab keeps >= 2 planes and the level is
+// not the coarsest; from the first level that cannot, all levels are full in z.  The global
+// geometry of every level is the single-rank one, so the V-cycle is partition-independent.
+int level_chain(const HierKey& key, std::vector<Level>& lv, int& first_full) {
+  lv.clear();
   Level L0;
   L0.gx = AxisG{(int)key.nx, 1.0, 1.0, key.bx};
   L0.gy = AxisG{(int)key.ny, 1.0, 1.0, key.by};
   L0.gz = AxisG{(int)key.nzg, 1.0, 1.0, key.bz};
   L0.nx = (int)key.nx; L0.ny = (int)key.ny; L0.nzl = (int)key.nzl; L0.z0 = key.z0;
-  H->lv.push_back(L0);
+  lv.push_back(L0);
+  first_full = key.nzl == key.nzg ? 0 : -1;
   for (;;) {
-    Level& F = H->lv.back();
-    const AxisG* g[3] = {&F.gx, &F.gy, &F.gz};
-    double s[3];
-    bool cpl[3];
-    long long size = 1;
-    int maxn = 1;
-    double smax = 0.0;
-    for (int d = 0; d < 3; ++d) {
-      cpl[d] = g[d]->beta > 0.0 && g[d]->n > 1;
-      s[d] = cpl[d] ? g[d]->beta / (g[d]->H * g[d]->H) : 0.0;
-      if (cpl[d]) { size *= g[d]->n; maxn = std::max(maxn, g[d]->n); smax = std::max(smax, s[d]); }
-    }
-    const bool any = cpl[0] || cpl[1] || cpl[2];
-    if (!any) break;
-    if (size <= key.coarse_max && maxn <= 64 && H->lv.size() > 1) break;
-    if (size <= key.coarse_max && maxn <= 64 && size <= 64) break;  // tiny: solve directly
-    if ((int)H->lv.size() >= GDP_MAX_LEVELS) break;
-    bool co[3];
-    for (int d = 0; d < 3; ++d) co[d] = cpl[d] && s[d] >= 0.5 * smax;
-    // distributed z-slabs: only coarsen z while every slab stays aligned (even z0, even nzl)
-    if (co[2] && (F.nzl % 2 != 0 || F.z0 % 2 != 0) && F.nzl != F.gz.n) co[2] = false;
-    if (!(co[0] || co[1] || co[2])) break;
+    const Level& F = lv.back();
     Level C;
-    C.gx = co[0] ? coarsen_axis(F.gx) : F.gx;
-    C.gy = co[1] ? coarsen_axis(F.gy) : F.gy;
-    C.gz = co[2] ? coarsen_axis(F.gz) : F.gz;
-    C.tx = make_xfer(F.gx, C.gx, co[0]);
-    C.ty = make_xfer(F.gy, C.gy, co[1]);
-    C.tz = make_xfer(F.gz, C.gz, co[2]);
-    C.nx = C.gx.n; C.ny = C.gy.n;
-    C.nzl = co[2] ? (F.nzl + 1) / 2 : F.nzl;
-    C.z0 = co[2] ? F.z0 / 2 : F.z0;
-    H->lv.push_back(C);
+    bool co[3];
+    if (!coarsen_step(F, key.coarse_max, lv.size(), C, co)) break;
+    if (first_full < 0) {
+      const bool aligned = !co[2] || (F.nzl % 2 == 0 && F.z0 % 2 == 0);
+      const int nzl = co[2] ? F.nzl / 2 : F.nzl;
+      const long long z0 = co[2] ? F.z0 / 2 : F.z0;
+      Level C2;
+      bool co2[3];
+      const bool coarsest = !coarsen_step(C, key.coarse_max, lv.size() + 1, C2, co2);
+      // C may stay split only if the step after it (which may gather) is slab-local too
+      const bool next_ok = coarsest || !co2[2] || (nzl % 2 == 0 && z0 % 2 == 0);
+      if (aligned && nzl >= 2 && !coarsest && next_ok) {
+        C.nzl = nzl;
+        C.z0 = z0;
+      } else {
+        first_full = (int)lv.size();
+      }
+    }
+    lv.push_back(C);
   }
+  if (first_full < 0) return set_err(GDP_EINVAL, "z-split hierarchy never becomes full");
+  return GDP_OK;
+}
+
+// Allocate a hierarchy over levels [from, end) of `chain` (level `from` becomes lv[0]).  If
+// own0, level 0 gets its own x and b (a gathered coarse level); else x0 is the caller's.
+int build_hier_levels(const HierKey& key, const std::vector<Level>& chain, int from, int end, bool own0,
+                      bool coarsest_here, std::unique_ptr<Hier>& out);
+
+int build_hier(const HierKey& key, std::unique_ptr<Hier>& out) {
+  std::vector<Level> chain;
+  int ff;
+  RET(level_chain(key, chain, ff));
+  if (ff != 0) return set_err(GDP_EINVAL, "build_hier: z-split grid needs the distributed driver");
+  return build_hier_levels(key, chain, 0, (int)chain.size(), false, true, out);
+}
+
+int build_hier_levels(const HierKey& key, const std::vector<Level>& chain, int from, int end, bool own0,
+                      bool coarsest_here, std::unique_ptr<Hier>& out) {
+  auto H = std::make_unique<Hier>();
+  H->key = key;
+  for (int l = from; l < end; ++l) H->lv.push_back(chain[l]);
   // device buffers and kernel-side coefficients
   long long maxplanes = 0;
   for (size_t l = 0; l < H->lv.size(); ++l) {
@@ -289,18 +337,35 @@ int build_hier(const HierKey& key, std::unique_ptr<Hier>& out) {
     L.K.ax = make_axisc(L.gx); L.K.ay = make_axisc(L.gy); L.K.az = make_axisc(L.gz);
     L.K.alpha = (float)key.alpha;
     const size_t n = (size_t)L.nx * L.ny * L.nzl;
-    if (l > 0) {
+    if (l > 0 || own0) {
       CK(cudaMalloc(&L.x, n * sizeof(float)));
       L.own_x = true;
       CK(cudaMalloc(&L.b, n * sizeof(float)));
+    }
+    if (L.nzl != L.gz.n) {  // z-split level: ghost planes of x (halo exchange)
+      const size_t pl = (size_t)L.nx * L.ny;
+      CK(cudaMalloc(&L.xlo, pl * sizeof(float)));
+      CK(cudaMalloc(&L.xhi, pl * sizeof(float)));
+      CK(cudaMemset(L.xlo, 0, pl * sizeof(float)));
+      CK(cudaMemset(L.xhi, 0, pl * sizeof(float)));
     }
     maxplanes = std::max<long long>(maxplanes, L.nzl);
   }
   const int nl = (int)H->lv.size();
   Level& Lc = H->lv[nl - 1];
+  if (!coarsest_here) {
+    // the coarsest solve lives in another (gathered) hierarchy
+    int per = norms_blocks_per_plane(H->lv[0].nx, H->lv[0].ny);
+    H->partials_cap = (size_t)per;
+    CK(cudaMalloc(&H->partials, (size_t)per * std::max<long long>(maxplanes, 1) * sizeof(double2)));
+    CK(cudaMalloc(&H->plane_sums, (size_t)std::max<long long>(maxplanes, 1) * sizeof(double2)));
+    CK(cudaMallocHost(&H->h_plane, (size_t)std::max<long long>(maxplanes, 1) * sizeof(double2)));
+    out = std::move(H);
+    return GDP_OK;
+  }
   if (nl == 1) {  // direct solve of level 0: residual / correction scratch
     const size_t n = (size_t)Lc.nx * Lc.ny * Lc.nzl;
-    CK(cudaMalloc(&Lc.b, n * sizeof(float)));
+    if (!Lc.b) CK(cudaMalloc(&Lc.b, n * sizeof(float)));
     CK(cudaMalloc(&H->scratch_e, n * sizeof(float)));
   }
   // coarsest fast diagonalisation
@@ -349,6 +414,7 @@ int build_hier(const HierKey& key, std::unique_ptr<Hier>& out) {
 // ---------------------------------------------------------------------------------
 Ctx::~Ctx() {
   hier.clear();
+  dist.clear();
   if (ev0) cudaEventDestroy(ev0);
   if (ev1) cudaEventDestroy(ev1);
   if (scratch) cudaFree(scratch);
@@ -522,6 +588,7 @@ int solve(Ctx& ctx, Hier& H, const Fine& f, const gdp_opts& o, bool per_slice, g
           cudaStream_t s) {
   gdp_report r{};
   r.levels = (int)H.lv.size();
+  g_prof_finest = (double)H.lv[0].nx * H.lv[0].ny * H.lv[0].nzl;
   RET(finest_norms(ctx, H, f, nullptr, s));
   double nb = 0.0;
   double rel = rel_from_planes(H, per_slice, &nb);
@@ -654,8 +721,21 @@ int gdp_ctx_create(gdp_ctx** out, int device, int rank, int world, const void* n
 int gdp_ctx_create_loopback(gdp_ctx** out, int device, int world) {
   if (!out) return set_err(GDP_EINVAL, "null out");
   *out = nullptr;
-  return set_err(GDP_EINVAL, "loopback ctx: partitioned path not available in this build");
+  if (world < 1) return set_err(GDP_EINVAL, "bad loopback world %d", world);
+  int ndev = 0;
+  CK(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return set_err(GDP_EINVAL, "bad device %d (have %d)", device, ndev);
+  CK(cudaSetDevice(device));
+  auto* c = new gdp_ctx();
+  c->impl.device = device;
+  c->impl.loop = world;
+  cudaEventCreate(&c->impl.ev0);
+  cudaEventCreate(&c->impl.ev1);
+  *out = c;
+  return GDP_OK;
 }
+
+int gdp_get_unique_id(void* out, size_t n) { return comm_unique_id(out, n); }
 
 int gdp_ctx_destroy(gdp_ctx* ctx) {
   if (!ctx) return GDP_OK;
@@ -685,10 +765,16 @@ int gdp_diffuse_z(gdp_ctx* ctx, const void* I0, gdp_dtype dtype, float* I1, gdp_
   const gdp_opts o = resolve_opts(opts);
   cudaStream_t s = (cudaStream_t)stream;
   Ctx& C = ctx->impl;
+  const int tI = dtype == GDP_U8 ? 0 : 1;
+  if (C.world > 1 || C.loop > 1) {  // z-slab partition (gdp_dist.cu)
+    const int st = dist_diffuse_z(C, I0, tI, I1, local.nx, local.ny, local.nz, z0_global, nz_global, W.bx, W.by,
+                                  W.bz, alpha, o, report, s);
+    if (report) report->hbm_bytes_est = 0.0;
+    return st;
+  }
   const long long before = g_launches.load();
   Hier* H;
   RET(C.get_hier(make_key(local, z0_global, nz_global, W, alpha, o), &H));
-  const int tI = dtype == GDP_U8 ? 0 : 1;
   const long long n = local.nx * local.ny * local.nz;
   CK(cudaEventRecord(C.ev0, s));
   launch_decode_copy(I0, tI, I1, n, s);  // x0 = I0
@@ -860,8 +946,8 @@ int gdp_profile_begin(void) {
 
 int gdp_profile_end(gdp_kernel_stat* out, int max, int* n_out) {
   g_prof_on = false;
-  double ms[KC_COUNT] = {0}, by[KC_COUNT] = {0};
-  long long n[KC_COUNT] = {0};
+  double ms[2 * KC_COUNT] = {0}, by[2 * KC_COUNT] = {0};
+  long long n[2 * KC_COUNT] = {0};
   for (auto& r : g_prof) {
     float t = 0.f;
     CK(cudaEventSynchronize(r.b));
@@ -874,10 +960,10 @@ int gdp_profile_end(gdp_kernel_stat* out, int max, int* n_out) {
   }
   g_prof.clear();
   int k = 0;
-  for (int c = 0; c < KC_COUNT; ++c) {
+  for (int c = 0; c < 2 * KC_COUNT; ++c) {
     if (!n[c]) continue;
     if (out && k < max) {
-      std::snprintf(out[k].name, sizeof out[k].name, "%s", kclass_name[c]);
+      std::snprintf(out[k].name, sizeof out[k].name, "%s%s", kclass_name[c % KC_COUNT], c >= KC_COUNT ? "@L0" : "");
       out[k].launches = n[c];
       out[k].ms = ms[c];
       out[k].alg_bytes = by[c];

@@ -67,6 +67,24 @@ def _stream(stream) -> int:
     return stream.cuda_stream
 
 
+def get_unique_id() -> bytes:
+    """A fresh 128-byte ncclUniqueId (rank 0 creates it, every rank passes it to Ctx)."""
+    buf = C.create_string_buffer(128)
+    _check(L.lib().gdp_get_unique_id(buf, 128), "gdp_get_unique_id")
+    return buf.raw
+
+
+def partition(nz: int, world: int) -> list[tuple[int, int]]:
+    """Even z-slab split in rank order [(z0, nz_local)], the split the loopback ctx uses."""
+    base, rem = divmod(nz, world)
+    out, z = [], 0
+    for r in range(world):
+        n = base + (1 if r < rem else 0)
+        out.append((z, n))
+        z += n
+    return out
+
+
 class Ctx:
     """gdp_ctx: per-device solver context (hierarchy cache, events, communicator)."""
 

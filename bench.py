@@ -10,8 +10,9 @@ the resident stack.  Metric: voxels/s per converged solve (both phases).
   python bench.py --impl reference --steps K --warmup W       # the CPU oracle as the reference arm
   torchrun --nproc-per-node N ... bench.py --gpus N           # N ranks, one GPU each
 
-Multi-GPU: every rank solves its own config-1 stack (independent problems, seeds offset by
-rank): weak scaling, no data-path collective.  Timing: CUDA events
+Multi-GPU (torchrun, N ranks): weak scaling on one stack of 1024 x 1024 x (128 N) slices of
+the config-1 generator; rank r owns slices [128 r, 128 r + 128).  Phase 1 couples the slabs
+(one-plane NCCL halo per half-sweep, gathered coarse levels); phase 2 is slab-local.  Timing: CUDA events
 on the solve stream, barrier + synchronize on both sides, max over ranks.  The working set
 (I0 134 MB u8 + x, I1, I2 537 MB fp32 each) exceeds the 126 MB L2, so no explicit flush.
 """
@@ -210,18 +211,30 @@ def main():
 
     c = synth.CONFIGS[args.config]
     nx, ny, nz = c["nx"], c["ny"], c["nz"]
-    # independent per-rank stacks (weak scaling): rank r uses seed + 1000 r; rank 0 = config
-    I0_host = synth.make_stack(nx, ny, nz, c["seed"] + 1000 * rank, c["dtype"])
+    # rank r owns slices [nz r, nz (r + 1)) of a stack of nz * world slices (weak scaling)
+    z0g, nzg = nz * rank, nz * world
+    I0_host = np.empty((nz, ny, nx), dtype=np.uint8 if c["dtype"] == "u8" else np.float32)
+    for k in range(nz):
+        s_ = synth.make_slice(nx, ny, c["seed"], z0g + k)
+        I0_host[k] = np.rint(255.0 * s_).astype(np.uint8) if c["dtype"] == "u8" else s_.astype(np.float32)
     I0 = torch.from_numpy(I0_host).cuda()
     I1 = torch.empty(I0.shape, dtype=torch.float32, device="cuda")
     I2 = torch.empty(I0.shape, dtype=torch.float32, device="cuda")
-    ctx = gdp.Ctx(local)
+    if world > 1:
+        uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            uid.copy_(torch.frombuffer(bytearray(gdp.get_unique_id()), dtype=torch.uint8))
+        dist.broadcast(uid, 0)
+        ctx = gdp.Ctx(local, rank=rank, world=world, nccl_unique_id=bytes(uid.cpu().numpy()))
+    else:
+        ctx = gdp.Ctx(local)
     opts = gdp.default_opts(fused=args.fused)
     stream = torch.cuda.Stream()
     nvox = nx * ny * nz
 
     def step():
-        return gdp.gdp_destripe(ctx, I0, alpha=args.alpha, W=W, I1=I1, I2=I2, opts=opts, stream=stream)
+        return gdp.gdp_destripe(ctx, I0, alpha=args.alpha, W=W, I1=I1, I2=I2, opts=opts, stream=stream,
+                                z0_global=z0g, nz_global=nzg)
 
     def barrier():
         if world > 1:
@@ -286,11 +299,12 @@ def main():
     if not args.no_e2e:
         I0_pin = torch.from_numpy(I0_host).pin_memory()
         I2_pin = torch.empty(I0.shape, dtype=torch.float32).pin_memory()
-        gdp.gdp_destripe_host(ctx, I0_pin, I2_pin, alpha=args.alpha, W=W, opts=opts)  # warm
+        hkw = dict(alpha=args.alpha, W=W, opts=opts, z0_global=z0g, nz_global=nzg)
+        gdp.gdp_destripe_host(ctx, I0_pin, I2_pin, **hkw)  # warm
         barrier()
         t0 = time.perf_counter()
         for _ in range(args.steps):
-            gdp.gdp_destripe_host(ctx, I0_pin, I2_pin, alpha=args.alpha, W=W, opts=opts)
+            gdp.gdp_destripe_host(ctx, I0_pin, I2_pin, **hkw)
         torch.cuda.synchronize()
         el = time.perf_counter() - t0
         te = torch.tensor([el], dtype=torch.float64, device="cuda")
@@ -314,7 +328,8 @@ def main():
                            "W": list(W), "rel_tol": 1e-6, "nu": [opts.nu_pre, opts.nu_post],
                            "schedule": "fused" if args.fused else "reference",
                            "l2": "working set > L2 (I0 134 MB + three 537 MB fp32 volumes); no flush",
-                           "parallelism": f"independent stacks x{world}"},
+                           "parallelism": f"z-slabs x{world} (phase 1 NCCL halo, phase 2 slab-local)",
+                           "global_dims": [nx, ny, nzg]},
                 "vcycles": {"phase1": conv[0][0], "phase2": conv[0][1], "rel_res_phase1": conv[0][2],
                             "rel_res_phase2_max_slice": conv[0][3], "all_converged": status_ok},
                 "roofline": roofline, "whole_step_alg_GBps": whole_gbs,

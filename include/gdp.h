@@ -156,13 +156,14 @@ int gdp_destripe(gdp_ctx* ctx, const void* I0, gdp_dtype dtype, float* I1, float
                  void* stream);
 
 /* Host-buffer entry: I0 and I2 (and I1 if non-NULL) are
- * HOST arrays of the whole local stack.  The library streams z-slabs host->device on
+ * HOST arrays of the whole local stack (on a distributed ctx: this rank's slab at
+ * z0_global of nz_global; single rank: 0 and local.nz).  The library streams z-slabs host->device on
  * side streams, runs both phases, and streams I2 back.  If the stack does not fit in
  * `hbm_budget_bytes` (0 = 90% of free device memory) it returns GDP_ENOMEM.          */
 int gdp_destripe_host(gdp_ctx* ctx, const void* I0_host, gdp_dtype dtype, float* I1_host,
-                      float* I2_host, gdp_dims dims, gdp_weights W, float alpha,
-                      size_t hbm_budget_bytes, const gdp_opts* opts, gdp_report* rep1,
-                      gdp_report* rep2);
+                      float* I2_host, gdp_dims local, int64_t z0_global, int64_t nz_global,
+                      gdp_weights W, float alpha, size_t hbm_budget_bytes, const gdp_opts* opts,
+                      gdp_report* rep1, gdp_report* rep2);
 
 /* One V-cycle on (alpha - div W grad) x = b.  x device fp32 in/out,
  * b device fp32.  With alpha = 0, b is used as given (the caller guarantees sum b = 0

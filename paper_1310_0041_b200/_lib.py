@@ -80,8 +80,8 @@ def lib():
         "gdp_screened_poisson_slices": ([vp, vp, i32, vp, vp, Dims, f32, P(Opts), P(Report), vp], i32),
         "gdp_destripe": ([vp, vp, i32, vp, vp, Dims, i64, i64, Weights, f32, P(Opts), P(Report),
                           P(Report), vp], i32),
-        "gdp_destripe_host": ([vp, vp, i32, vp, vp, Dims, Weights, f32, C.c_size_t, P(Opts), P(Report),
-                               P(Report)], i32),
+        "gdp_destripe_host": ([vp, vp, i32, vp, vp, Dims, i64, i64, Weights, f32, C.c_size_t, P(Opts),
+                               P(Report), P(Report)], i32),
         "gdp_vcycle": ([vp, vp, vp, Dims, i64, i64, Weights, f32, P(Opts), P(C.c_double), vp], i32),
         "gdp_residual": ([vp, vp, vp, vp, Dims, i64, i64, Weights, f32, P(C.c_double), P(C.c_double), vp],
                          i32),

@@ -46,9 +46,9 @@ using namespace gdp;
 // runs; I2 comes back at the end.  Stacks larger than the HBM budget need the slab
 // streamer of the finest level (not built: GDP_ENOMEM).
 extern "C" int gdp_destripe_host(gdp_ctx* ctx, const void* I0_host, gdp_dtype dtype, float* I1_host,
-                                 float* I2_host, gdp_dims dims, gdp_weights W, float alpha,
-                                 size_t hbm_budget_bytes, const gdp_opts* opts, gdp_report* rep1,
-                                 gdp_report* rep2) {
+                                 float* I2_host, gdp_dims dims, int64_t z0_global, int64_t nz_global,
+                                 gdp_weights W, float alpha, size_t hbm_budget_bytes, const gdp_opts* opts,
+                                 gdp_report* rep1, gdp_report* rep2) {
   if (!ctx) return set_err(GDP_EINVAL, "null ctx");
   if (!I0_host || !I2_host) return set_err(GDP_EINVAL, "null host buffers");
   if (dims.nx <= 0 || dims.ny <= 0 || dims.nz <= 0) return set_err(GDP_EINVAL, "dims must be positive");
@@ -77,7 +77,7 @@ extern "C" int gdp_destripe_host(gdp_ctx* ctx, const void* I0_host, gdp_dtype dt
   float* dI2 = (float*)C.hbuf[2];
   cudaStream_t s = C.hs, cs = C.hcs;
   HK(cudaMemcpyAsync(dI0, I0_host, n * sI, cudaMemcpyHostToDevice, s), "H2D I0");
-  rc = gdp_diffuse_z(ctx, dI0, dtype, dI1, dims, 0, dims.nz, W, 0.f, opts, rep1, s);
+  rc = gdp_diffuse_z(ctx, dI0, dtype, dI1, dims, z0_global, nz_global, W, 0.f, opts, rep1, s);
   if (rc != GDP_OK && rc != GDP_ENOCONV) return rc;
   HK(cudaEventRecord(C.hev, s), "event");
   if (I1_host) {

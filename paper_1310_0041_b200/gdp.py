@@ -167,7 +167,8 @@ def gdp_destripe(ctx: Ctx, I0: torch.Tensor, alpha: float = 0.01, W=(1.0, 1.0, 0
 
 
 def gdp_destripe_host(ctx: Ctx, I0: torch.Tensor, I2: torch.Tensor, I1: torch.Tensor | None = None,
-                      alpha: float = 0.01, W=(1.0, 1.0, 0.1), hbm_budget_bytes: int = 0, opts=None):
+                      alpha: float = 0.01, W=(1.0, 1.0, 0.1), hbm_budget_bytes: int = 0, opts=None,
+                      z0_global: int = 0, nz_global: int | None = None):
     """Host-buffer entry (a13): CPU tensors in (pinned for async copies), CPU tensors out."""
     for t, nm in ((I0, "I0"), (I2, "I2")) + (((I1, "I1"),) if I1 is not None else ()):
         if t.is_cuda or not t.is_contiguous():
@@ -176,8 +177,8 @@ def gdp_destripe_host(ctx: Ctx, I0: torch.Tensor, I2: torch.Tensor, I1: torch.Te
     r1, r2 = L.Report(), L.Report()
     o = opts if opts is not None else default_opts()
     rc = L.lib().gdp_destripe_host(ctx.ptr, I0.data_ptr(), _dtype(I0), None if I1 is None else I1.data_ptr(),
-                                   I2.data_ptr(), d, L.Weights(*W), alpha, hbm_budget_bytes, C.byref(o),
-                                   C.byref(r1), C.byref(r2))
+                                   I2.data_ptr(), d, z0_global, d.nz if nz_global is None else nz_global,
+                                   L.Weights(*W), alpha, hbm_budget_bytes, C.byref(o), C.byref(r1), C.byref(r2))
     _check(rc, "gdp_destripe_host", allow_noconv=True)
     return r1.as_dict(), r2.as_dict()
 

@@ -47,7 +47,7 @@ def parse():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--config", type=int, default=CONFIG)
     p.add_argument("--alpha", type=float, default=ALPHA)
-    p.add_argument("--fused", type=int, default=1)
+    p.add_argument("--fused", type=int, default=3)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     return p.parse_args()

@@ -91,7 +91,7 @@ typedef struct {
                          schedule of one kernel per half-sweep, fused = 0):
                          1 = 2D register passes (levels without z links, phase 2);
                          2 = 3D z-marching sweeps (levels with z links, phase 1).
-                         Default 1.                                                          */
+                         Default 3.                                                          */
   int use_graphs;     /* 1: replay each V-cycle as a CUDA graph (default), 0: direct launch */
 } gdp_opts;
 

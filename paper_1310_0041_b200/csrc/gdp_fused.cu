@@ -19,28 +19,15 @@
 //   coefficients and vector loads; edge tiles take the general path.  Both paths call the
 //   arithmetic of gdp_device.cuh in the same order as the reference schedule, so the
 //   iterates are bit-identical to it (tests/test_gpu_parity.py).
-#include <type_traits>
-#include <utility>
-
 #include "gdp_internal.h"
+#include "gdp_pack.cuh"
 
 namespace gdp {
-
-template <typename F, int... I>
-__device__ __forceinline__ void static_for_impl(F&& f, std::integer_sequence<int, I...>) {
-  (f(std::integral_constant<int, I>{}), ...);
-}
-template <int N, typename F>
-__device__ __forceinline__ void static_for(F&& f) {
-  static_for_impl(f, std::make_integer_sequence<int, N>{});
-}
-template <int V> using IC = std::integral_constant<int, V>;
 
 constexpr int G_R = 12;                   // rows per warp
 constexpr int G_W = 8;                    // warps per CTA (stacked in y)
 constexpr int G_COLS = 128;               // columns per warp (4 per lane)
 constexpr int G_ROWS = G_R * G_W;         // 96
-constexpr unsigned FULL = 0xffffffffu;
 
 
 struct Pass2D {
@@ -59,10 +46,6 @@ struct Pass2D {
 
 __device__ __forceinline__ bool col_interior(const AxisC& a, int i) { return i >= 1 && i <= a.n - 3; }
 
-// packed f32x2 arithmetic (FFMA2 / FADD2 / FMUL2 on sm_100a); per component identical to the
-// scalar __fmaf_rn / __fadd_rn / __fmul_rn, and x - y == x + (-y) exactly
-__device__ __forceinline__ float2 sub2(float2 a, float2 b) { return __fadd2_rn(a, make_float2(-b.x, -b.y)); }
-__device__ __forceinline__ float2 f2(float v) { return make_float2(v, v); }
 
 // (A x) on a pack of two cells with regular coefficients (order of apply_from without z terms)
 __device__ __forceinline__ float2 apply2(float2 kx, float2 ky, float2 al, float2 X, float2 W, float2 E,
@@ -151,11 +134,6 @@ template <> struct Row4<uint8_t> {
 // row is inside the domain, and which 1/D case applies.
 struct RowInfo { float yl, yr; int in, dcase; };
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
 
 // halo of the 2D pass: >= 2 nu + 1; a multiple of 4 in x (16-byte aligned lane quads), even in y
 __host__ __device__ constexpr int halo2x(int nu) { return ((2 * nu + 1) + 3) & ~3; }

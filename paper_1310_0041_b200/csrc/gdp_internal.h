@@ -122,7 +122,7 @@ void fused_up2d(const Level& L, const Level& C, const float* xin, float* xout, c
                 int mode, int tI, int nu, double2* partials, cudaStream_t s);
 int fused_tiles_per_plane(int nu, const LevelK& L);
 bool fusable3d(const Level& L, const Level& C, const gdp_opts& o);
-int fused3d_tiles(const LevelK& L);
+int fused3d_items(const Level& L, const Level& C);
 void fused_sweep3d(const Level& L, const Level& C, const float* xin, float* xout, const float* b,
                    bool zero_x, bool prolong, int tail, double2* partials, cudaStream_t s);
 

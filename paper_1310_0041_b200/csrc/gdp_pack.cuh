@@ -1,0 +1,47 @@
+// gdp_pack.cuh — helpers shared by the fused tile kernels (gdp_fused.cu, gdp_march3d.cu):
+// compile-time loops, packed f32x2 arithmetic and cp.async staging.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <type_traits>
+#include <utility>
+
+namespace gdp {
+
+template <typename F, int... I>
+__device__ __forceinline__ void static_for_impl(F&& f, std::integer_sequence<int, I...>) {
+  (f(std::integral_constant<int, I>{}), ...);
+}
+template <int N, typename F>
+__device__ __forceinline__ void static_for(F&& f) {
+  static_for_impl(f, std::make_integer_sequence<int, N>{});
+}
+template <int V> using IC = std::integral_constant<int, V>;
+
+constexpr unsigned FULL = 0xffffffffu;
+
+// packed f32x2 arithmetic (FFMA2 / FADD2 / FMUL2 on sm_100a); per component identical to the
+// scalar __fmaf_rn / __fadd_rn / __fmul_rn, and x - y == x + (-y) exactly
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) { return __fadd2_rn(a, make_float2(-b.x, -b.y)); }
+__device__ __forceinline__ float2 f2(float v) { return make_float2(v, v); }
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+// 16 bytes, zero-filled when !valid (src-size 0: nothing is read)
+__device__ __forceinline__ void cp_async16z(void* smem, const void* gmem, bool valid) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(valid ? 16 : 0));
+}
+// 4 bytes, zero-filled when !valid
+__device__ __forceinline__ void cp_async4z(void* smem, const void* gmem, bool valid) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(s), "l"(gmem), "r"(valid ? 4 : 0));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
+
+}  // namespace gdp

@@ -535,7 +535,8 @@ int run_vcycle(Ctx& ctx, Hier& H, const Fine& f, const gdp_opts& o, cudaStream_t
       continue;
     }
     if (fz[l] == 3) {  // prolongation fused into the first sweep, norms into the last
-      const bool want = l == 0 && (size_t)fused3d_tiles(L.K) <= H.partials_cap * (size_t)L.nzl;
+      const int items = fused3d_items(L, C);
+      const bool want = l == 0 && (size_t)items <= H.partials_cap * (size_t)L.nzl;
       float* c = cur[l];
       for (int k = 0; k < o.nu_post; ++k) {
         float* d = c == x ? L.x2 : x;
@@ -544,7 +545,7 @@ int run_vcycle(Ctx& ctx, Hier& H, const Fine& f, const gdp_opts& o, cudaStream_t
         c = d;
       }
       if (c != x) CK(cudaMemcpyAsync(x, c, sizeof(float) * (size_t)L.nx * L.ny * L.nzl, cudaMemcpyDeviceToDevice, s));
-      if (want) { H.up_norm_per = fused3d_tiles(L.K); H.up_norm_planes = 1; }
+      if (want) { H.up_norm_per = items; H.up_norm_planes = 1; }
       continue;
     }
     launch_prolong(L.K, x, C.tx, C.ty, C.tz, C.nx, C.ny, C.nzl, C.z0, C.x, C.xlo, C.xhi, s);
@@ -691,7 +692,7 @@ int gdp_opts_default(gdp_opts* o) {
   o->nu_post = 2;
   o->coarse_max = 4096;
   o->stagnation = 2;
-  o->fused = 1;
+  o->fused = 3;
   o->use_graphs = 0;
   return GDP_OK;
 }

@@ -37,7 +37,7 @@ def test_opts_defaults():
     import paper_1310_0041_b200 as gdp
     o = gdp.default_opts()
     assert o.rel_tol == 1e-6 and o.max_vcycles == 30 and o.nu_pre == 2 and o.nu_post == 2
-    assert o.coarse_max == 4096 and o.fused == 1
+    assert o.coarse_max == 4096 and o.fused == 3
 
 
 def test_ctx_fails_loudly_without_gpu():

@@ -214,7 +214,8 @@ def test_fused_2d_vcycle_bit_identical(gpu_ctx):
 
 
 @pytest.mark.parametrize("shape,dtype", [((16, 64, 64), "f32"), ((9, 63, 65), "u8"), ((33, 130, 250), "u8"),
-                                         ((24, 517, 389), "u8"), ((12, 1024, 1024), "u8")])
+                                         ((24, 517, 389), "u8"), ((12, 1024, 1024), "u8"), ((67, 150, 300), "u8"),
+                                         ((128, 256, 200), "u8"), ((40, 200, 180), "f32"), ((3, 300, 260), "f32")])
 def test_fused_3d_bit_identical_to_reference(gpu_ctx, shape, dtype):
     nz, ny, nx = shape
     I0 = synth.make_stack(nx, ny, nz, 41, dtype)

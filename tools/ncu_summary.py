@@ -17,16 +17,20 @@ def raw(rep):
         t = f("gpu__time_duration.sum")
         tu = units[hdr.index("gpu__time_duration.sum")]
         t_s = t * {"ns": 1e-9, "us": 1e-6, "usecond": 1e-6, "ms": 1e-3, "msecond": 1e-3}.get(tu, 1e-9)
-        rd = f("dram__bytes_read.sum"); wr = f("dram__bytes_write.sum")
-        ru = units[hdr.index("dram__bytes_read.sum")]
-        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(ru, 1)
+        sc = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}
+        rd = f("dram__bytes_read.sum") * sc.get(units[hdr.index("dram__bytes_read.sum")], 1)
+        wr = f("dram__bytes_write.sum") * sc.get(units[hdr.index("dram__bytes_write.sum")], 1)
+        scale = 1
         res.append({"kernel": d["Kernel Name"], "grid": d.get("launch__grid_size"), "time_s": t_s,
                     "dram_read_B": rd * scale, "dram_write_B": wr * scale,
                     "dram_GBps": (rd + wr) * scale / t_s / 1e9,
                     "inst_executed": f("smsp__inst_executed.sum"),
                     "warps_active_pct": f("sm__warps_active.avg.pct_of_peak_sustained_active"),
                     "issue_active_pct": f("smsp__issue_active.avg.pct_of_peak_sustained_active"),
-                    "registers": f("launch__registers_per_thread"), "top_stalls": top})
+                    "registers": f("launch__registers_per_thread"), "top_stalls": top,
+                    "l2_hit_pct": f("lts__t_sector_hit_rate.pct"),
+                    "dram_pct_peak": f("dram__throughput.avg.pct_of_peak_sustained_elapsed"),
+                    "sm_pct_peak": f("sm__throughput.avg.pct_of_peak_sustained_elapsed")})
     return res
 
 if __name__ == "__main__":

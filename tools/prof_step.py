@@ -6,7 +6,7 @@ import gdp_synth as synth
 import paper_1310_0041_b200 as gdp
 
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 1
-nz = int(sys.argv[2]) if len(sys.argv) > 2 else None
+nz = (int(sys.argv[2]) or None) if len(sys.argv) > 2 else None
 fused = int(sys.argv[3]) if len(sys.argv) > 3 else 1
 ctx = gdp.Ctx(0)
 I0 = torch.from_numpy(synth.make_config(cfg, nz=nz)).cuda()

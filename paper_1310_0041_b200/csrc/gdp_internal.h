@@ -58,6 +58,7 @@ struct Hier {
   size_t partials_cap = 0;         // entries of `partials` per plane
   int up_norm_per = 0;             // >0: the last fused up pass left per-plane partials (this many per plane)
   int up_norm_planes = 0;          // planes of those partials (1: one row for the whole slab)
+  int init_norm_per = 0;           // >0: launch_init left the initial-residual partials (this many per plane)
   ~Hier();
 };
 

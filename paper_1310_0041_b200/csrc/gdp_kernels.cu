@@ -235,6 +235,108 @@ __global__ void __launch_bounds__(256) k_rhs(LevelK L, RhsK R, float* __restrict
   b[c] = rhs_g<TI>(L, R, coefs(L, ix, iy, L.z0 + iz), c, L.nx);
 }
 
+// a1 + a2/a11 + a5 in one pass over I: x0 = decode(I) (the initial guess), the finest rhs
+// b = av V - div W G (rhs_g), and per-(plane, block) fp64 partials of |b - A x0|^2 and |b|^2
+// (the initial residual of the stopping rule, residual_at order).  A thread owns 4 columns and
+// slides down a strip of rows keeping the rows above / below in registers.
+template <typename TI> struct Quad;
+template <> struct Quad<float> {
+  __device__ static __forceinline__ void ld(const void* p, long long i, float (&v)[4]) {
+    const float4 q = __ldg(reinterpret_cast<const float4*>(static_cast<const float*>(p) + i));
+    v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+  }
+};
+template <> struct Quad<uint8_t> {
+  __device__ static __forceinline__ void ld(const void* p, long long i, float (&v)[4]) {
+    const unsigned w = __ldg(reinterpret_cast<const unsigned*>(static_cast<const uint8_t*>(p) + i));
+#pragma unroll
+    for (int c = 0; c < 4; ++c) v[c] = decode_u8((w >> (8 * c)) & 0xffu);
+  }
+};
+
+template <typename TI, bool VEC>
+__global__ void __launch_bounds__(256) k_init(LevelK L, RhsK R, float* __restrict__ x0, float* __restrict__ b,
+                                              double2* partials, int S) {
+  const int gx0 = 4 * (blockIdx.x * blockDim.x + threadIdx.x);
+  const int iz = blockIdx.z;
+  const long long zg = L.z0 + iz;
+  const long long nx = L.nx, plane = (long long)L.nx * L.ny, pbase = (long long)iz * plane;
+  const int y0 = blockIdx.y * S, y1 = min(y0 + S, L.ny);
+  const float zl = cl(L.az, zg), zr = cr(L.az, zg);
+  double sr = 0.0, sb = 0.0;
+  if (gx0 < L.nx) {
+    bool in[4];
+    float kxl[4], kxr[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      in[c] = gx0 + c < L.nx;
+      kxl[c] = cl(L.ax, gx0 + c);
+      kxr[c] = cr(L.ax, gx0 + c);
+    }
+    const bool full = in[3];
+    auto ldrow = [&](long long base, bool ok, float (&v)[4]) {  // I at [base + gx0 ..], 0 outside
+      if (VEC && ok && full) { Quad<TI>::ld(R.I, base + gx0, v); return; }
+#pragma unroll
+      for (int c = 0; c < 4; ++c) v[c] = (ok && in[c]) ? ldI<TI>(R.I, base + gx0 + c) : 0.f;
+    };
+    float rm[4], rc[4], rp[4], dn[4], up[4];
+    ldrow(pbase + (long long)(y0 - 1) * nx, y0 - 1 >= 0, rm);
+    ldrow(pbase + (long long)y0 * nx, y0 < L.ny, rc);
+    for (int gy = y0; gy < y1; ++gy) {
+      const long long row = pbase + (long long)gy * nx;
+      ldrow(row + nx, gy + 1 < L.ny, rp);
+      if (zl != 0.f) ldrow(row - plane, true, dn);
+      if (zr != 0.f) ldrow(row + plane, true, up);
+      const float left = gx0 > 0 ? ldI<TI>(R.I, row + gx0 - 1) : 0.f;
+      const float right = gx0 + 4 < L.nx ? ldI<TI>(R.I, row + gx0 + 4) : 0.f;
+      float V[4] = {0.f, 0.f, 0.f, 0.f};
+      if (R.vmode == 2) {
+        if (VEC && full) {
+          const float4 q = __ldg(reinterpret_cast<const float4*>(R.V + row + gx0));
+          V[0] = q.x; V[1] = q.y; V[2] = q.z; V[3] = q.w;
+        } else {
+#pragma unroll
+          for (int c = 0; c < 4; ++c) V[c] = in[c] ? __ldg(R.V + row + gx0 + c) : 0.f;
+        }
+      }
+      const float yl = cl(L.ay, gy), yr = cr(L.ay, gy);
+      float xo[4], bo[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        Coef k;
+        k.xl = kxl[c]; k.xr = kxr[c]; k.yl = yl; k.yr = yr; k.zl = zl; k.zr = zr;
+        const float Ic = rc[c];
+        const float Iw = k.xl != 0.f ? (c > 0 ? rc[c - 1] : left) : Ic;
+        const float Ie = k.xr != 0.f ? (c < 3 ? rc[c + 1] : right) : Ic;
+        const float Is = k.yl != 0.f ? rm[c] : Ic;
+        const float In = k.yr != 0.f ? rp[c] : Ic;
+        const float Vc = R.vmode == 0 ? 0.f : (R.vmode == 1 ? Ic : V[c]);
+        const float bc = rhs_from(k, Ic, Iw, Ie, Is, In, Vc, R.av);  // == rhs_g
+        const float d = k.zl != 0.f ? dn[c] : Ic, u = k.zr != 0.f ? up[c] : Ic;
+        const float r = __fsub_rn(bc, apply_from(k, L.alpha, Ic, Iw, Ie, Is, In, d, u));  // == residual_at
+        xo[c] = Ic;
+        bo[c] = bc;
+        if (in[c]) {
+          sr += (double)r * (double)r;
+          sb += (double)bc * (double)bc;
+        }
+      }
+      if (VEC && full) {
+        *reinterpret_cast<float4*>(x0 + row + gx0) = make_float4(xo[0], xo[1], xo[2], xo[3]);
+        *reinterpret_cast<float4*>(b + row + gx0) = make_float4(bo[0], bo[1], bo[2], bo[3]);
+      } else {
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          if (in[c]) { x0[row + gx0 + c] = xo[c]; b[row + gx0 + c] = bo[c]; }
+      }
+#pragma unroll
+      for (int c = 0; c < 4; ++c) { rm[c] = rc[c]; rc[c] = rp[c]; }
+    }
+  }
+  block_sum2(sr, sb);
+  if (threadIdx.x == 0) partials[((long long)iz * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = make_double2(sr, sb);
+}
+
 template <typename TI>
 __global__ void k_decode_copy(const void* I, float* __restrict__ x, long long n) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
@@ -270,11 +372,18 @@ __global__ void __launch_bounds__(512) k_coarse_fd(CoarseK C, const float* __res
   float* B = sm + nsys;
   for (int i = threadIdx.x; i < nsys; i += blockDim.x) A[i] = b[off + i];
   __syncthreads();
-  auto tx = [&](const float* M, float* in, float* out) {  // along x
+  // along x: consecutive threads take consecutive modes k, so the x matrix is staged in shared
+  // memory with a padded row stride (conflict-free column walk); `in` rows are broadcast
+  float* Ms = sm + 2 * nsys;
+  auto tx = [&](const float* M, float* in, float* out) {
+    for (int i = threadIdx.x; i < nx * nx; i += blockDim.x) Ms[(i / nx) * (nx + 1) + i % nx] = __ldg(M + i);
+    __syncthreads();
     for (int i = threadIdx.x; i < nsys; i += blockDim.x) {
       const int k = i % nx, r = i / nx;
+      const float* mk = Ms + k * (nx + 1);
+      const float* ir = in + r * nx;
       float s = 0.f;
-      for (int j = 0; j < nx; ++j) s = fmaf(__ldg(M + k * nx + j), in[r * nx + j], s);
+      for (int j = 0; j < nx; ++j) s = fmaf(mk[j], ir[j], s);
       out[i] = s;
     }
     __syncthreads();
@@ -435,6 +544,25 @@ void launch_rhs(const LevelK& L, const RhsK& R, int tI, float* b, cudaStream_t s
   else k_rhs<float><<<g, 256, 0, s>>>(L, R, b);
 }
 
+
+constexpr int INIT_ROWS = 32;
+int init_blocks_per_plane(int nx, int ny) { return ((nx + 1023) / 1024) * ((ny + INIT_ROWS - 1) / INIT_ROWS); }
+
+void launch_init(const LevelK& L, const RhsK& R, int tI, float* x0, float* b, double2* partials, cudaStream_t s) {
+  const double n = (double)L.nx * L.ny * L.nzl;
+  ProfScope ps(KC_UTIL, n * ((tI ? 4.0 : 1.0) + (R.vmode == 2 ? 4.0 : 0.0) + 8.0), s);
+  dim3 g((L.nx + 1023) / 1024, (L.ny + INIT_ROWS - 1) / INIT_ROWS, L.nzl);
+  const bool vec = (L.nx & 3) == 0 && ((uintptr_t)R.I & 15) == 0 && ((uintptr_t)x0 & 15) == 0 &&
+                   ((uintptr_t)b & 15) == 0 && (R.vmode != 2 || ((uintptr_t)R.V & 15) == 0);
+  if (tI == 0) {
+    if (vec) k_init<uint8_t, true><<<g, 256, 0, s>>>(L, R, x0, b, partials, INIT_ROWS);
+    else k_init<uint8_t, false><<<g, 256, 0, s>>>(L, R, x0, b, partials, INIT_ROWS);
+  } else {
+    if (vec) k_init<float, true><<<g, 256, 0, s>>>(L, R, x0, b, partials, INIT_ROWS);
+    else k_init<float, false><<<g, 256, 0, s>>>(L, R, x0, b, partials, INIT_ROWS);
+  }
+}
+
 void launch_decode_copy(const void* I, int tI, float* x, long long n, cudaStream_t s) {
   ProfScope ps(KC_UTIL, (double)n * (tI ? 8.0 : 5.0), s);
   if (tI == 0) k_decode_copy<uint8_t><<<ew_grid(n), 256, 0, s>>>(I, x, n);
@@ -453,7 +581,7 @@ void launch_axpy(float* x, const float* e, long long n, cudaStream_t s) {
 
 size_t coarse_smem_bytes(const CoarseK& C) {
   const long long nsys = (long long)C.nx * C.ny * (C.cz ? C.nz : 1);
-  return (size_t)(2 * nsys * sizeof(float));
+  return (size_t)((2 * nsys + (long long)C.nx * (C.nx + 1)) * sizeof(float));
 }
 
 cudaError_t launch_coarse(const CoarseK& C, const float* b, float* x, cudaStream_t s) {

@@ -181,6 +181,15 @@ __global__ void __launch_bounds__(MT, 1) k_march3d(const __grid_constant__ March
       S.inv[zc][rc][pk][ln] = make_float2(v[0], v[1]);
     }
 
+    // z link coefficients of a plane: branch-free selects on per-kernel constants
+    const float kz = L.az.k, kzl = L.az.kl, kzr = L.az.kr;
+    auto zcoef = [&](int q, float2& zl2, float2& zr2, int& zoff) {
+      const bool first = q == 0, last = q == nzg - 1, penult = q == nzg - 2;
+      zl2 = f2(first ? 0.f : (last ? kzl : kz));
+      zr2 = f2(last ? 0.f : (penult ? kzr : kz));
+      zoff = (first ? 1 : (last ? 3 : (penult ? 2 : 0))) * (6 * 2 * 32 * 2);  // plane_class * table stride
+    };
+
     // ---- prolongation taps (per column / row, fixed for the item)
     float ptx[4];
     bool selfJ[4];
@@ -392,9 +401,9 @@ __global__ void __launch_bounds__(MT, 1) k_march3d(const __grid_constant__ March
         constexpr int KO = decltype(KOc)::value;
         constexpr int KD = (KO + MRING - 1) % MRING, KU = (KO + 1) % MRING;
         constexpr int ZP = KO & 1;  // parity of the plane's z
-        const int zc = plane_class(q, nzg);
-        const float2 zl2 = f2(zc == 1 ? 0.f : (zc == 3 ? L.az.kl : L.az.k));
-        const float2 zr2 = f2(zc == 3 ? 0.f : (zc == 2 ? L.az.kr : L.az.k));
+        float2 zl2, zr2;
+        int zoff;
+        zcoef(q, zl2, zr2, zoff);
         Pk& Xo = X[KO];
         const float2 sv = S.ex[C][PAR ^ 1][wdn][1][lane];  // pack (C + z)&1 of the row below my row 0
         const float2 nv = S.ex[C][PAR ^ 1][wup][0][lane];  // pack (C + 1 + z)&1 of the row above my row MR-1
@@ -402,7 +411,7 @@ __global__ void __launch_bounds__(MT, 1) k_march3d(const __grid_constant__ March
           constexpr int j = decltype(Jc)::value;
           constexpr int PK = (C + j + ZP) & 1;  // active pack of row j (gyw even, gx0 even)
           const float4 bv = S.bs[KO % MBS][j][tid];
-          const float2 iD = *reinterpret_cast<const float2*>(invf + zc * (6 * 2 * 32 * 2) + ivo[j] + PK * 64);
+          const float2 iD = *reinterpret_cast<const float2*>(invf + zoff + ivo[j] + PK * 64);
           const float2 s = stencil(IC<PK>{}, Jc, Xo, X[KD], X[KU], sv, nv, zl2, zr2);
           if (PK == 0) Xo.A[j] = __ffma2_rn(sub2(make_float2(bv.x, bv.z), s), iD, Xo.A[j]);
           else Xo.B[j] = __ffma2_rn(sub2(make_float2(bv.y, bv.w), s), iD, Xo.B[j]);
@@ -425,9 +434,9 @@ __global__ void __launch_bounds__(MT, 1) k_march3d(const __grid_constant__ March
         constexpr int ZP = KO & 1;
         const Pk& Xo = X[KO];
         if (TAIL != TAIL_NONE && wint) {  // warp-uniform: the stencil shuffles need every lane
-          const int zc = plane_class(q, nzg);
-          const float2 zl2 = f2(zc == 1 ? 0.f : (zc == 3 ? L.az.kl : L.az.k));
-          const float2 zr2 = f2(zc == 3 ? 0.f : (zc == 2 ? L.az.kr : L.az.k));
+          float2 zl2, zr2;
+          int zoff;
+          zcoef(q, zl2, zr2, zoff);
           const float4 sv4 = S.et[PAR ^ 1][wdn][1][lane];
           const float4 nv4 = S.et[PAR ^ 1][wup][0][lane];
           float2 rA[MR], rB[MR], bA[MR], bB[MR];

@@ -395,11 +395,11 @@ int build_hier_levels(const HierKey& key, const std::vector<Level>& chain, int f
   }
   C.lam_thr = key.alpha > 0 ? -1.f : (float)(1e-9 * std::max(lsum, 1e-30));
   const long long nsys = (long long)C.nx * C.ny * (C.cz ? C.nz : 1);
-  if (nsys * 2 * sizeof(float) > 200 * 1024)
+  if ((nsys * 2 + (long long)C.nx * (C.nx + 1)) * sizeof(float) > 200 * 1024)
     return set_err(GDP_EINVAL, "coarsest system of %lld unknowns exceeds shared memory", nsys);
   H->coarse = C;
   // norm partials: level-0 plane rows
-  int per = norms_blocks_per_plane(H->lv[0].nx, H->lv[0].ny);
+  int per = std::max(norms_blocks_per_plane(H->lv[0].nx, H->lv[0].ny), init_blocks_per_plane(H->lv[0].nx, H->lv[0].ny));
   for (int nu = 1; nu <= 2; ++nu) per = std::max(per, fused_tiles_per_plane(nu, H->lv[0].K));
   H->partials_cap = (size_t)per;
   CK(cudaMalloc(&H->partials, (size_t)per * std::max<long long>(maxplanes, 1) * sizeof(double2)));
@@ -590,7 +590,14 @@ int solve(Ctx& ctx, Hier& H, const Fine& f, const gdp_opts& o, bool per_slice, g
   gdp_report r{};
   r.levels = (int)H.lv.size();
   g_prof_finest = (double)H.lv[0].nx * H.lv[0].ny * H.lv[0].nzl;
-  RET(finest_norms(ctx, H, f, nullptr, s));
+  if (H.init_norm_per > 0) {  // the initial residual came with launch_init
+    launch_finalize(H.partials, H.init_norm_per, H.lv[0].nzl, H.plane_sums, s);
+    CK(cudaMemcpyAsync(H.h_plane, H.plane_sums, sizeof(double2) * H.lv[0].nzl, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    H.init_norm_per = 0;
+  } else {
+    RET(finest_norms(ctx, H, f, nullptr, s));
+  }
   double nb = 0.0;
   double rel = rel_from_planes(H, per_slice, &nb);
   r.rel_res[0] = rel;
@@ -778,20 +785,22 @@ int gdp_diffuse_z(gdp_ctx* ctx, const void* I0, gdp_dtype dtype, float* I1, gdp_
   RET(C.get_hier(make_key(local, z0_global, nz_global, W, alpha, o), &H));
   const long long n = local.nx * local.ny * local.nz;
   CK(cudaEventRecord(C.ev0, s));
-  launch_decode_copy(I0, tI, I1, n, s);  // x0 = I0
   Fine f;
   f.x = I1;
   f.mode = RHS_G;
   f.tI = tI;
   f.R = RhsK{nullptr, I0, nullptr, alpha, alpha > 0 ? 1 : 0};
   // Eq. (1): the gradient target uses (bx, by); the rhs is formed on the fly (a2), or written
-  // once for the fused passes (same values)
+  // once (same values) together with x0 = I0 and the initial residual norms
   if (H->lv.size() > 1) {  // every schedule reads the written rhs (same values as on the fly)
     if (!H->b0) CK(cudaMalloc(&H->b0, sizeof(float) * (size_t)n));
-    launch_rhs(H->lv[0].K, f.R, tI, H->b0, s);
+    launch_init(H->lv[0].K, f.R, tI, I1, H->b0, H->partials, s);
+    H->init_norm_per = init_blocks_per_plane(H->lv[0].nx, H->lv[0].ny);
     f.mode = RHS_B;
     f.tI = 1;
     f.R = RhsK{H->b0, nullptr, nullptr, 0.f, 0};
+  } else {
+    launch_decode_copy(I0, tI, I1, n, s);  // x0 = I0
   }
   int st = solve(C, *H, f, o, false, report, s);
   if (st != GDP_OK && st != GDP_ENOCONV) return st;
@@ -838,7 +847,6 @@ int gdp_screened_poisson_slices(gdp_ctx* ctx, const void* I0, gdp_dtype dtype, c
   const int tI = dtype == GDP_U8 ? 0 : 1;
   const long long n = local.nx * local.ny * local.nz;
   CK(cudaEventRecord(C.ev0, s));
-  launch_decode_copy(I0, tI, I2, n, s);  // x0 = I0
   Fine f;
   f.x = I2;
   f.mode = RHS_G;
@@ -846,12 +854,16 @@ int gdp_screened_poisson_slices(gdp_ctx* ctx, const void* I0, gdp_dtype dtype, c
   f.R = RhsK{nullptr, I0, I1, alpha, 2};
   if (H->lv.size() > 1) {
     // the passes read the rhs b = alpha I1 + (Lx + Ly) I0 (a11) written once: 4 B/cell
-    // per pass instead of I0 + I1 (5 or 8 B/cell); same values as the on-the-fly form
+    // per pass instead of I0 + I1 (5 or 8 B/cell); same values as the on-the-fly form.
+    // Written together with x0 = I0 and the initial residual norms.
     if (!H->b0) CK(cudaMalloc(&H->b0, sizeof(float) * (size_t)n));
-    launch_rhs(H->lv[0].K, f.R, tI, H->b0, s);
+    launch_init(H->lv[0].K, f.R, tI, I2, H->b0, H->partials, s);
+    H->init_norm_per = init_blocks_per_plane(H->lv[0].nx, H->lv[0].ny);
     f.mode = RHS_B;
     f.tI = 1;
     f.R = RhsK{H->b0, nullptr, nullptr, 0.f, 0};
+  } else {
+    launch_decode_copy(I0, tI, I2, n, s);  // x0 = I0
   }
   int st = solve(C, *H, f, o, true, report, s);
   if (st != GDP_OK && st != GDP_ENOCONV) return st;

@@ -259,7 +259,9 @@ def test_loopback_partition_bit_identical(gpu_ctx, shape, world):
         out, r2 = gdp.gdp_diffuse_z(lb, dev(I0), opts=o)
     finally:
         lb.close()
-    assert r1["vcycles"] == r2["vcycles"] and r1["rel_res"] == r2["rel_res"]
+    # norms are fp64 sums in different orders (fused initial residual vs per-slab partials)
+    assert r1["vcycles"] == r2["vcycles"]
+    assert np.allclose(r1["rel_res"], r2["rel_res"], rtol=1e-9, atol=0)
     assert np.array_equal(ref.cpu().numpy(), out.cpu().numpy())
     assert np.abs(host(out) - O.diffuse_z(I0)).max() <= TOL_X
 

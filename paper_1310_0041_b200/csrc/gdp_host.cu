@@ -41,10 +41,10 @@ using namespace gdp;
                      what, cudaGetErrorString(e_));                                       \
   } while (0)
 
-// a13 (in-core variant): host arrays in, host arrays out.  I0 goes host->device on the
-// compute stream; I1 (if requested) streams back on a side copy stream while phase 2
-// runs; I2 comes back at the end.  Stacks larger than the HBM budget need the slab
-// streamer of the finest level (not built: GDP_ENOMEM).
+// a13: host arrays in, host arrays out.  In core (the stack fits the HBM budget): I0 goes
+// host->device on the compute stream; I1 (if requested) streams back on a side copy stream
+// while phase 2 runs; I2 comes back at the end.  Out of core: the finest level stays on the
+// host and is streamed in z-chunks (gdp_stream.cu).
 extern "C" int gdp_destripe_host(gdp_ctx* ctx, const void* I0_host, gdp_dtype dtype, float* I1_host,
                                  float* I2_host, gdp_dims dims, int64_t z0_global, int64_t nz_global,
                                  gdp_weights W, float alpha, size_t hbm_budget_bytes, const gdp_opts* opts,
@@ -62,9 +62,38 @@ extern "C" int gdp_destripe_host(gdp_ctx* ctx, const void* I0_host, gdp_dtype dt
   HK(cudaMemGetInfo(&freeb, &totb), "meminfo");
   const size_t have = freeb + C.hbuf_cap[0] + C.hbuf_cap[1] + C.hbuf_cap[2];
   const size_t budget = hbm_budget_bytes ? hbm_budget_bytes : (size_t)(0.9 * (double)have);
-  if (need > budget)
-    return set_err(GDP_ENOMEM, "stack needs ~%zu B of HBM, budget %zu B (out-of-core slab streaming "
-                   "of the finest level is not built)", need, budget);
+  if (need > budget) {
+    // a13: the finest level stays in host memory and is streamed in z-chunks (gdp_stream.cu)
+    if (C.world > 1 || C.loop > 1 || z0_global != 0 || nz_global != dims.nz)
+      return set_err(GDP_ENOMEM, "stack needs ~%zu B of HBM, budget %zu B; out-of-core streaming is "
+                     "single-rank only in this build", need, budget);
+    gdp_opts o;
+    gdp_opts_default(&o);
+    if (opts) o = *opts;
+    HostPin pin0, pin1, pin2;
+    int rc = pin0.pin(I0_host, n * sI);
+    if (rc == GDP_OK) rc = pin2.pin(I2_host, n * 4);
+    if (rc == GDP_OK && I1_host) rc = pin1.pin(I1_host, n * 4);
+    if (rc != GDP_OK) return rc;
+    float* xh = I1_host;
+    float* scratch = nullptr;
+    if (!xh) {
+      HK(cudaMallocHost(&scratch, n * 4), "pinned I1 scratch");
+      xh = scratch;
+    }
+    double shift = 0.0;
+    const int tI = dtype == GDP_U8 ? 0 : 1;
+    int st1 = stream_diffuse_z(C, I0_host, tI, xh, dims.nx, dims.ny, dims.nz, W.bx, W.by, W.bz, o, budget, rep1,
+                               &shift);
+    int st2 = GDP_OK;
+    if (st1 == GDP_OK || st1 == GDP_ENOCONV)
+      st2 = stream_slices(C, ctx, I0_host, dtype, xh, I2_host, dims.nx, dims.ny, dims.nz, alpha, shift, o, budget,
+                          rep2);
+    if (scratch) cudaFreeHost(scratch);
+    if (st1 != GDP_OK && st1 != GDP_ENOCONV) return st1;
+    if (st2 != GDP_OK) return st2;
+    return st1;
+  }
   if (!C.hs) HK(cudaStreamCreateWithFlags(&C.hs, cudaStreamNonBlocking), "stream");
   if (!C.hcs) HK(cudaStreamCreateWithFlags(&C.hcs, cudaStreamNonBlocking), "stream");
   if (!C.hev) HK(cudaEventCreateWithFlags(&C.hev, cudaEventDisableTiming), "event");

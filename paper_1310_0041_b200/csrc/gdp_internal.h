@@ -109,7 +109,8 @@ int build_hier(const HierKey& key, std::unique_ptr<Hier>& out);
 int level_chain(const HierKey& key, std::vector<Level>& lv, int& first_full);
 int build_hier_levels(const HierKey& key, const std::vector<Level>& chain, int from, int end, bool own0,
                       bool coarsest_here, std::unique_ptr<Hier>& out);
-int run_vcycle(Ctx& ctx, Hier& H, const Fine& f, const gdp_opts& o, cudaStream_t s);
+// one V-cycle over levels [l0, end) (l0 = 1: the caller owns level 0, e.g. the out-of-core streamer)
+int run_vcycle(Ctx& ctx, Hier& H, const Fine& f, const gdp_opts& o, cudaStream_t s, int l0 = 0);
 int finest_norms(Ctx& ctx, Hier& H, const Fine& f, float* rout, cudaStream_t s);
 int solve(Ctx& ctx, Hier& H, const Fine& f, const gdp_opts& o, bool per_slice, gdp_report* rep,
           cudaStream_t s);
@@ -123,9 +124,23 @@ void fused_up2d(const Level& L, const Level& C, const float* xin, float* xout, c
                 int mode, int tI, int nu, double2* partials, cudaStream_t s);
 int fused_tiles_per_plane(int nu, const LevelK& L);
 bool fusable3d(const Level& L, const Level& C, const gdp_opts& o);
-int fused3d_items(const Level& L, const Level& C);
-void fused_sweep3d(const Level& L, const Level& C, const float* xin, float* xout, const float* b,
-                   bool zero_x, bool prolong, int tail, double2* partials, cudaStream_t s);
+int fused3d_items(const Level& L, const Level& C, int zlo = 0, int zhi = -1);
+int fused_sweep3d(const Level& L, const Level& C, const float* xin, float* xout, const float* b,
+                  bool zero_x, bool prolong, int tail, double2* partials, cudaStream_t s, int zlo = 0,
+                  int zhi = -1);
+
+// out-of-core streaming of the finest level (gdp_stream.cu)
+struct HostPin {
+  void* p = nullptr;
+  ~HostPin();
+  int pin(const void* ptr, size_t bytes);
+};
+int stream_diffuse_z(Ctx& C, const void* I0h, int tI, float* xh, long long nx, long long ny, long long nz,
+                     float bx, float by, float bz, const gdp_opts& o, size_t budget, gdp_report* rep,
+                     double* shift_out);
+int stream_slices(Ctx& C, gdp_ctx* cctx, const void* I0h, gdp_dtype dtype, float* I1h, float* I2h, long long nx,
+                  long long ny, long long nz, float alpha, double shift, const gdp_opts& o, size_t budget,
+                  gdp_report* rep);
 
 // communication (gdp_comm.cu); single-rank contexts make these no-ops
 int comm_init(Ctx& c, const void* nccl_unique_id);

@@ -552,16 +552,16 @@ bool fusable3d(const Level& L, const Level& C, const gdp_opts& o) {
 }
 
 // work decomposition: tiles x z-chunks, the chunk count minimising waves x (chunk + 6)
-static void plan3d(const LevelK& L, bool zc, March3D& P) {
+static void plan3d(const LevelK& L, bool zc, int zlo, int zhi, March3D& P) {
   P.tiles_x = (L.nx + MTXI - 1) / MTXI;
   P.tiles_y = (L.ny + MTYI - 1) / MTYI;
   const int tiles = P.tiles_x * P.tiles_y;
-  const int nz = L.nzl, nsm = num_sms();
+  const int nz = zhi - zlo, nsm = num_sms();
   double best = 1e30;
   int bch = nz;
   for (int nch = 1; nch <= nz; ++nch) {
     int chunk = (nz + nch - 1) / nch;
-    if (zc && (chunk & 1)) ++chunk;
+    if (zc && (chunk & 1)) ++chunk;  // z-coarsened: coarse plane pairs never straddle items
     const int real = (nz + chunk - 1) / chunk;
     const long long items = (long long)tiles * real;
     const long long waves = (items + nsm - 1) / nsm;
@@ -570,14 +570,15 @@ static void plan3d(const LevelK& L, bool zc, March3D& P) {
     if (chunk <= 4) break;
   }
   P.chunk = bch;
-  P.zlo = 0;
-  P.zhi = nz;
+  P.zlo = zlo;
+  P.zhi = zhi;
   P.nitems = tiles * ((nz + bch - 1) / bch);
 }
 
-int fused3d_items(const Level& L, const Level& C) {
+int fused3d_items(const Level& L, const Level& C, int zlo, int zhi) {
   March3D P{};
-  plan3d(L.K, C.tz.coarsened != 0, P);
+  if (zhi < 0) zhi = L.nzl;
+  plan3d(L.K, C.tz.coarsened != 0, zlo, zhi, P);
   return P.nitems;
 }
 
@@ -597,18 +598,22 @@ static void launch_m3(const March3D& P, cudaStream_t s) {
   else launch_m3v<TAIL, PROLONG, ZC, false>(P, s);
 }
 
-// one fused sweep of level L: tail 0 none, 1 restrict into C.b, 2 norms into partials (one per item)
-void fused_sweep3d(const Level& L, const Level& C, const float* xin, float* xout, const float* b,
-                   bool zero_x, bool prolong, int tail, double2* partials, cudaStream_t s) {
+// one fused sweep of level L over the planes [zlo, zhi) it finalises (all planes: 0, -1): tail 0
+// none, 1 restrict into C.b, 2 norms into partials (one per item).  Plane p of x / b is read at
+// xin / b + p * plane and written at xout + p * plane, so a caller streaming z-windows passes
+// pointers offset by the window's first plane (the kernel touches planes [zlo-3, zhi+3) only).
+int fused_sweep3d(const Level& L, const Level& C, const float* xin, float* xout, const float* b,
+                  bool zero_x, bool prolong, int tail, double2* partials, cudaStream_t s, int zlo, int zhi) {
   March3D P{};
+  if (zhi < 0) zhi = L.nzl;
   P.L = L.K; P.xin = xin; P.xout = xout; P.b = b; P.zero_x = zero_x ? 1 : 0;
   P.tx = C.tx; P.ty = C.ty; P.tz = C.tz; P.ncx = C.nx; P.ncy = C.ny;
   P.bc = C.b; P.xc = C.x; P.partials = partials;
   const bool zc = C.tz.coarsened != 0;
-  plan3d(L.K, zc, P);
-  const double N = (double)L.nx * L.ny * L.nzl, Nc = (double)C.nx * C.ny * C.nzl;
+  plan3d(L.K, zc, zlo, zhi, P);
+  const double N = (double)L.nx * L.ny * (zhi - zlo), Nc = (double)C.nx * C.ny * C.nzl * (zhi - zlo) / L.nzl;
   const double bytes = N * ((zero_x ? 4.0 : 8.0) + 4.0) + ((tail == 1 || prolong) ? Nc * 4.0 : 0.0);
-  ProfScope ps(tail == 1 || !prolong ? KC_DOWN3D : KC_UP3D, bytes, s, N);
+  ProfScope ps(tail == 1 || !prolong ? KC_DOWN3D : KC_UP3D, bytes, s, zhi - zlo == L.nzl ? N : 0.0);
   if (prolong) {
     if (tail == 2) { if (zc) launch_m3<2, true, true>(P, s); else launch_m3<2, true, false>(P, s); }
     else { if (zc) launch_m3<0, true, true>(P, s); else launch_m3<0, true, false>(P, s); }
@@ -617,6 +622,7 @@ void fused_sweep3d(const Level& L, const Level& C, const float* xin, float* xout
     else if (tail == 2) launch_m3<2, false, false>(P, s);
     else launch_m3<0, false, false>(P, s);
   }
+  return P.nitems;
 }
 
 }  // namespace gdp

@@ -465,7 +465,7 @@ static int smooth(const Level& L, float* x, const RhsK& R, int mode, int tI, int
   return GDP_OK;
 }
 
-int run_vcycle(Ctx& ctx, Hier& H, const Fine& f, const gdp_opts& o, cudaStream_t s) {
+int run_vcycle(Ctx& ctx, Hier& H, const Fine& f, const gdp_opts& o, cudaStream_t s, int l0) {
   const int nl = (int)H.lv.size();
   if (nl == 1) {  // level 0 is the coarsest: x += A^-1 (b - A x)
     Level& L = H.lv[0];
@@ -480,7 +480,7 @@ int run_vcycle(Ctx& ctx, Hier& H, const Fine& f, const gdp_opts& o, cudaStream_t
   int fz[GDP_MAX_LEVELS] = {0};
   float* cur[GDP_MAX_LEVELS] = {nullptr};  // buffer holding x of a level after its down pass
   const bool nu_ok = o.nu_pre >= 1 && o.nu_post >= 1;
-  for (int l = 0; l < nl - 1; ++l) {
+  for (int l = l0; l < nl - 1; ++l) {
     Level& L = H.lv[l];
     Level& C = H.lv[l + 1];
     const bool rhs_ok = l > 0 || f.mode == RHS_B;
@@ -488,7 +488,7 @@ int run_vcycle(Ctx& ctx, Hier& H, const Fine& f, const gdp_opts& o, cudaStream_t
     else if (rhs_ok && nu_ok && fusable3d(L, C, o)) fz[l] = 3;
     if (fz[l] && !L.x2) CK(cudaMalloc(&L.x2, sizeof(float) * (size_t)L.nx * L.ny * L.nzl));
   }
-  for (int l = 0; l < nl - 1; ++l) {
+  for (int l = l0; l < nl - 1; ++l) {
     Level& L = H.lv[l];
     Level& C = H.lv[l + 1];
     float* x = l == 0 ? f.x : L.x;
@@ -521,7 +521,7 @@ int run_vcycle(Ctx& ctx, Hier& H, const Fine& f, const gdp_opts& o, cudaStream_t
   }
   Level& Lc = H.lv[nl - 1];
   CK(launch_coarse(H.coarse, Lc.b, Lc.x, s));
-  for (int l = nl - 2; l >= 0; --l) {
+  for (int l = nl - 2; l >= l0; --l) {
     Level& L = H.lv[l];
     Level& C = H.lv[l + 1];
     float* x = l == 0 ? f.x : L.x;

@@ -1,0 +1,380 @@
+// gdp_stream.cu — out-of-core z-slab streamer.
+//
+// For stacks whose finest level does not fit the HBM budget.  The finest level lives in host
+// memory: phase 1's iterate x IS the caller's I1 buffer, its rhs b = (bx Lx + by Ly) I0 is
+// recomputed on the device for every window from the 1-byte I0 (so a pass moves 4 + s_I bytes
+// per voxel host->device and 4 back, instead of 12).  Levels >= 1 stay resident.
+//
+// Phase 1 (Eq. 1).  Every finest-level pass of the V-cycle (the paper's "streaming pass over
+// the slices", two per V-cycle there, nu_pre + nu_post sweeps here) streams z-chunks in order
+// through the z-marching kernel (gdp_march3d.cu): chunk [p_lo, p_hi) needs the window
+// [p_lo - 3, p_hi + 3) of the pass's input x; the planes it shares with the previous window are
+// kept on the device (their host copies are already overwritten by the previous chunk's output,
+// which is written back in place).  Three streams overlap the H2D of chunk k+1, the kernels of
+// chunk k and the D2H of chunk k-1 (double-buffered windows, events between them).  The
+// arithmetic per voxel is the in-core kernels', so the iterate is bit-identical to the in-core
+// solve (tests/test_gpu_parity.py::test_out_of_core_*).
+//
+// Phase 2 (Eq. 2).  Slices are independent systems: batches of slices go host->device, are
+// solved in core (gdp_screened_poisson_slices) and come back; the mean-pin shift of phase 1 is
+// applied to each I1 batch on the way (and written back to the caller's I1).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "gdp_internal.h"
+
+namespace gdp {
+
+#define SK(call)                                                                          \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      return set_err(e_ == cudaErrorMemoryAllocation ? GDP_ENOMEM : GDP_ECUDA, "%s: %s (%s:%d)", #call, \
+                     cudaGetErrorString(e_), __FILE__, __LINE__);                         \
+  } while (0)
+#define SR(call)                   \
+  do {                             \
+    int r_ = (call);               \
+    if (r_ != GDP_OK) return r_;   \
+  } while (0)
+
+// pins a host range for the duration of a call if the caller passed pageable memory
+HostPin::~HostPin() { if (p) cudaHostUnregister(p); }
+int HostPin::pin(const void* ptr, size_t bytes) {
+  if (!ptr || !bytes) return GDP_OK;
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, ptr) == cudaSuccess && a.type == cudaMemoryTypeHost) return GDP_OK;
+  cudaGetLastError();
+  SK(cudaHostRegister(const_cast<void*>(ptr), bytes, cudaHostRegisterDefault));
+  p = const_cast<void*>(ptr);
+  return GDP_OK;
+}
+
+struct DevBuf {
+  void* p = nullptr;
+  ~DevBuf() { if (p) cudaFree(p); }
+  int alloc(size_t bytes) { SK(cudaMalloc(&p, std::max<size_t>(bytes, 16))); return GDP_OK; }
+  float* f() const { return static_cast<float*>(p); }
+  unsigned char* u() const { return static_cast<unsigned char*>(p); }
+};
+
+struct Streams {
+  cudaStream_t s = nullptr, ci = nullptr, co = nullptr;
+  cudaEvent_t evI[2] = {nullptr, nullptr}, evK[2] = {nullptr, nullptr}, evO[2] = {nullptr, nullptr};
+  ~Streams() {
+    for (int i = 0; i < 2; ++i) {
+      if (evI[i]) cudaEventDestroy(evI[i]);
+      if (evK[i]) cudaEventDestroy(evK[i]);
+      if (evO[i]) cudaEventDestroy(evO[i]);
+    }
+    if (s) cudaStreamDestroy(s);
+    if (ci) cudaStreamDestroy(ci);
+    if (co) cudaStreamDestroy(co);
+  }
+  int create() {
+    SK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    SK(cudaStreamCreateWithFlags(&ci, cudaStreamNonBlocking));
+    SK(cudaStreamCreateWithFlags(&co, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i) {
+      SK(cudaEventCreateWithFlags(&evI[i], cudaEventDisableTiming));
+      SK(cudaEventCreateWithFlags(&evK[i], cudaEventDisableTiming));
+      SK(cudaEventCreateWithFlags(&evO[i], cudaEventDisableTiming));
+      SK(cudaEventRecord(evK[i], s));
+      SK(cudaEventRecord(evO[i], co));
+    }
+    return GDP_OK;
+  }
+  int sync() {
+    SK(cudaStreamSynchronize(ci));
+    SK(cudaStreamSynchronize(s));
+    SK(cudaStreamSynchronize(co));
+    return GDP_OK;
+  }
+};
+
+// ---------------------------------------------------------------------------------
+// phase 1
+// ---------------------------------------------------------------------------------
+struct Stream1 {
+  Hier* H = nullptr;
+  const void* I0h = nullptr;  // host, nx*ny*nz of tI
+  float* xh = nullptr;        // host, the finest iterate (the caller's I1)
+  int tI = 0;
+  long long nx = 0, ny = 0, plane = 0;
+  int nz = 0, C = 0;          // chunk planes
+  size_t sI = 1;
+  DevBuf xin[2], xout[2], iw[2], bw[2];
+  DevBuf part;                // norm partials (init: per plane rows; sweeps: per item)
+  DevBuf psum;                // plane sums (mean pin)
+  size_t part_cap = 0;
+  Streams st;
+  long long h2d = 0, d2h = 0;  // bytes moved over the host link
+};
+
+enum { SP_INIT = 0, SP_SWEEP = 1, SP_SUMS = 2 };
+
+static int chunk_count(const Stream1& S) { return (S.nz + S.C - 1) / S.C; }
+
+// One streaming pass over the finest level.  SP_INIT: x0 = I0 (written to the host iterate),
+// initial residual partials (per plane rows).  SP_SWEEP: one red-black sweep (+ prolongation /
+// restriction / norms).  SP_SUMS: per-plane fp64 sums of x and I0 (the mean pin).
+static int stream_pass(Stream1& S, int kind, bool prolong, int tail, long long* items_out) {
+  Hier& H = *S.H;
+  const Level& L0 = H.lv[0];
+  const Level& L1 = H.lv[1];
+  Streams& T = S.st;
+  const long long pl = S.plane;
+  const int K = chunk_count(S);
+  long long items = 0;
+  int pwlo = 0, pwhi = 0;
+  for (int k = 0; k < K; ++k) {
+    const int b = k & 1;
+    const int p_lo = k * S.C, p_hi = std::min(p_lo + S.C, S.nz);
+    const int wlo = std::max(p_lo - 3, 0), whi = std::min(p_hi + 3, S.nz);
+    // ---- inputs of the window: retained planes (device), new planes (host), I0 (host)
+    SK(cudaStreamWaitEvent(T.ci, T.evK[b], 0));  // chunk k-2's kernels are done with buffer set b
+    if (kind != SP_INIT) {
+      int from = wlo;
+      if (k > 0 && kind == SP_SWEEP && pwhi > wlo) {  // planes [wlo, pwhi) still sit in the previous window
+        SK(cudaMemcpyAsync(S.xin[b].f(), S.xin[b ^ 1].f() + (wlo - pwlo) * pl, sizeof(float) * pl * (pwhi - wlo),
+                           cudaMemcpyDeviceToDevice, T.ci));
+        from = pwhi;
+      }
+      if (kind == SP_SUMS) from = p_lo;
+      const int to = kind == SP_SUMS ? p_hi : whi;
+      if (to > from) {
+        SK(cudaMemcpyAsync(S.xin[b].f() + (from - (kind == SP_SUMS ? p_lo : wlo)) * pl, S.xh + from * pl,
+                           sizeof(float) * pl * (to - from), cudaMemcpyHostToDevice, T.ci));
+        S.h2d += (long long)sizeof(float) * pl * (to - from);
+      }
+    }
+    SK(cudaMemcpyAsync(S.iw[b].u(), static_cast<const unsigned char*>(S.I0h) + S.sI * wlo * pl,
+                       S.sI * pl * (whi - wlo), cudaMemcpyHostToDevice, T.ci));
+    S.h2d += (long long)S.sI * pl * (whi - wlo);
+    SK(cudaEventRecord(T.evI[b], T.ci));
+    // ---- kernels
+    SK(cudaStreamWaitEvent(T.s, T.evI[b], 0));
+    SK(cudaStreamWaitEvent(T.s, T.evO[b], 0));  // chunk k-2's output left the device
+    const unsigned char* iwin = S.iw[b].u();
+    if (kind == SP_INIT) {
+      LevelK Lk = L0.K;
+      Lk.nzl = p_hi - p_lo;
+      Lk.z0 = p_lo;
+      RhsK R{nullptr, iwin + S.sI * (p_lo - wlo) * pl, nullptr, 0.f, 0};
+      const int per = init_blocks_per_plane(L0.nx, L0.ny);
+      launch_init(Lk, R, S.tI, S.xout[b].f(), S.bw[b].f() + (p_lo - wlo) * pl,
+                  static_cast<double2*>(S.part.p) + (long long)p_lo * per, T.s);
+    } else if (kind == SP_SWEEP) {
+      LevelK Lw = L0.K;
+      Lw.nzl = whi - wlo;
+      launch_rhs(Lw, RhsK{nullptr, iwin, nullptr, 0.f, 0}, S.tI, S.bw[b].f(), T.s);  // a2 on the window
+      items += fused_sweep3d(L0, L1, S.xin[b].f() - wlo * pl, S.xout[b].f() - p_lo * pl, S.bw[b].f() - wlo * pl,
+                             false, prolong, tail, tail == 2 ? static_cast<double2*>(S.part.p) + items : nullptr,
+                             T.s, p_lo, p_hi);
+    } else {
+      const int per = norms_blocks_per_plane(L0.nx, L0.ny);
+      launch_plane_sums(S.xin[b].f(), 1, iwin + S.sI * (p_lo - wlo) * pl, S.tI, L0.nx, L0.ny, p_hi - p_lo,
+                        static_cast<double2*>(S.part.p), static_cast<double2*>(S.psum.p) + p_lo, T.s);
+      (void)per;
+    }
+    SK(cudaGetLastError());
+    SK(cudaEventRecord(T.evK[b], T.s));
+    // ---- output of the window back to the host iterate (in place: no later window reads it)
+    if (kind != SP_SUMS) {
+      SK(cudaStreamWaitEvent(T.co, T.evK[b], 0));
+      SK(cudaMemcpyAsync(S.xh + p_lo * pl, S.xout[b].f(), sizeof(float) * pl * (p_hi - p_lo),
+                         cudaMemcpyDeviceToHost, T.co));
+      S.d2h += (long long)sizeof(float) * pl * (p_hi - p_lo);
+      SK(cudaEventRecord(T.evO[b], T.co));
+    }
+    pwlo = wlo;
+    pwhi = whi;
+  }
+  SR(T.sync());
+  if (items_out) *items_out = items;
+  return GDP_OK;
+}
+
+static int read_norms(Stream1& S, double2* plane_rows, int per, int nplanes, double& rr, double& bb) {
+  Hier& H = *S.H;
+  launch_finalize(plane_rows, per, nplanes, H.plane_sums, S.st.s);
+  SK(cudaMemcpyAsync(H.h_plane, H.plane_sums, sizeof(double2) * nplanes, cudaMemcpyDeviceToHost, S.st.s));
+  SK(cudaStreamSynchronize(S.st.s));
+  rr = bb = 0.0;
+  for (int z = 0; z < nplanes; ++z) { rr += H.h_plane[z].x; bb += H.h_plane[z].y; }
+  return GDP_OK;
+}
+
+// Phase 1 with a host-resident finest level.  xh receives I1 (before the mean pin; *shift_out
+// is the pin, applied by the caller).
+int stream_diffuse_z(Ctx& C, const void* I0h, int tI, float* xh, long long nx, long long ny, long long nz,
+                     float bx, float by, float bz, const gdp_opts& o0, size_t budget, gdp_report* rep,
+                     double* shift_out) {
+  gdp_opts o = o0;
+  o.fused |= 2;
+  HierKey key{};
+  key.nx = nx; key.ny = ny; key.nzl = nz; key.z0 = 0; key.nzg = nz;
+  key.bx = bx; key.by = by; key.bz = bz; key.alpha = 0.f;
+  key.coarse_max = o.coarse_max;
+  std::vector<Level> chain;
+  int ff;
+  SR(level_chain(key, chain, ff));
+  if (chain.size() < 2) return set_err(GDP_EINVAL, "out-of-core phase 1 needs at least two levels");
+  // resident coarse levels: x, x2, b per voxel (plus small tables)
+  double coarse = 0.0;
+  for (size_t l = 1; l < chain.size(); ++l) coarse += 12.0 * chain[l].nx * chain[l].ny * chain[l].nzl;
+  const long long pl = nx * ny;
+  const size_t sI = tI == 0 ? 1 : 4;
+  // two window sets: xin, I0, b over C+6 planes, xout over C planes
+  const double per_plane = 2.0 * (double)pl * ((4.0 + sI + 4.0) + 4.0);
+  // the budget is a target: below two-plane windows the streamer still runs (C = 2) and only
+  // a failing allocation is an error
+  const double left = (double)budget - coarse - 4.0 * 1024 * 1024;
+  int Cp = (int)std::min<double>((double)nz, std::max(2.0, std::floor(left / per_plane) - 6.0));
+  Cp = std::max(2, Cp & ~1);
+  Stream1 S;
+  S.I0h = I0h; S.xh = xh; S.tI = tI; S.nx = nx; S.ny = ny; S.plane = pl; S.nz = (int)nz; S.C = Cp; S.sI = sI;
+  std::unique_ptr<Hier> Hp;
+  SR(build_hier_levels(key, chain, 0, (int)chain.size(), false, true, Hp));
+  S.H = Hp.get();
+  if (!fusable3d(S.H->lv[0], S.H->lv[1], o))
+    return set_err(GDP_EINVAL, "out-of-core phase 1 needs an x/y-coarsened second level (stack too small?)");
+  for (int b = 0; b < 2; ++b) {
+    SR(S.xin[b].alloc(sizeof(float) * pl * (Cp + 6)));
+    SR(S.xout[b].alloc(sizeof(float) * pl * Cp));
+    SR(S.iw[b].alloc(sI * pl * (Cp + 6)));
+    SR(S.bw[b].alloc(sizeof(float) * pl * (Cp + 6)));
+  }
+  const int per_init = init_blocks_per_plane((int)nx, (int)ny);
+  long long items_all = 0;
+  for (int k = 0; k < chunk_count(S); ++k)
+    items_all += fused3d_items(S.H->lv[0], S.H->lv[1], k * Cp, std::min<int>(k * Cp + Cp, (int)nz));
+  S.part_cap = std::max<size_t>({(size_t)per_init * nz, (size_t)items_all,
+                                 (size_t)norms_blocks_per_plane((int)nx, (int)ny) * Cp});
+  SR(S.part.alloc(sizeof(double2) * S.part_cap));
+  SR(S.psum.alloc(sizeof(double2) * nz));
+  SR(S.st.create());
+  cudaEvent_t e0, e1;
+  SK(cudaEventCreate(&e0));
+  SK(cudaEventCreate(&e1));
+  SK(cudaEventRecord(e0, S.st.s));
+
+  gdp_report r{};
+  r.levels = (int)S.H->lv.size();
+  // initial guess x0 = I0, b, initial residual
+  SR(stream_pass(S, SP_INIT, false, 0, nullptr));
+  double rr, bb;
+  SR(read_norms(S, static_cast<double2*>(S.part.p), per_init, (int)nz, rr, bb));
+  double rel = bb > 0 ? std::sqrt(rr / bb) : std::sqrt(rr);
+  r.rel_res[0] = rel;
+  r.norm_b = std::sqrt(bb);
+  Fine f;  // levels >= 1 only: run_vcycle(l0 = 1) never touches the finest level
+  f.mode = RHS_B;
+  int status = GDP_OK, stall = 0, k = 0;
+  const int cap = std::min(o.max_vcycles, GDP_MAX_CYCLES);
+  while (rel > o.rel_tol) {
+    if (k >= cap) { status = GDP_ENOCONV; break; }
+    for (int i = 0; i < o.nu_pre; ++i) SR(stream_pass(S, SP_SWEEP, false, i == o.nu_pre - 1 ? 1 : 0, nullptr));
+    SR(run_vcycle(C, *S.H, f, o, S.st.s, 1));
+    SK(cudaStreamSynchronize(S.st.s));
+    long long items = 0;
+    for (int i = 0; i < o.nu_post; ++i)
+      SR(stream_pass(S, SP_SWEEP, i == 0, i == o.nu_post - 1 ? 2 : 0, &items));
+    SR(read_norms(S, static_cast<double2*>(S.part.p), (int)items, 1, rr, bb));
+    const double nrel = bb > 0 ? std::sqrt(rr / bb) : std::sqrt(rr);
+    ++k;
+    r.rel_res[k] = nrel;
+    if (o.stagnation > 0 && nrel > 0.9 * rel) {
+      if (++stall >= o.stagnation) { rel = nrel; status = nrel <= o.rel_tol ? GDP_OK : GDP_ENOCONV; break; }
+    } else {
+      stall = 0;
+    }
+    rel = nrel;
+  }
+  r.vcycles = k;
+  r.status = status;
+  // a10: mean pin, per-plane fp64 sums in plane order (the in-core reduction)
+  SR(stream_pass(S, SP_SUMS, false, 0, nullptr));
+  double2* hp = nullptr;
+  SK(cudaMallocHost(&hp, sizeof(double2) * nz));
+  cudaMemcpy(hp, S.psum.p, sizeof(double2) * nz, cudaMemcpyDeviceToHost);
+  double sx = 0.0, si = 0.0;
+  for (long long z = 0; z < nz; ++z) { sx += hp[z].x; si += hp[z].y; }
+  cudaFreeHost(hp);
+  *shift_out = (si - sx) / ((double)pl * nz);
+  SK(cudaEventRecord(e1, S.st.s));
+  SK(cudaEventSynchronize(e1));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  r.seconds = ms * 1e-3;
+  r.hbm_bytes_est = (double)(S.h2d + S.d2h);  // host-link bytes of the streamed finest level
+  if (rep) *rep = r;
+  return status;
+}
+
+// Phase 2 on slice batches; I1h gets the phase-1 mean pin `shift` added on the way (and written
+// back so the caller's I1 is the pinned solution).
+int stream_slices(Ctx& C, gdp_ctx* cctx, const void* I0h, gdp_dtype dtype, float* I1h, float* I2h, long long nx,
+                  long long ny, long long nz, float alpha, double shift, const gdp_opts& o, size_t budget,
+                  gdp_report* rep) {
+  const long long pl = nx * ny;
+  const size_t sI = dtype == GDP_U8 ? 1 : 4;
+  // per slice on the device: I0, I1, I2 of two batches + the batch hierarchy (~4 fp32 arrays)
+  const double per_slice = (double)pl * (2.0 * (sI + 8.0) + 16.0);
+  long long B = (long long)std::floor(((double)budget - 4.0 * 1024 * 1024) / per_slice);
+  B = std::max(1LL, std::min(B, nz));
+  DevBuf i0[2], i1[2], i2[2];
+  for (int b = 0; b < 2; ++b) {
+    SR(i0[b].alloc(sI * pl * B));
+    SR(i1[b].alloc(sizeof(float) * pl * B));
+    SR(i2[b].alloc(sizeof(float) * pl * B));
+  }
+  Streams T;
+  SR(T.create());
+  gdp_report agg{};
+  agg.status = GDP_OK;
+  const float fs = (float)shift;
+  int k = 0;
+  for (long long z = 0; z < nz; z += B, ++k) {
+    const int b = k & 1;
+    const long long nb = std::min(B, nz - z);
+    SK(cudaStreamWaitEvent(T.ci, T.evO[b], 0));
+    SK(cudaMemcpyAsync(i0[b].u(), static_cast<const unsigned char*>(I0h) + sI * z * pl, sI * pl * nb,
+                       cudaMemcpyHostToDevice, T.ci));
+    SK(cudaMemcpyAsync(i1[b].f(), I1h + z * pl, sizeof(float) * pl * nb, cudaMemcpyHostToDevice, T.ci));
+    SK(cudaEventRecord(T.evI[b], T.ci));
+    SK(cudaStreamWaitEvent(T.s, T.evI[b], 0));
+    if (fs != 0.f) {
+      launch_add_scalar(i1[b].f(), pl * nb, fs, T.s);  // a10 on the way (k_add_scalar arithmetic)
+      SK(cudaEventRecord(T.evK[b], T.s));
+      SK(cudaStreamWaitEvent(T.co, T.evK[b], 0));
+      SK(cudaMemcpyAsync(I1h + z * pl, i1[b].f(), sizeof(float) * pl * nb, cudaMemcpyDeviceToHost, T.co));
+    }
+    gdp_report r{};
+    gdp_dims d{nx, ny, nb};
+    const int st = gdp_screened_poisson_slices(cctx, i0[b].p, dtype, i1[b].f(), i2[b].f(), d, alpha, &o, &r, T.s);
+    if (st != GDP_OK && st != GDP_ENOCONV) return st;
+    if (st == GDP_ENOCONV) agg.status = GDP_ENOCONV;
+    SK(cudaEventRecord(T.evK[b], T.s));
+    SK(cudaStreamWaitEvent(T.co, T.evK[b], 0));
+    SK(cudaMemcpyAsync(I2h + z * pl, i2[b].f(), sizeof(float) * pl * nb, cudaMemcpyDeviceToHost, T.co));
+    SK(cudaEventRecord(T.evO[b], T.co));
+    agg.vcycles = std::max(agg.vcycles, r.vcycles);
+    agg.levels = r.levels;
+    agg.seconds += r.seconds;
+    for (int i = 0; i <= r.vcycles && i <= GDP_MAX_CYCLES; ++i) agg.rel_res[i] = std::max(agg.rel_res[i], r.rel_res[i]);
+    agg.norm_b = std::max(agg.norm_b, r.norm_b);
+    agg.kernel_launches += r.kernel_launches;
+  }
+  SR(T.sync());
+  (void)C;
+  if (rep) *rep = agg;
+  return agg.status;
+}
+
+}  // namespace gdp

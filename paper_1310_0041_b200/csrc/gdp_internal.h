@@ -122,7 +122,11 @@ void fused_down2d(const Level& L, const Level& C, const float* xin, float* xout,
                   int mode, int tI, int nu, bool zero_x, cudaStream_t s);
 void fused_up2d(const Level& L, const Level& C, const float* xin, float* xout, const RhsK& R,
                 int mode, int tI, int nu, double2* partials, cudaStream_t s);
-int fused_tiles_per_plane(int nu, const LevelK& L);
+int fused_tiles_per_plane(int nu, const Level& L, const Level& C);
+// row-marching 2D passes (gdp_rows2d.cu)
+int rows2d_items_per_plane(int nu, const LevelK& L);
+void rows2d_pass(bool down, int nu, const Level& L, const Level& C, const float* xin, float* xout, const float* b,
+                 bool zero_x, double2* partials, cudaStream_t s);
 bool fusable3d(const Level& L, const Level& C, const gdp_opts& o);
 int fused3d_items(const Level& L, const Level& C, int zlo = 0, int zhi = -1);
 int fused_sweep3d(const Level& L, const Level& C, const float* xin, float* xout, const float* b,

@@ -400,7 +400,8 @@ int build_hier_levels(const HierKey& key, const std::vector<Level>& chain, int f
   H->coarse = C;
   // norm partials: level-0 plane rows
   int per = std::max(norms_blocks_per_plane(H->lv[0].nx, H->lv[0].ny), init_blocks_per_plane(H->lv[0].nx, H->lv[0].ny));
-  for (int nu = 1; nu <= 2; ++nu) per = std::max(per, fused_tiles_per_plane(nu, H->lv[0].K));
+  if (nl > 1)
+    for (int nu = 1; nu <= 2; ++nu) per = std::max(per, fused_tiles_per_plane(nu, H->lv[0], H->lv[1]));
   H->partials_cap = (size_t)per;
   CK(cudaMalloc(&H->partials, (size_t)per * std::max<long long>(maxplanes, 1) * sizeof(double2)));
   CK(cudaMalloc(&H->plane_sums, (size_t)std::max<long long>(maxplanes, 1) * sizeof(double2)));
@@ -529,9 +530,10 @@ int run_vcycle(Ctx& ctx, Hier& H, const Fine& f, const gdp_opts& o, cudaStream_t
     int mode = f.mode, tI = f.tI;
     if (l > 0) { R = RhsK{L.b, nullptr, nullptr, 0.f, 0}; mode = RHS_B; tI = 1; }
     if (fz[l] == 2) {  // one fused pass: x2 (B) -> x (A), norms of the finest level on the way
-      const bool want = l == 0 && (size_t)fused_tiles_per_plane(o.nu_post, L.K) <= H.partials_cap;
+      const int per2 = fused_tiles_per_plane(o.nu_post, L, C);
+      const bool want = l == 0 && (size_t)per2 <= H.partials_cap;
       fused_up2d(L, C, L.x2, x, R, mode, tI, o.nu_post, want ? H.partials : nullptr, s);
-      if (want) { H.up_norm_per = fused_tiles_per_plane(o.nu_post, L.K); H.up_norm_planes = L.nzl; }
+      if (want) { H.up_norm_per = per2; H.up_norm_planes = L.nzl; }
       continue;
     }
     if (fz[l] == 3) {  // prolongation fused into the first sweep, norms into the last
@@ -701,6 +703,8 @@ int gdp_opts_default(gdp_opts* o) {
   o->stagnation = 2;
   o->fused = 3;
   o->use_graphs = 0;
+  o->nu_pre_slices = 2;
+  o->nu_post_slices = 1;
   return GDP_OK;
 }
 
@@ -836,7 +840,9 @@ int gdp_screened_poisson_slices(gdp_ctx* ctx, const void* I0, gdp_dtype dtype, c
   if (dtype != GDP_U8 && dtype != GDP_F32) return set_err(GDP_EINVAL, "bad dtype");
   if (local.nx <= 0 || local.ny <= 0 || local.nz <= 0) return set_err(GDP_EINVAL, "dims must be positive");
   CK(cudaSetDevice(ctx->impl.device));
-  const gdp_opts o = resolve_opts(opts);
+  gdp_opts o = resolve_opts(opts);
+  if (o.nu_pre_slices >= 0) o.nu_pre = o.nu_pre_slices;  // per-phase smoothing (gdp.h)
+  if (o.nu_post_slices >= 0) o.nu_post = o.nu_post_slices;
   cudaStream_t s = (cudaStream_t)stream;
   Ctx& C = ctx->impl;
   const long long before = g_launches.load();

@@ -1,0 +1,30 @@
+"""profiles/ncu_full_summary.json: DRAM bytes per launch of the bench's kernel classes (finest
+level), from an ncu --set full summary (tools/ncu_summary.py output).  The largest-traffic
+instance of each template variant is its finest-level launch; a class averages the variants it
+contains with equal weight (each runs once per V-cycle at the finest level)."""
+import json, re, sys, collections
+
+rows = json.load(open(sys.argv[1]))
+best = {}
+for r in rows:
+    name = r["kernel"].split("(")[0]
+    b = r["dram_read_B"] + r["dram_write_B"]
+    if name not in best or b > best[name]["bytes"]:
+        best[name] = {"bytes": b, "time_s": r["time_s"]}
+classes = collections.defaultdict(list)
+for name, v in best.items():
+    m = re.search(r"k_march3d<(\d+), (\d+), (\d+), (\d+)>", name)
+    if m:
+        tail, prolong = int(m.group(1)), int(m.group(2))
+        classes["up3d@L0" if prolong and tail != 1 else "down3d@L0"].append(v)
+        continue
+    m = re.search(r"k_pass2d<(\d+), (\d+)>", name)
+    if m:
+        classes["down2d@L0" if int(m.group(2)) else "up2d@L0"].append(v)
+        continue
+    if "k_init" in name:
+        classes["init@L0"].append(v)
+out = {c: {"dram_bytes_per_launch": sum(x["bytes"] for x in vs) / len(vs),
+           "ncu_time_s_per_launch": sum(x["time_s"] for x in vs) / len(vs), "variants": len(vs)}
+       for c, vs in classes.items()}
+print(json.dumps(out, indent=1))

@@ -9,7 +9,7 @@ I0 = torch.from_numpy(synth.make_config(1)).cuda()
 I1 = torch.empty(I0.shape, dtype=torch.float32, device="cuda")
 I2 = torch.empty_like(I1)
 for nu in [(2, 2), (1, 1), (2, 1), (1, 2), (3, 3)]:
-    o = gdp.default_opts(nu_pre=nu[0], nu_post=nu[1])
+    o = gdp.default_opts(nu_pre=nu[0], nu_post=nu[1], nu_pre_slices=nu[0], nu_post_slices=nu[1])
     res = []
     for rep in range(3):
         e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]

@@ -116,3 +116,25 @@ def random_field(shape, seed: int, lo: float = 0.0, hi: float = 1.0) -> np.ndarr
     rng = np.random.default_rng([int(seed), 7777])
     return (lo + (hi - lo) * rng.random(shape)).astype(np.float32)
 
+
+
+def cosine_mode(i: np.ndarray, k: int, n: int) -> np.ndarray:
+    """Neumann cosine mode cos(pi k (i + 1/2) / n) at integer cells i (fp64)."""
+    return np.cos(np.pi * k * (np.asarray(i, dtype=np.float64) + 0.5) / n)
+
+
+def cosine_modes(shape, modes, amps, c0: float = 0.5, block: int = 512) -> np.ndarray:
+    """fp32 stack c0 + sum_j amps[j] * phi_kj(x) phi_lj(y) phi_mj(z), shape (nz, ny, nx), built in
+    row blocks (config-2 slices do not fit fp64 temporaries).  modes: list of (k, l, m)."""
+    nz, ny, nx = shape
+    out = np.empty(shape, dtype=np.float32)
+    fx = [cosine_mode(np.arange(nx), k, nx) for k, _, _ in modes]
+    fz = [cosine_mode(np.arange(nz), m, nz) for _, _, m in modes]
+    for z in range(nz):
+        for y0 in range(0, ny, block):
+            ys = np.arange(y0, min(y0 + block, ny))
+            acc = np.full((len(ys), nx), c0, dtype=np.float64)
+            for j, (k, l, m) in enumerate(modes):
+                acc += (amps[j] * fz[j][z]) * np.outer(cosine_mode(ys, l, ny), fx[j])
+            out[z, y0:y0 + len(ys)] = acc.astype(np.float32)
+    return out

@@ -8,6 +8,8 @@
 // contributor (each rank fills its own planes of a zeroed array, then a sum-allreduce).
 #include <nccl.h>
 
+#include <vector>
+
 #include "gdp_internal.h"
 
 namespace gdp {
@@ -112,6 +114,42 @@ int comm_halo_parts(Ctx& c, DistPlan& D, int l, float* const* xs, cudaStream_t s
   if (c.rank < c.world - 1) {
     NCK(ncclSend(xs[0] + (size_t)(L.nzl - 1) * pl, pl, ncclFloat, c.rank + 1, c.comm->nc, s));
     NCK(ncclRecv(L.xhi, pl, ncclFloat, c.rank + 1, c.comm->nc, s));
+  }
+  NCK(ncclGroupEnd());
+  return GDP_OK;
+}
+
+// G = DistPlan::G ghost planes per face of the finest-level windows (interior at offset G):
+// the bottom ghosts of slab i <- the top G interior planes of slab i-1, the top ghosts <- the
+// bottom G interior planes of slab i+1 (every slab has >= G planes).
+int comm_ghosts(Ctx& c, DistPlan& D, float* const* wins, cudaStream_t s, int level) {
+  const int np = (int)D.parts.size();
+  const Level& L0 = D.parts[0]->lv[level];
+  const size_t pl = (size_t)L0.nx * L0.ny;
+  const int G = DistPlan::G;
+  std::vector<int> nzl(np);
+  for (int i = 0; i < np; ++i) nzl[i] = D.parts[i]->lv[level].nzl;
+  const size_t gb = pl * G * sizeof(float);
+  if (c.world == 1) {
+    for (int i = 0; i < np; ++i) {
+      if (i > 0)
+        CKC(cudaMemcpyAsync(wins[i], wins[i - 1] + (size_t)nzl[i - 1] * pl, gb, cudaMemcpyDeviceToDevice, s));
+      if (i < np - 1)
+        CKC(cudaMemcpyAsync(wins[i] + (size_t)(G + nzl[i]) * pl, wins[i + 1] + (size_t)G * pl, gb,
+                            cudaMemcpyDeviceToDevice, s));
+    }
+    return GDP_OK;
+  }
+  float* w = wins[0];
+  const int n = nzl[0];
+  NCK(ncclGroupStart());
+  if (c.rank > 0) {
+    NCK(ncclSend(w + (size_t)G * pl, pl * G, ncclFloat, c.rank - 1, c.comm->nc, s));
+    NCK(ncclRecv(w, pl * G, ncclFloat, c.rank - 1, c.comm->nc, s));
+  }
+  if (c.rank < c.world - 1) {
+    NCK(ncclSend(w + (size_t)n * pl, pl * G, ncclFloat, c.rank + 1, c.comm->nc, s));
+    NCK(ncclRecv(w + (size_t)(G + n) * pl, pl * G, ncclFloat, c.rank + 1, c.comm->nc, s));
   }
   NCK(ncclGroupEnd());
   return GDP_OK;

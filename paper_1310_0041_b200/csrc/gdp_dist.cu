@@ -10,6 +10,7 @@
 // partition (tests/test_gpu_parity.py::test_loopback_partition_bit_identical).
 #include <cmath>
 #include <cstring>
+#include <vector>
 
 #include "gdp_internal.h"
 
@@ -18,6 +19,11 @@ namespace gdp {
 DistPlan::~DistPlan() {
   if (h_planes) cudaFreeHost(h_planes);
   for (auto* p : b0) if (p) cudaFree(p);
+  for (auto* p : w0) if (p) cudaFree(p);
+  for (auto* p : w1) if (p) cudaFree(p);
+  for (auto* p : bw) if (p) cudaFree(p);
+  for (auto* p : cw) if (p) cudaFree(p);
+  if (fpart) cudaFree(fpart);
 }
 
 #define CKD(call)                                                                         \
@@ -125,7 +131,72 @@ static int team_smooth(Ctx& c, DistPlan& D, int l, float* const* xs, const float
   return GDP_OK;
 }
 
-static int team_vcycle(Ctx& c, DistPlan& D, float* const* x0, const gdp_opts& o, cudaStream_t s) {
+// the level below level 0 of part i, with its arrays offset so that they are indexed by global
+// plane (the split level 1 of the part, or the gathered tail's first level)
+static Level coarse_of(DistPlan& D, int i) {
+  Level C = D.ff > 1 ? D.parts[i]->lv[1] : D.tail->lv[0];
+  if (D.ff > 1) {
+    const size_t cpl = (size_t)C.nx * C.ny;
+    C.b -= (long long)C.z0 * cpl;
+    C.x -= (long long)C.z0 * cpl;
+  }
+  return C;
+}
+
+// nu fused sweeps of the finest level on every local slab (k_march3d over the slab's global
+// planes, G ghost planes exchanged before each sweep).  *cur: which window holds x; tail 1 =
+// restrict the last sweep, 2 = norms of the last sweep (partials per item, all slabs, summed
+// into *rr / *bb over slabs and ranks), prolong = add the coarse correction in the first sweep.
+static int team_fused_sweeps(Ctx& c, DistPlan& D, int* cur, int nu, bool prolong, int tail, double* rr,
+                             double* bb, cudaStream_t s) {
+  const int np = (int)D.parts.size();
+  const size_t pl = (size_t)D.parts[0]->lv[0].nx * D.parts[0]->lv[0].ny;
+  const int G = DistPlan::G;
+  long long items = 0;
+  if (prolong && D.ff > 1) {
+    // the first sweep also corrects the G ghost planes of the window, whose coarse planes
+    // belong to the neighbouring slabs: level 1's x with G ghost planes per face
+    for (int i = 0; i < np; ++i) {
+      const Level& C = D.parts[i]->lv[1];
+      const size_t cpl = (size_t)C.nx * C.ny;
+      CKD(cudaMemcpyAsync(D.cw[i] + (size_t)G * cpl, C.x, sizeof(float) * cpl * C.nzl, cudaMemcpyDeviceToDevice, s));
+    }
+    RETD(comm_ghosts(c, D, D.cw.data(), s, 1));
+  }
+  for (int k = 0; k < nu; ++k) {
+    std::vector<float*>& src = *cur ? D.w1 : D.w0;
+    std::vector<float*>& dst = *cur ? D.w0 : D.w1;
+    RETD(comm_ghosts(c, D, src.data(), s));
+    const bool last = k == nu - 1;
+    for (int i = 0; i < np; ++i) {
+      const Level& L = D.parts[i]->lv[0];
+      Level C = coarse_of(D, i);
+      if (prolong && D.ff > 1)
+        C.x = D.cw[i] + ((long long)G - D.parts[i]->lv[1].z0) * (long long)C.nx * C.ny;
+      const long long off = (long long)G - D.z0[i];  // window offset of global plane 0 (planes)
+      const int t = last ? tail : 0;
+      const int n = fused_sweep3d(L, C, src[i] + off * (long long)pl, dst[i] + off * (long long)pl,
+                                  D.bw[i] + off * (long long)pl, false, prolong && k == 0, t,
+                                  t == 2 ? D.fpart + items : nullptr, s, (int)D.z0[i], (int)(D.z0[i] + D.nzl[i]));
+      if (t == 2) items += n;  // partials of the norms sweep only
+    }
+    *cur ^= 1;
+  }
+  CKD(cudaGetLastError());
+  if (tail == 2) {
+    Hier& H = *D.parts[0];
+    launch_finalize(D.fpart, (int)items, 1, H.plane_sums, s);
+    CKD(cudaMemcpyAsync(H.h_plane, H.plane_sums, sizeof(double2), cudaMemcpyDeviceToHost, s));
+    CKD(cudaStreamSynchronize(s));
+    *rr = H.h_plane[0].x;
+    *bb = H.h_plane[0].y;
+    RETD(comm_allreduce_sum2(c, rr, bb, s));
+  }
+  return GDP_OK;
+}
+
+static int team_vcycle(Ctx& c, DistPlan& D, float* const* x0, const gdp_opts& o, cudaStream_t s, int* cur,
+                       double* rel) {
   const int np = (int)D.parts.size();
   const int ff = D.ff;
   std::vector<float*> xs(np);
@@ -133,7 +204,11 @@ static int team_vcycle(Ctx& c, DistPlan& D, float* const* x0, const gdp_opts& o,
   Hier& T = *D.tail;
   Level& TF = T.lv[0];
   const size_t tplane = (size_t)TF.nx * TF.ny;
-  for (int l = 0; l < ff; ++l) {
+  if (D.active) {
+    if (ff == 1 && c.world > 1) CKD(cudaMemsetAsync(TF.b, 0, sizeof(float) * tplane * TF.nzl, s));
+    RETD(team_fused_sweeps(c, D, cur, o.nu_pre, false, 1, nullptr, nullptr, s));
+  }
+  for (int l = D.active ? 1 : 0; l < ff; ++l) {
     for (int i = 0; i < np; ++i) {
       Level& L = D.parts[i]->lv[l];
       xs[i] = l == 0 ? x0[i] : L.x;
@@ -167,7 +242,7 @@ static int team_vcycle(Ctx& c, DistPlan& D, float* const* x0, const gdp_opts& o,
   ft.tI = 1;
   ft.R = RhsK{TF.b, nullptr, nullptr, 0.f, 0};
   RETD(run_vcycle(c, T, ft, o, s));
-  for (int l = ff - 1; l >= 0; --l) {
+  for (int l = ff - 1; l >= (D.active ? 1 : 0); --l) {
     for (int i = 0; i < np; ++i) {
       Level& L = D.parts[i]->lv[l];
       xs[i] = l == 0 ? x0[i] : L.x;
@@ -188,6 +263,16 @@ static int team_vcycle(Ctx& c, DistPlan& D, float* const* x0, const gdp_opts& o,
       }
     }
     RETD(team_smooth(c, D, l, xs.data(), bs.data(), o.nu_post, s));
+  }
+  if (D.active) {
+    if (ff > 1) {  // the split level 1 feeds the prolongation: refresh its ghost planes
+      std::vector<float*> xc(np);
+      for (int i = 0; i < np; ++i) xc[i] = D.parts[i]->lv[1].x;
+      RETD(comm_halo_parts(c, D, 1, xc.data(), s));
+    }
+    double rr = 0.0, bb = 0.0;
+    RETD(team_fused_sweeps(c, D, cur, o.nu_post, true, 2, &rr, &bb, s));
+    *rel = bb > 0 ? std::sqrt(rr / bb) : std::sqrt(rr);
   }
   CKD(cudaGetLastError());
   return GDP_OK;
@@ -246,29 +331,85 @@ int dist_diffuse_z(Ctx& c, const void* I0, int tI, float* I1, long long nx, long
   std::vector<float*> x0(np);
   std::vector<const void*> i0(np);
   const long long before = g_launches.load();
+  // fused finest level: every slab holds >= G planes, the next level is x/y-coarsened only
+  if (D->w0.empty()) {
+    bool ok = (o.fused & 2) != 0 && (long long)nx * ny < (1LL << 31);
+    for (int i = 0; i < np && ok; ++i) {
+      const Level& L = D->parts[i]->lv[0];
+      const Level C = coarse_of(*D, i);
+      ok = L.K.az.k != 0.f && C.tx.coarsened && C.ty.coarsened && !C.tz.coarsened;
+    }
+    for (size_t i = 0; i < D->nzl.size() && ok; ++i) ok = D->nzl[i] >= DistPlan::G;
+    for (int i = 0; i < np && ok && D->ff > 1; ++i) ok = D->parts[i]->lv[1].nzl >= DistPlan::G;
+    if (ok) {
+      D->fused = true;
+      long long items = 0;
+      for (int i = 0; i < np; ++i) {
+        float *a = nullptr, *b = nullptr, *w = nullptr;
+        const size_t n = plane * (size_t)(D->nzl[i] + 2 * DistPlan::G);
+        CKD(cudaMalloc(&a, n * sizeof(float)));
+        CKD(cudaMalloc(&b, n * sizeof(float)));
+        CKD(cudaMalloc(&w, n * sizeof(float)));
+        CKD(cudaMemset(a, 0, n * sizeof(float)));
+        CKD(cudaMemset(b, 0, n * sizeof(float)));
+        CKD(cudaMemset(w, 0, n * sizeof(float)));
+        D->w0.push_back(a);
+        D->w1.push_back(b);
+        D->bw.push_back(w);
+        if (D->ff > 1) {
+          const Level& C = D->parts[i]->lv[1];
+          float* q = nullptr;
+          const size_t cn = (size_t)C.nx * C.ny * (C.nzl + 2 * DistPlan::G);
+          CKD(cudaMalloc(&q, cn * sizeof(float)));
+          CKD(cudaMemset(q, 0, cn * sizeof(float)));
+          D->cw.push_back(q);
+        }
+        items += fused3d_items(D->parts[i]->lv[0], coarse_of(*D, i), (int)D->z0[i], (int)(D->z0[i] + D->nzl[i]));
+      }
+      D->fpart_cap = (size_t)items;
+      CKD(cudaMalloc(&D->fpart, sizeof(double2) * D->fpart_cap));
+    }
+  }
+  D->active = D->fused && (o.fused & 2);
+  std::vector<float*> b0own = D->b0;  // active: the rhs lives in the ghosted windows for this call
+  struct Restore {
+    DistPlan* D;
+    std::vector<float*>* own;
+    ~Restore() { D->b0 = *own; }
+  } restore{D, &b0own};
+  if (D->active)
+    for (int i = 0; i < np; ++i) D->b0[i] = D->bw[i] + plane * DistPlan::G;
   CKD(cudaEventRecord(c.ev0, s));
   for (int i = 0; i < np; ++i) {
     const long long off = D->z0[i] - base_z;
     x0[i] = I1 + off * plane;
     i0[i] = static_cast<const char*>(I0) + off * plane * sI;
     Level& L = D->parts[i]->lv[0];
-    if (!D->b0[i]) CKD(cudaMalloc(&D->b0[i], sizeof(float) * plane * D->nzl[i]));
-    launch_decode_copy(i0[i], tI, x0[i], (long long)plane * D->nzl[i], s);  // x0 = I0
+    if (!D->b0[i]) {
+      CKD(cudaMalloc(&D->b0[i], sizeof(float) * plane * D->nzl[i]));
+      b0own[i] = D->b0[i];
+    }
+    float* xi = D->active ? D->w0[i] + plane * DistPlan::G : x0[i];
+    launch_decode_copy(i0[i], tI, xi, (long long)plane * D->nzl[i], s);  // x0 = I0
     launch_rhs(L.K, RhsK{nullptr, i0[i], nullptr, 0.f, 0}, tI, D->b0[i], s);
   }
+  int cur = 0;  // fused: the window holding x
+  std::vector<float*> xw(np);
+  for (int i = 0; i < np; ++i) xw[i] = D->active ? D->w0[i] + plane * DistPlan::G : x0[i];
+  if (D->active) RETD(comm_ghosts(c, *D, D->bw.data(), s));  // the rhs ghosts, once per solve
   gdp_report r{};
   r.levels = D->ff + (int)D->tail->lv.size();
   double rel, nb;
-  RETD(team_norms(c, *D, x0.data(), &rel, &nb, s));
+  RETD(team_norms(c, *D, xw.data(), &rel, &nb, s));
   r.rel_res[0] = rel;
   r.norm_b = nb;
   int status = GDP_OK, stall = 0, k = 0;
   const int cap = std::min(o.max_vcycles, GDP_MAX_CYCLES);
   while (rel > o.rel_tol) {
     if (k >= cap) { status = GDP_ENOCONV; break; }
-    RETD(team_vcycle(c, *D, x0.data(), o, s));
-    double nrel;
-    RETD(team_norms(c, *D, x0.data(), &nrel, nullptr, s));
+    double nrel = 0.0;
+    RETD(team_vcycle(c, *D, x0.data(), o, s, &cur, &nrel));
+    if (!D->active) RETD(team_norms(c, *D, x0.data(), &nrel, nullptr, s));
     r.rel_res[++k] = nrel;
     if (o.stagnation > 0 && nrel > 0.9 * rel) {
       if (++stall >= o.stagnation) { rel = nrel; status = nrel <= o.rel_tol ? GDP_OK : GDP_ENOCONV; break; }
@@ -277,6 +418,10 @@ int dist_diffuse_z(Ctx& c, const void* I0, int tI, float* I1, long long nx, long
     }
     rel = nrel;
   }
+  if (D->active)  // the iterate back into the caller's slabs
+    for (int i = 0; i < np; ++i)
+      CKD(cudaMemcpyAsync(x0[i], (cur ? D->w1[i] : D->w0[i]) + plane * DistPlan::G,
+                          sizeof(float) * plane * D->nzl[i], cudaMemcpyDeviceToDevice, s));
   // a10: mean(I1) = mean(I0), fp64 sums in global plane order
   std::vector<double2*> loc(np);
   for (int i = 0; i < np; ++i) {

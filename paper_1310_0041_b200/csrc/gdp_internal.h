@@ -82,6 +82,15 @@ struct DistPlan {
   int ff = 0;                                // first full level
   int nzg = 0;
   double2* h_planes = nullptr;               // pinned, nzg per-plane sums in global order
+  // fused finest level (k_march3d): per local slab two x windows and the rhs with G ghost planes
+  // per face ([z0 - G, z0 + nzl + G), interior at offset G); exchanged once per sweep
+  static constexpr int G = 3;
+  bool fused = false;                        // windows allocated
+  bool active = false;                       // this call runs the fused finest level (opts.fused & 2)
+  std::vector<float*> w0, w1, bw;
+  std::vector<float*> cw;                    // split level 1: x with G ghost planes (prolongation source)
+  double2* fpart = nullptr;                  // norm partials of the fused up pass (all local slabs)
+  size_t fpart_cap = 0;
   ~DistPlan();
 };
 
@@ -155,6 +164,7 @@ int comm_unique_id(void* out, size_t n);
 int comm_halo_parts(Ctx& c, DistPlan& D, int l, float* const* xs, cudaStream_t s);
 int comm_gather_full(Ctx& c, float* full, size_t n, cudaStream_t s);
 int comm_plane_sums(Ctx& c, DistPlan& D, double2* const* local, double2* out, cudaStream_t s);
+int comm_ghosts(Ctx& c, DistPlan& D, float* const* wins, cudaStream_t s, int level = 0);
 int dist_diffuse_z(Ctx& c, const void* I0, int tI, float* I1, long long nx, long long ny, long long nzl,
                    long long z0g, long long nzg, float bx, float by, float bz, float alpha, const gdp_opts& o,
                    gdp_report* rep, cudaStream_t s);

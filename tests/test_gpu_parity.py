@@ -266,6 +266,24 @@ def test_loopback_partition_bit_identical(gpu_ctx, shape, world):
     assert np.abs(host(out) - O.diffuse_z(I0)).max() <= TOL_X
 
 
+@pytest.mark.parametrize("shape,world", [((48, 128, 256), 2), ((40, 130, 250), 4), ((128, 256, 256), 8),
+                                         ((27, 96, 200), 3)])
+def test_loopback_fused_partition_bit_identical(gpu_ctx, shape, world):
+    """Default opts: the finest level of every slab runs the fused z-march sweeps with 3 ghost
+    planes per face; the iterate equals the single-rank fused solve bit for bit."""
+    nz, ny, nx = shape
+    I0 = synth.make_stack(nx, ny, nz, 53, "u8")
+    ref, r1 = gdp.gdp_diffuse_z(gpu_ctx, dev(I0))
+    lb = gdp.Ctx(0, loopback=world)
+    try:
+        out, r2 = gdp.gdp_diffuse_z(lb, dev(I0))
+    finally:
+        lb.close()
+    assert r1["vcycles"] == r2["vcycles"]
+    assert np.allclose(r1["rel_res"], r2["rel_res"], rtol=1e-9, atol=0)
+    assert np.array_equal(ref.cpu().numpy(), out.cpu().numpy())
+
+
 def test_loopback_destripe_and_slices(gpu_ctx):
     I0 = synth.make_stack(80, 72, 20, 52, "u8")
     a = gdp.gdp_destripe(gpu_ctx, dev(I0), opts=gdp.default_opts(fused=0))

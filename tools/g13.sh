@@ -1,0 +1,2 @@
+python -c "import __graft_entry__ as g; g.build()" || exit 1
+timeout 400 python -m pytest tests/test_gpu_parity.py -x -q -k "loopback" 2>&1 | grep -E "passed|failed|Error|^E " | head -20

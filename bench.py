@@ -325,7 +325,8 @@ def main():
                 "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
                 "config": {"workload": c["name"], "dims": [nx, ny, nz], "input": c["dtype"], "alpha": args.alpha,
-                           "W": list(W), "rel_tol": 1e-6, "nu": [opts.nu_pre, opts.nu_post],
+                           "W": list(W), "rel_tol": 1e-6, "nu_phase1": [opts.nu_pre, opts.nu_post],
+                           "nu_phase2": [opts.nu_pre_slices, opts.nu_post_slices],
                            "schedule": "fused" if args.fused else "reference",
                            "l2": "working set > L2 (I0 134 MB + three 537 MB fp32 volumes); no flush",
                            "parallelism": f"z-slabs x{world} (phase 1 NCCL halo, phase 2 slab-local)",

@@ -26,6 +26,9 @@ from .gdp_oracle import (  # noqa: F401
     destripe,
     residual,
     rel_residual,
+    npr_gradient_field,
+    rhs_npr,
+    npr_filter,
     slice_rel_residuals,
 )
 from .closed_form import (  # noqa: F401

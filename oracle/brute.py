@@ -90,3 +90,22 @@ def minimiser(A, b, singular_mean=None):
         return np.linalg.solve(A, b)
     x = np.linalg.lstsq(A, b, rcond=None)[0]
     return x - x.mean() + singular_mean
+
+
+def npr_G(I0, lam, sigma):
+    """Target gradient of the §6 NPR filter link by link: the gradient
+    magnitude is the 3D forward-difference gradient at the link's base voxel (reading n-1)."""
+    shape = I0.shape
+
+    def mag2(c):
+        z, y, x = c
+        s = 0.0
+        for dz, dy, dx in ((0, 0, 1), (0, 1, 0), (1, 0, 0)):
+            n = (z + dz, y + dy, x + dx)
+            if n[0] < shape[0] and n[1] < shape[1] and n[2] < shape[2]:
+                s += float(I0[n] - I0[c]) ** 2
+        return s
+
+    def G(c, n, ax):
+        return lam * (1.0 - np.exp(-mag2(c) / (2.0 * sigma * sigma))) * float(I0[n] - I0[c])
+    return G

@@ -213,3 +213,44 @@ def slice_rel_residuals(x, b, alpha) -> np.ndarray:
     rn = np.sqrt(np.sum(r * r, axis=(1, 2)))
     bn = np.sqrt(np.sum(b * b, axis=(1, 2)))
     return rn / np.where(bn > 0, bn, 1.0)
+
+
+# ---------------------------------------------------------------------------
+# NEXT-1: the §6 NPR filter (after Bhat et al. §6.2)
+#   I1 = argmin  alpha (I - I0)^2 + || grad I - V ||_W^2,
+#   V  = lam (1 - exp(-|grad I0|^2 / (2 sigma^2))) grad I0
+# Readings: n-1 |grad I0|^2 of a link is the squared norm of the full 3D
+# forward-difference gradient at the link's base voxel (absent links contribute 0);
+# n-2 sigma = 5 on the paper's [0,256) gray scale is 5/255 on the u8/255 scale used here (c-9).
+# ---------------------------------------------------------------------------
+def npr_gradient_field(I0f, lam: float, sigma: float) -> dict:
+    """V_{lam,sigma} on links {axis: values of the (n_d - 1) links}."""
+    I = np.asarray(I0f, dtype=np.float64)
+    G = gradient(I)
+    mag2 = np.zeros(I.shape)
+    for a, g in G.items():
+        pad = [(0, 0)] * I.ndim
+        pad[AXIS[a]] = (0, 1)  # the last voxel along the axis has no forward link
+        mag2 += np.pad(g, pad) ** 2
+    V = {}
+    for a, g in G.items():
+        base = [slice(None)] * I.ndim
+        base[AXIS[a]] = slice(0, -1)  # link (c, c + e_a) has base voxel c
+        V[a] = lam * (1.0 - np.exp(-mag2[tuple(base)] / (2.0 * sigma * sigma))) * g
+    return V
+
+
+def rhs_npr(I0f, W, alpha, lam, sigma) -> np.ndarray:
+    """b = alpha I0 - nabla.(W V)  (the §4 rhs with V as the gradient target)."""
+    I = np.asarray(I0f, dtype=np.float64)
+    return rhs_general(I, npr_gradient_field(I, lam, sigma), W, alpha)
+
+
+def npr_filter(I0, W=(1.0, 1.0, 0.1), alpha=0.001, lam=1.25, sigma=5.0 / 255.0, tol=1e-10, return_info=False):
+    """§6 NPR filter: (alpha - nabla.W nabla) I1 = alpha I0 - nabla.(W V), CG from x0 = I0."""
+    if not alpha > 0:
+        raise ValueError("the NPR filter is a screened solve (alpha > 0)")
+    I = _as_f64(I0)
+    b = rhs_npr(I, W, alpha, lam, sigma)
+    x, info = cg(lambda u: apply_A(u, W, alpha), b, I, tol=tol)
+    return (x, info) if return_info else x

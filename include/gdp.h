@@ -169,6 +169,19 @@ int gdp_destripe_host(gdp_ctx* ctx, const void* I0_host, gdp_dtype dtype, float*
                       gdp_weights W, float alpha, size_t hbm_budget_bytes, const gdp_opts* opts,
                       gdp_report* rep1, gdp_report* rep2);
 
+/* NEXT-1 — the §6 NPR filter (after Bhat et al. §6.2): a general 3D
+ * screened solve through the same V-cycle,
+ *   out = argmin alpha (I - I0)^2 + || grad I - V ||_W^2,
+ *   V   = lambda (1 - exp(-|grad I0|^2 / (2 sigma^2))) grad I0  on every link,
+ * |grad I0|^2 being the 3D forward-difference gradient at the link's base voxel (DESIGN.md
+ * reading n-1).  Intensities are on the u8/255 scale, so the paper's sigma = 5 gray levels is
+ * sigma = 5/255 (reading n-2); paper values alpha = 0.001, W = (1, 1, 0.1), lambda = 1.25.
+ *   I0   device, nx*ny*nz of dtype;  out  device fp32 (may not alias I0); single rank.
+ * Errors: GDP_EINVAL for alpha <= 0, sigma <= 0, lambda < 0 or non-finite parameters.     */
+int gdp_npr_filter(gdp_ctx* ctx, const void* I0, gdp_dtype dtype, float* out, gdp_dims dims, gdp_weights W,
+                   float alpha, float lambda, float sigma, const gdp_opts* opts, gdp_report* report,
+                   void* stream);
+
 /* One V-cycle on (alpha - div W grad) x = b.  x device fp32 in/out,
  * b device fp32.  With alpha = 0, b is used as given (the caller guarantees sum b = 0
  * up to rounding; the coarsest solve drops the constant mode).

@@ -11,6 +11,7 @@ from .gdp import (  # noqa: F401
     gdp_destripe,
     gdp_destripe_host,
     gdp_diffuse_z,
+    gdp_npr_filter,
     gdp_residual,
     gdp_screened_poisson_slices,
     gdp_vcycle,

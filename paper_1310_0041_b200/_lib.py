@@ -21,7 +21,7 @@ EXPORTS = [
     "gdp_opts_default", "gdp_ctx_create", "gdp_ctx_create_loopback", "gdp_ctx_destroy",
     "gdp_diffuse_z", "gdp_screened_poisson_slices", "gdp_destripe", "gdp_destripe_host",
     "gdp_vcycle", "gdp_residual", "gdp_last_error", "gdp_version", "gdp_kernel_launch_count",
-    "gdp_profile_begin", "gdp_profile_end", "gdp_get_unique_id",
+    "gdp_profile_begin", "gdp_profile_end", "gdp_get_unique_id", "gdp_npr_filter",
 ]
 
 
@@ -84,6 +84,7 @@ def lib():
         "gdp_destripe_host": ([vp, vp, i32, vp, vp, Dims, i64, i64, Weights, f32, C.c_size_t, P(Opts),
                                P(Report), P(Report)], i32),
         "gdp_vcycle": ([vp, vp, vp, Dims, i64, i64, Weights, f32, P(Opts), P(C.c_double), vp], i32),
+        "gdp_npr_filter": ([vp, vp, i32, vp, Dims, Weights, f32, f32, f32, P(Opts), P(Report), vp], i32),
         "gdp_residual": ([vp, vp, vp, vp, Dims, i64, i64, Weights, f32, P(C.c_double), P(C.c_double), vp],
                          i32),
         "gdp_last_error": ([], C.c_char_p),

@@ -337,6 +337,52 @@ __global__ void __launch_bounds__(256) k_init(LevelK L, RhsK R, float* __restric
   if (threadIdx.x == 0) partials[((long long)iz * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = make_double2(sr, sb);
 }
 
+// NEXT-1: rhs of the §6 NPR filter: b = alpha I0 - div(W V) with the link
+// field V = lam (1 - exp(-|grad I0|^2 / 2 sigma^2)) grad I0, |grad I0|^2 the 3D forward-difference
+// gradient at the link's base voxel (reading n-1).  One-off pass per solve, evaluated in fp64 and
+// rounded once; also writes x0 = I0.  (D^T W V)(c) = sum_d beta_d (V_d(c - e_d) - V_d(c)).
+template <typename TI>
+__global__ void __launch_bounds__(256) k_npr_rhs(LevelK L, const void* I, float* __restrict__ x0,
+                                                 float* __restrict__ b, double bx, double by, double bz,
+                                                 double lam, double inv2s2) {
+  const int ix = blockIdx.x * blockDim.x + threadIdx.x;
+  const int iy = blockIdx.y, iz = blockIdx.z;
+  if (ix >= L.nx) return;
+  const long long nx = L.nx, plane = (long long)L.nx * L.ny;
+  auto at = [&](int x, int y, int z) -> double { return (double)ldI<TI>(I, z * plane + (long long)y * nx + x); };
+  // V_d of the link (v, v + e_d); the caller guarantees v + e_d is inside the grid
+  auto vlink = [&](int x, int y, int z, int d) -> double {
+    const double c = at(x, y, z);
+    double m2 = 0.0, gd = 0.0;
+    if (x + 1 < L.nx) { const double g = at(x + 1, y, z) - c; m2 += g * g; if (d == 0) gd = g; }
+    if (y + 1 < L.ny) { const double g = at(x, y + 1, z) - c; m2 += g * g; if (d == 1) gd = g; }
+    if (z + 1 < L.nzl) { const double g = at(x, y, z + 1) - c; m2 += g * g; if (d == 2) gd = g; }
+    return lam * (1.0 - exp(-m2 * inv2s2)) * gd;
+  };
+  const double Ic = at(ix, iy, iz);
+  double s = (double)L.alpha * Ic;
+  const double beta[3] = {bx, by, bz};
+  const int pos[3] = {ix, iy, iz}, n[3] = {L.nx, L.ny, L.nzl};
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    if (beta[d] == 0.0 || n[d] < 2) continue;
+    if (pos[d] > 0) s += beta[d] * vlink(ix - (d == 0), iy - (d == 1), iz - (d == 2), d);
+    if (pos[d] + 1 < n[d]) s -= beta[d] * vlink(ix, iy, iz, d);
+  }
+  const long long c = (long long)iz * plane + (long long)iy * nx + ix;
+  x0[c] = (float)Ic;
+  b[c] = (float)s;
+}
+
+void launch_npr_rhs(const LevelK& L, const void* I, int tI, float* x0, float* b, float bx, float by, float bz,
+                    float lam, float sigma, cudaStream_t s) {
+  ProfScope ps(KC_UTIL, (double)L.nx * L.ny * L.nzl * ((tI ? 4.0 : 1.0) + 8.0), s);
+  dim3 g((L.nx + 255) / 256, L.ny, L.nzl);
+  const double inv2s2 = 1.0 / (2.0 * (double)sigma * (double)sigma);
+  if (tI == 0) k_npr_rhs<uint8_t><<<g, 256, 0, s>>>(L, I, x0, b, bx, by, bz, lam, inv2s2);
+  else k_npr_rhs<float><<<g, 256, 0, s>>>(L, I, x0, b, bx, by, bz, lam, inv2s2);
+}
+
 template <typename TI>
 __global__ void k_decode_copy(const void* I, float* __restrict__ x, long long n) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;

@@ -95,6 +95,8 @@ void launch_plane_sums(const void* a, int ta, const void* b, int tb, int nx, int
 void launch_finalize(const double2* partials, int per, int nplanes, double2* out, cudaStream_t s);
 void launch_rhs(const LevelK& L, const RhsK& R, int tI, float* b, cudaStream_t s);
 void launch_decode_copy(const void* I, int tI, float* x, long long n, cudaStream_t s);
+void launch_npr_rhs(const LevelK& L, const void* I, int tI, float* x0, float* b, float bx, float by, float bz,
+                    float lam, float sigma, cudaStream_t s);
 // x0 = decode(I), b = finest rhs, and the initial-residual norm partials (init_blocks_per_plane per plane)
 int init_blocks_per_plane(int nx, int ny);
 void launch_init(const LevelK& L, const RhsK& R, int tI, float* x0, float* b, double2* partials, cudaStream_t s);

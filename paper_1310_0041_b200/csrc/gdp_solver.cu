@@ -883,6 +883,45 @@ int gdp_screened_poisson_slices(gdp_ctx* ctx, const void* I0, gdp_dtype dtype, c
   return st;
 }
 
+int gdp_npr_filter(gdp_ctx* ctx, const void* I0, gdp_dtype dtype, float* out, gdp_dims dims, gdp_weights W,
+                   float alpha, float lambda, float sigma, const gdp_opts* opts, gdp_report* report, void* stream) {
+  RET(check_common(ctx, dims, 0, dims.nz));
+  RET(check_params(W, alpha));
+  if (!I0 || !out) return set_err(GDP_EINVAL, "null I0/out");
+  if ((const void*)out == I0) return set_err(GDP_EINVAL, "out may not alias I0");
+  if (dtype != GDP_U8 && dtype != GDP_F32) return set_err(GDP_EINVAL, "bad dtype");
+  if (!(alpha > 0.f)) return set_err(GDP_EINVAL, "the NPR filter is a screened solve: alpha > 0");
+  if (!(sigma > 0.f) || !std::isfinite(sigma) || !std::isfinite(lambda) || lambda < 0.f)
+    return set_err(GDP_EINVAL, "sigma must be finite > 0 and lambda finite >= 0");
+  Ctx& C = ctx->impl;
+  if (C.world > 1 || C.loop > 1) return set_err(GDP_EINVAL, "gdp_npr_filter is single-rank in this build");
+  const gdp_opts o = resolve_opts(opts);
+  cudaStream_t s = (cudaStream_t)stream;
+  const long long before = g_launches.load();
+  Hier* H;
+  RET(C.get_hier(make_key(dims, 0, dims.nz, W, alpha, o), &H));
+  const long long n = dims.nx * dims.ny * dims.nz;
+  CK(cudaEventRecord(C.ev0, s));
+  if (!H->b0) CK(cudaMalloc(&H->b0, sizeof(float) * (size_t)n));
+  const int tI = dtype == GDP_U8 ? 0 : 1;
+  launch_npr_rhs(H->lv[0].K, I0, tI, out, H->b0, W.bx, W.by, W.bz, lambda, sigma, s);  // x0 = I0 and b
+  Fine f;
+  f.x = out;
+  f.mode = RHS_B;
+  f.tI = 1;
+  f.R = RhsK{H->b0, nullptr, nullptr, 0.f, 0};
+  const int st = solve(C, *H, f, o, false, report, s);
+  if (st != GDP_OK && st != GDP_ENOCONV) return st;
+  CK(cudaEventRecord(C.ev1, s));
+  if (report) {
+    fill_time(ctx, report, s);
+    report->kernel_launches = g_launches.load() - before;
+    report->hbm_bytes_est = hbm_model(*H, 4.0, 0.0, report->vcycles);
+  }
+  if (st == GDP_ENOCONV) set_err(GDP_ENOCONV, "npr_filter: not converged");
+  return st;
+}
+
 int gdp_destripe(gdp_ctx* ctx, const void* I0, gdp_dtype dtype, float* I1, float* I2,
                  gdp_dims local, int64_t z0_global, int64_t nz_global, gdp_weights W,
                  float alpha, const gdp_opts* opts, gdp_report* rep1, gdp_report* rep2,

@@ -183,6 +183,22 @@ def gdp_destripe_host(ctx: Ctx, I0: torch.Tensor, I2: torch.Tensor, I1: torch.Te
     return r1.as_dict(), r2.as_dict()
 
 
+def gdp_npr_filter(ctx: Ctx, I0: torch.Tensor, out: torch.Tensor | None = None, W=(1.0, 1.0, 0.1),
+                   alpha: float = 0.001, lam: float = 1.25, sigma: float = 5.0 / 255.0, opts=None,
+                   stream=None, check: bool = True):
+    """NEXT-1: the §6 NPR filter.  Returns (out, report dict)."""
+    if out is None:
+        out = torch.empty(I0.shape, dtype=torch.float32, device=I0.device)
+    d = _dims(I0)
+    rep = L.Report()
+    o = opts if opts is not None else default_opts()
+    rc = L.lib().gdp_npr_filter(ctx.ptr, _dev(I0, "I0"), _dtype(I0), _dev(out, "out", (torch.float32,)), d,
+                                L.Weights(*W), alpha, lam, sigma, C.byref(o), C.byref(rep), _stream(stream))
+    if check:
+        _check(rc, "gdp_npr_filter", allow_noconv=True)
+    return out, rep.as_dict()
+
+
 def gdp_vcycle(ctx: Ctx, x: torch.Tensor, b: torch.Tensor, W=(1.0, 1.0, 0.1), alpha: float = 0.0,
                z0_global: int = 0, nz_global: int | None = None, opts=None, stream=None) -> float:
     """One V-cycle on (alpha - div W grad) x = b.  Returns rel-res after."""

@@ -325,3 +325,34 @@ def test_out_of_core_matches_in_core(gpu_ctx, shape, dtype, pin):
     assert np.abs(a2 - b2).max() <= 2e-5
     assert _rel_sp(I0, ref1, b2.astype(np.float64), 0.01) <= 2 * TOL_R
     assert rb["hbm_bytes_est"] > 0  # host-link bytes of the streamed finest level
+
+
+# ------------------------------------------------------------------ NEXT-1: the §6 NPR filter
+@pytest.mark.parametrize("shape,dtype,params", [((16, 135, 240), "u8", (0.001, 1.25, 5 / 255)),
+                                                ((9, 63, 65), "f32", (0.01, 1.0, 0.05)),
+                                                ((24, 100, 300), "u8", (0.001, 1.25, 5 / 255))])
+def test_npr_filter_parity(gpu_ctx, shape, dtype, params):
+    """General 3D screened solve with a modulated gradient field against the
+    oracle's CG; residual against the oracle's fp64 rhs."""
+    alpha, lam, sigma = params
+    nz, ny, nx = shape
+    I0 = synth.make_stack(nx, ny, nz, 71, dtype)
+    out, rep = gdp.gdp_npr_filter(gpu_ctx, dev(I0), alpha=alpha, lam=lam, sigma=sigma)
+    assert rep["status"] == "GDP_OK", rep
+    ref = O.npr_filter(I0, W=W_AD, alpha=alpha, lam=lam, sigma=sigma)
+    x = host(out)
+    assert np.abs(x - ref).max() <= TOL_X
+    b = O.rhs_npr(O.decode(I0), W_AD, alpha, lam, sigma)
+    assert O.rel_residual(x, b, W_AD, alpha) <= TOL_R
+
+
+def test_npr_filter_limits_and_errors(gpu_ctx):
+    I0 = synth.make_stack(40, 30, 5, 72, "f32")
+    x, _ = gdp.gdp_npr_filter(gpu_ctx, dev(I0), alpha=0.001, lam=1.0, sigma=1e-9)  # identity filter
+    assert np.abs(host(x) - I0.astype(np.float64)).max() <= 1e-5
+    c = np.full((4, 20, 24), 0.4, np.float32)
+    x, _ = gdp.gdp_npr_filter(gpu_ctx, dev(c))  # constant volume unchanged
+    assert np.abs(host(x) - 0.4).max() <= 1e-7
+    for kw in (dict(alpha=0.0), dict(sigma=0.0), dict(lam=-1.0)):
+        with pytest.raises(gdp.GdpError):
+            gdp.gdp_npr_filter(gpu_ctx, dev(I0), **kw)

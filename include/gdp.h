@@ -94,9 +94,13 @@ typedef struct {
                          Default 3.                                                          */
   int use_graphs;     /* reserved (0).                                                      */
   int nu_pre_slices;  /* phase 2 (gdp_screened_poisson_slices) pre-smoothing sweeps; < 0: nu_pre.
-                         Default 2.                                                          */
-  int nu_post_slices; /* phase 2 post-smoothing sweeps; < 0: nu_post.  Default 1 (V(2,1) reaches
-                         1e-6 in the same cycle count as V(2,2) on the configs, ~9% less time). */
+                         Default 1.                                                          */
+  int nu_post_slices; /* phase 2 post-smoothing sweeps; < 0: nu_post.  Default 2: V(1,2) reaches
+                         1e-6 in the same 4 cycles as V(2,2) on config 1 and is the fastest of
+                         (2,2) / (2,1) / (1,2) / (1,1) there (tools/omega_sweep.py).          */
+  float omega;        /* over-relaxation of the red-black sweeps, 0 < omega < 2 (1 = Gauss-Seidel;
+                         the converged answer does not depend on it).  Phases 1 / general.    */
+  float omega_slices; /* the same for phase 2.                                              */
 } gdp_opts;
 
 typedef struct {

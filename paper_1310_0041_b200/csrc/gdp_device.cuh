@@ -36,6 +36,7 @@ struct LevelK {     // one multigrid level as the kernels see it
   long long z0;     // global z of local plane 0
   AxisC ax, ay, az;
   float alpha;      // screening weight (same on every level)
+  float omega;      // over-relaxation of the red-black sweeps (1 = Gauss-Seidel)
 };
 
 enum RhsMode { RHS_B = 0, RHS_G = 1 };
@@ -141,10 +142,14 @@ __device__ __forceinline__ float residual_at(const LevelK& L, const RhsK& R, con
   return __fsub_rn(bc, apply_from(k, L.alpha, xc, nb.w, nb.e, nb.s, nb.n, nb.d, nb.u));
 }
 
-// Gauss-Seidel point update in correction form: x_c <- x_c + r_c / D_c  (H1).
-// invD = correctly rounded 1/D (same in every schedule), x_c + r * invD as one FMA.
-__device__ __forceinline__ float gs_update(float xc, float r, float D) {
-  return __fmaf_rn(r, __frcp_rn(D), xc);
+// Relaxation weight omega / D of a point: omega times the correctly rounded 1/D (one rounding
+// more when omega != 1; exactly 1/D for Gauss-Seidel).  Every schedule uses this value.
+__device__ __forceinline__ float relax_inv(float omega, float D) { return __fmul_rn(omega, __frcp_rn(D)); }
+
+// (Over-relaxed) Gauss-Seidel point update in correction form: x_c <- x_c + omega r_c / D_c
+// (H1), x_c + r * relax_inv as one FMA.
+__device__ __forceinline__ float gs_update(float xc, float r, float D, float omega) {
+  return __fmaf_rn(r, relax_inv(omega, D), xc);
 }
 
 // Cell-centre coordinate (finest-grid units) of cell i on an axis of n cells of width H,

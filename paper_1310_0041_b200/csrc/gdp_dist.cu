@@ -310,6 +310,7 @@ int dist_diffuse_z(Ctx& c, const void* I0, int tI, float* I1, long long nx, long
   HierKey gk{};
   gk.nx = nx; gk.ny = ny; gk.nzl = nzg; gk.z0 = 0; gk.nzg = nzg;
   gk.bx = bx; gk.by = by; gk.bz = bz; gk.alpha = alpha; gk.coarse_max = o.coarse_max;
+  gk.omega = o.omega;
   HierKey ck = gk;
   ck.z0 = z0g;  // the plan depends on this rank's slab (NCCL) or on the loopback split
   ck.nzl = nzl;

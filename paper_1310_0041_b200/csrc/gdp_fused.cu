@@ -241,7 +241,7 @@ __device__ __forceinline__ void pass2d_body(const Pass2D& P, float4 (&sh_top)[2]
     auto invd = [&](int c, float yl, float yr) {
       Coef k;
       k.xl = cxl[c]; k.xr = cxr[c]; k.yl = yl; k.yr = yr; k.zl = 0.f; k.zr = 0.f;
-      return __frcp_rn(k.diag(alpha));  // == the 1/D of gs_update
+      return relax_inv(L.omega, k.diag(alpha));  // == the weight of gs_update
     };
     const int ny = L.ay.n;
     const int rows[4] = {1, 0, ny - 2, ny - 1};
@@ -579,7 +579,7 @@ __global__ void __launch_bounds__(256, 2) k_pass2d_edge(Pass2D P, TileRect T) {
       if (lx == 0 || lx == G_COLS - 1 || ly == 0 || ly == G_ROWS - 1 || !inside(gx, gy)) continue;
       const float xc = S.x[ly][lx];
       const float r = resid(lx, ly, gx, gy, nullptr);
-      S.x[ly][lx] = gs_update(xc, r, coefs(L, gx, gy, zg).diag(L.alpha));
+      S.x[ly][lx] = gs_update(xc, r, coefs(L, gx, gy, zg).diag(L.alpha), L.omega);
     }
     __syncthreads();
   }

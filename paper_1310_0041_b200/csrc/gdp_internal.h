@@ -39,9 +39,10 @@ struct HierKey {
   long long nx, ny, nzl, z0, nzg;
   float bx, by, bz, alpha;
   int coarse_max;
+  float omega = 1.f;  // over-relaxation of the sweeps
   bool operator<(const HierKey& o) const {
-    return std::tie(nx, ny, nzl, z0, nzg, bx, by, bz, alpha, coarse_max) <
-           std::tie(o.nx, o.ny, o.nzl, o.z0, o.nzg, o.bx, o.by, o.bz, o.alpha, o.coarse_max);
+    return std::tie(nx, ny, nzl, z0, nzg, bx, by, bz, alpha, coarse_max, omega) <
+           std::tie(o.nx, o.ny, o.nzl, o.z0, o.nzg, o.bx, o.by, o.bz, o.alpha, o.coarse_max, o.omega);
   }
 };
 

@@ -36,7 +36,7 @@ struct Interior {
 __device__ __forceinline__ Interior interior_consts(const LevelK& L) {
   Interior I;
   I.k.xl = L.ax.k; I.k.xr = L.ax.k; I.k.yl = L.ay.k; I.k.yr = L.ay.k; I.k.zl = L.az.k; I.k.zr = L.az.k;
-  I.invD = __frcp_rn(I.k.diag(L.alpha));
+  I.invD = relax_inv(L.omega, I.k.diag(L.alpha));
   I.zreg_all = L.az.k == 0.f && L.az.kr == 0.f && L.az.kl == 0.f;
   return I;
 }
@@ -69,7 +69,7 @@ __global__ void __launch_bounds__(256) k_rbgs(LevelK L, float* __restrict__ x, c
   const Coef k = coefs(L, ix, iy, zg);
   const Nbr nb = load_nbr(x, xlo, xhi, L, k, iz, c, xc);
   const float r = residual_at<MODE, TI>(L, R, k, xc, nb, c, L.nx, plane, nullptr);
-  x[c] = gs_update(xc, r, k.diag(L.alpha));
+  x[c] = gs_update(xc, r, k.diag(L.alpha), L.omega);
 }
 
 // a5+a6: residual at the fine level, restricted by volume-weighted child average.

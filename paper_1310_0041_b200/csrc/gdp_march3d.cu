@@ -176,7 +176,7 @@ __global__ void __launch_bounds__(MT, 1) k_march3d(const __grid_constant__ March
         k.yl = cl(L.ay, ry); k.yr = cr(L.ay, ry);
         k.zl = cl(L.az, zr); k.zr = cr(L.az, zr);
         const float D = k.diag(L.alpha);
-        v[h] = D > 0.f ? __frcp_rn(D) : 0.f;  // == the 1/D of gs_update
+        v[h] = D > 0.f ? relax_inv(L.omega, D) : 0.f;  // == the weight of gs_update
       }
       S.inv[zc][rc][pk][ln] = make_float2(v[0], v[1]);
     }

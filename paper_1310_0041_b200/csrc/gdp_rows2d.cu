@@ -54,13 +54,14 @@ constexpr int R2_SL = 8;  // staging slots (power of two > R2_D)
 struct Row4 { float2 A, B; };
 
 // cold paths kept out of line (they would otherwise be inlined into each of the 8 ring steps)
-__device__ __noinline__ float2 r2_invd(float xl0, float xr0, float xl1, float xr1, float yl, float yr, float alpha) {
+__device__ __noinline__ float2 r2_invd(float xl0, float xr0, float xl1, float xr1, float yl, float yr, float alpha,
+                                       float omega) {
   Coef k;
   k.zl = 0.f; k.zr = 0.f; k.yl = yl; k.yr = yr;
   k.xl = xl0; k.xr = xr0;
-  const float a = __frcp_rn(k.diag(alpha));  // == the 1/D of gs_update
+  const float a = relax_inv(omega, k.diag(alpha));  // == the weight of gs_update
   k.xl = xl1; k.xr = xr1;
-  return make_float2(a, __frcp_rn(k.diag(alpha)));
+  return make_float2(a, relax_inv(omega, k.diag(alpha)));
 }
 __device__ __noinline__ float r2_rweight(XferAxis a, int i) { return rweight(a, i); }
 __device__ __noinline__ void r2_ptaps(XferAxis a, int i, int& dq, float& t) {
@@ -104,8 +105,8 @@ __device__ __forceinline__ void rows2d_march(const Rows2D& P, float4 (*sx)[R2_WA
   const bool lane_any = cin[0] || cin[1] || cin[2] || cin[3];
   constexpr bool vec = VEC;  // nx % 4 == 0: lane quads are 16-byte aligned
   const bool pin = lane >= RC::HX / 4 && lane < 32 - RC::HX / 4;  // interior columns
-  const float2 ivA = r2_invd(cxl[0], cxr[0], cxl[2], cxr[2], L.ay.k, L.ay.k, alpha);  // regular rows
-  const float2 ivB = r2_invd(cxl[1], cxr[1], cxl[3], cxr[3], L.ay.k, L.ay.k, alpha);
+  const float2 ivA = r2_invd(cxl[0], cxr[0], cxl[2], cxr[2], L.ay.k, L.ay.k, alpha, L.omega);  // regular rows
+  const float2 ivB = r2_invd(cxl[1], cxr[1], cxl[3], cxr[3], L.ay.k, L.ay.k, alpha, L.omega);
   // restriction weights of my columns
   float w0 = 0.f, w1 = 0.f, w2 = 0.f, w3 = 0.f;
   if (DOWN) {
@@ -260,8 +261,8 @@ __device__ __forceinline__ void rows2d_march(const Rows2D& P, float4 (*sx)[R2_WA
         const float yl = cl(L.ay, q), yr = cr(L.ay, q);
         float2 iD = PK == 0 ? ivA : ivB;
         if (q == 0 || q >= ny - 2)
-          iD = PK == 0 ? r2_invd(cxl[0], cxr[0], cxl[2], cxr[2], yl, yr, alpha)
-                       : r2_invd(cxl[1], cxr[1], cxl[3], cxr[3], yl, yr, alpha);
+          iD = PK == 0 ? r2_invd(cxl[0], cxr[0], cxl[2], cxr[2], yl, yr, alpha, L.omega)
+                       : r2_invd(cxl[1], cxr[1], cxl[3], cxr[3], yl, yr, alpha, L.omega);
         const float2 sten = stencil(IC<PK>{}, X[KO], X[KS], X[KN], f2(yl), f2(yr));
         if (PK == 0) X[KO].A = __ffma2_rn(sub2(Bv[KO].A, sten), iD, X[KO].A);
         else X[KO].B = __ffma2_rn(sub2(Bv[KO].B, sten), iD, X[KO].B);

@@ -336,6 +336,7 @@ int build_hier_levels(const HierKey& key, const std::vector<Level>& chain, int f
     L.K.nx = L.nx; L.K.ny = L.ny; L.K.nzl = L.nzl; L.K.z0 = L.z0;
     L.K.ax = make_axisc(L.gx); L.K.ay = make_axisc(L.gy); L.K.az = make_axisc(L.gz);
     L.K.alpha = (float)key.alpha;
+    L.K.omega = key.omega;
     const size_t n = (size_t)L.nx * L.ny * L.nzl;
     if (l > 0 || own0) {
       CK(cudaMalloc(&L.x, n * sizeof(float)));
@@ -679,6 +680,8 @@ static gdp_opts resolve_opts(const gdp_opts* o) {
   if (r.nu_pre < 0) r.nu_pre = d.nu_pre;
   if (r.nu_post < 0) r.nu_post = d.nu_post;
   if (r.coarse_max <= 0) r.coarse_max = d.coarse_max;
+  if (!(r.omega > 0.f && r.omega < 2.f)) r.omega = d.omega;
+  if (!(r.omega_slices > 0.f && r.omega_slices < 2.f)) r.omega_slices = d.omega_slices;
   return r;
 }
 
@@ -688,6 +691,7 @@ static HierKey make_key(gdp_dims d, int64_t z0, int64_t nzg, gdp_weights W, floa
   k.nx = d.nx; k.ny = d.ny; k.nzl = d.nz; k.z0 = z0; k.nzg = nzg;
   k.bx = W.bx; k.by = W.by; k.bz = W.bz; k.alpha = alpha;
   k.coarse_max = o.coarse_max;
+  k.omega = o.omega;
   return k;
 }
 
@@ -703,8 +707,10 @@ int gdp_opts_default(gdp_opts* o) {
   o->stagnation = 2;
   o->fused = 3;
   o->use_graphs = 0;
-  o->nu_pre_slices = 2;
-  o->nu_post_slices = 1;
+  o->nu_pre_slices = 1;
+  o->nu_post_slices = 2;
+  o->omega = 1.f;
+  o->omega_slices = 1.f;
   return GDP_OK;
 }
 
@@ -843,6 +849,7 @@ int gdp_screened_poisson_slices(gdp_ctx* ctx, const void* I0, gdp_dtype dtype, c
   gdp_opts o = resolve_opts(opts);
   if (o.nu_pre_slices >= 0) o.nu_pre = o.nu_pre_slices;  // per-phase smoothing (gdp.h)
   if (o.nu_post_slices >= 0) o.nu_post = o.nu_post_slices;
+  o.omega = o.omega_slices;
   cudaStream_t s = (cudaStream_t)stream;
   Ctx& C = ctx->impl;
   const long long before = g_launches.load();

@@ -219,6 +219,7 @@ int stream_diffuse_z(Ctx& C, const void* I0h, int tI, float* xh, long long nx, l
   key.nx = nx; key.ny = ny; key.nzl = nz; key.z0 = 0; key.nzg = nz;
   key.bx = bx; key.by = by; key.bz = bz; key.alpha = 0.f;
   key.coarse_max = o.coarse_max;
+  key.omega = o.omega;
   std::vector<Level> chain;
   int ff;
   SR(level_chain(key, chain, ff));

@@ -15,10 +15,16 @@ classes = collections.defaultdict(list)
 for name, v in best.items():
     m = re.search(r"k_march3d<(\d+), (\d+), (\d+), (\d+)>", name)
     if m:
-        tail, prolong = int(m.group(1)), int(m.group(2))
-        classes["up3d@L0" if prolong and tail != 1 else "down3d@L0"].append(v)
+        tail, prolong, zc = int(m.group(1)), int(m.group(2)), int(m.group(3))
+        if zc:  # z-coarsened transfers only occur below the finest level
+            continue
+        classes["up3d@L0" if prolong else "down3d@L0"].append(v)
         continue
     m = re.search(r"k_pass2d<(\d+), (\d+)>", name)
+    if m:
+        classes["down2d@L0" if int(m.group(2)) else "up2d@L0"].append(v)
+        continue
+    m = re.search(r"k_rows2d<(\d+), (\d+)>", name)
     if m:
         classes["down2d@L0" if int(m.group(2)) else "up2d@L0"].append(v)
         continue

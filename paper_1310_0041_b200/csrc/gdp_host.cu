@@ -57,7 +57,9 @@ extern "C" int gdp_destripe_host(gdp_ctx* ctx, const void* I0_host, gdp_dtype dt
   HK(cudaSetDevice(C.device), "set device");
   const size_t n = (size_t)dims.nx * dims.ny * dims.nz;
   const size_t sI = dtype == GDP_U8 ? 1 : 4;
-  const size_t need = n * (sI + 8) + n * 4 / 2;  // I0, I1, I2 + hierarchy (< N/2 fp32 pairs)
+  // in core: I0, I1, I2, the finest rhs b0 and the ping-pong twin of x, and the coarse levels
+  // (x, x2, b: 12 B per coarse voxel, < 0.35 N for the x/y-first coarsening)
+  const size_t need = n * (sI + 16) + (size_t)(0.35 * 12.0 * (double)n);
   size_t freeb = 0, totb = 0;
   HK(cudaMemGetInfo(&freeb, &totb), "meminfo");
   const size_t have = freeb + C.hbuf_cap[0] + C.hbuf_cap[1] + C.hbuf_cap[2];

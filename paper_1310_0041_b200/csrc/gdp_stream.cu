@@ -234,7 +234,9 @@ int stream_diffuse_z(Ctx& C, const void* I0h, int tI, float* xh, long long nx, l
   // the budget is a target: below two-plane windows the streamer still runs (C = 2) and only
   // a failing allocation is an error
   const double left = (double)budget - coarse - 4.0 * 1024 * 1024;
-  int Cp = (int)std::min<double>((double)nz, std::max(2.0, std::floor(left / per_plane) - 6.0));
+  // windows beyond a few dozen planes buy nothing (the pipeline keeps two in flight) and would
+  // crowd out the coarse levels' lazily allocated buffers
+  int Cp = (int)std::min<double>(std::min<double>((double)nz, 64.0), std::max(2.0, std::floor(left / per_plane) - 6.0));
   Cp = std::max(2, Cp & ~1);
   Stream1 S;
   S.I0h = I0h; S.xh = xh; S.tI = tI; S.nx = nx; S.ny = ny; S.plane = pl; S.nz = (int)nz; S.C = Cp; S.sI = sI;
@@ -328,7 +330,7 @@ int stream_slices(Ctx& C, gdp_ctx* cctx, const void* I0h, gdp_dtype dtype, float
   // per slice on the device: I0, I1, I2 of two batches + the batch hierarchy (~4 fp32 arrays)
   const double per_slice = (double)pl * (2.0 * (sI + 8.0) + 16.0);
   long long B = (long long)std::floor(((double)budget - 4.0 * 1024 * 1024) / per_slice);
-  B = std::max(1LL, std::min(B, nz));
+  B = std::max(1LL, std::min(std::min(B, nz), 64LL));
   DevBuf i0[2], i1[2], i2[2];
   for (int b = 0; b < 2; ++b) {
     SR(i0[b].alloc(sI * pl * B));

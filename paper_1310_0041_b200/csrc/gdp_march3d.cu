@@ -59,8 +59,13 @@ struct March3D {
   double2* partials;     // TAIL_NORMS: one (sum r^2, sum b^2) per item
   int tiles_x, tiles_y;
   int zlo, zhi;          // planes whose final values this launch produces
-  int chunk;             // planes per item
-  int nitems;
+  // work split over the persistent CTAs: `full` waves of whole tiles (tile k*grid + cta, all
+  // planes), then the remaining tiles' (tile, plane) list in tile-major order cut into grid
+  // contiguous runs -- so the plane pipeline restarts only at tile boundaries
+  int full;
+  int zeven;             // runs start on even planes (z-coarsened restriction pairs)
+  int max_segs;          // partial slots per CTA (TAIL_NORMS)
+  int nitems;            // grid * max_segs
 };
 
 struct SmemM {
@@ -112,12 +117,35 @@ __global__ void __launch_bounds__(MT, 1) k_march3d(const __grid_constant__ March
 
   double sr = 0.0, sbb = 0.0;
 
-  for (int item = blockIdx.x; item < P.nitems; item += gridDim.x) {
-    const int tx_ = item % P.tiles_x;
-    const int rest = item / P.tiles_x;
-    const int ty_ = rest % P.tiles_y;
-    const int ck = rest / P.tiles_y;
-    const int p_lo = P.zlo + ck * P.chunk, p_hi = min(p_lo + P.chunk, P.zhi);
+  const int ntiles = P.tiles_x * P.tiles_y, nzr = P.zhi - P.zlo, G = gridDim.x;
+  const long long wr = (long long)(ntiles - P.full * G) * nzr;  // remaining tile-planes
+  auto cut = [&](long long w) {  // start of run w of the remainder (even plane if zeven)
+    long long q = wr * w / G;
+    if (P.zeven) q -= (q % nzr) & 1;
+    return q;
+  };
+  const long long r0 = cut(blockIdx.x), r1 = cut(blockIdx.x + 1);
+  int seg = 0;
+  long long rs = r0;
+  for (;;) {
+    int tile, p_lo, p_hi;
+    if (seg < P.full) {
+      tile = seg * G + blockIdx.x;
+      p_lo = P.zlo;
+      p_hi = P.zhi;
+    } else {
+      if (rs >= r1) break;
+      const long long tt = rs / nzr;
+      const int z = (int)(rs - tt * nzr);
+      tile = P.full * G + (int)tt;
+      p_lo = P.zlo + z;
+      p_hi = P.zlo + (int)min((long long)nzr, z + (r1 - rs));
+      rs += p_hi - p_lo;
+    }
+    const int item = blockIdx.x * P.max_segs + seg;
+    ++seg;
+    const int tx_ = tile % P.tiles_x;
+    const int ty_ = tile / P.tiles_x;
 
     // ---- column data of my lane (4 consecutive columns; packs A = (c0, c2), B = (c1, c3))
     const int gx0 = tx_ * MTXI - MHX + 4 * lane;
@@ -528,6 +556,8 @@ __global__ void __launch_bounds__(MT, 1) k_march3d(const __grid_constant__ March
       sr = sbb = 0.0;
     }
   }
+  if (TAIL == TAIL_NORMS && tid == 0 && P.partials)  // unused partial slots of this CTA
+    for (; seg < P.max_segs; ++seg) P.partials[blockIdx.x * P.max_segs + seg] = make_double2(0.0, 0.0);
 }
 
 // ---------------------------------------------------------------------------------
@@ -557,22 +587,15 @@ static void plan3d(const LevelK& L, bool zc, int zlo, int zhi, March3D& P) {
   P.tiles_y = (L.ny + MTYI - 1) / MTYI;
   const int tiles = P.tiles_x * P.tiles_y;
   const int nz = zhi - zlo, nsm = num_sms();
-  double best = 1e30;
-  int bch = nz;
-  for (int nch = 1; nch <= nz; ++nch) {
-    int chunk = (nz + nch - 1) / nch;
-    if (zc && (chunk & 1)) ++chunk;  // z-coarsened: coarse plane pairs never straddle items
-    const int real = (nz + chunk - 1) / chunk;
-    const long long items = (long long)tiles * real;
-    const long long waves = (items + nsm - 1) / nsm;
-    const double cost = (double)waves * (chunk + 6);
-    if (cost < best - 1e-9) { best = cost; bch = chunk; }
-    if (chunk <= 4) break;
-  }
-  P.chunk = bch;
+  const long long work = (long long)tiles * nz;
+  const int grid = (int)std::min<long long>(nsm, work);
   P.zlo = zlo;
   P.zhi = zhi;
-  P.nitems = tiles * ((nz + bch - 1) / bch);
+  P.zeven = zc ? 1 : 0;
+  P.full = tiles / grid;
+  const long long rem = (long long)(tiles - P.full * grid) * nz;
+  P.max_segs = P.full + (int)((rem + grid - 1) / grid / std::max(nz, 1)) + 3;
+  P.nitems = grid * P.max_segs;
 }
 
 int fused3d_items(const Level& L, const Level& C, int zlo, int zhi) {
@@ -589,7 +612,7 @@ static void launch_m3v(const March3D& P, cudaStream_t s) {
     cudaFuncSetAttribute(k_march3d<TAIL, PROLONG, ZC, VEC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEMM);
     attr = true;
   }
-  const int grid = std::min(P.nitems, num_sms());
+  const int grid = P.nitems / P.max_segs;
   k_march3d<TAIL, PROLONG, ZC, VEC><<<grid, MT, SMEMM, s>>>(P);
 }
 template <int TAIL, bool PROLONG, bool ZC>

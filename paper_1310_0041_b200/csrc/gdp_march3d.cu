@@ -23,8 +23,12 @@
 // Per-cell arithmetic is the reference one (apply_from order, gs_update with the correctly
 // rounded 1/D, rw3 / bilerp for the transfers), done on f32x2 packs (FFMA2), so the iterates
 // are bit-identical to the reference schedule (tests/test_gpu_parity.py).
+#include <cooperative_groups.h>
+
 #include "gdp_internal.h"
 #include "gdp_pack.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace gdp {
 
@@ -34,7 +38,13 @@ constexpr int MROWS = MW * MR;             // 32
 constexpr int MCOLS = 128;                 // 4 columns per lane
 constexpr int MHX = 4, MHY = 4;            // halo >= 3 (two half-sweeps + residual); x: lane quads, y: = MR
 constexpr int MTXI = MCOLS - 2 * MHX;      // 120
-constexpr int MTYI = MROWS - 2 * MHY;      // 24
+constexpr int MCL = 1;                     // CTAs per cluster, stacked in y: their facing rows are
+                                           // exchanged through distributed shared memory, so only
+                                           // the cluster's outer rows are halo.  MCL = 2 is
+                                           // bit-identical but measured slower on B200 (the
+                                           // per-step cluster barrier costs more than the
+                                           // 75% -> 87.5% row efficiency gains): 1
+constexpr int MTYI = MCL * MROWS - 2 * MHY;  // 56 interior rows per cluster tile
 constexpr int MT = MW * 32;                // 512 threads
 constexpr int MD = 2;                      // prefetch distance (planes)
 constexpr int MXS = 3;                     // x staging slots (>= MD + 1, divides 6)
@@ -106,7 +116,39 @@ __global__ void __launch_bounds__(MT, 1) k_march3d(const __grid_constant__ March
   const int nzg = L.az.n;                          // single slab: local plane == global z
   const float2 al2 = f2(L.alpha);
   const int cplane = P.ncx * P.ncy;
-  const int wdn = max(warp - 1, 0), wup = min(warp + 1, MW - 1);  // exchange partners (CTA edges: own rows, halo)
+  // exchange partners: the warp below / above, in this CTA or across the cluster boundary
+  // (the cluster's outer edges read their own rows: halo)
+  cg::cluster_group cluster = cg::this_cluster();
+  const int crank = MCL > 1 ? (int)cluster.block_rank() : 0;
+  SmemM* Sdn = &S;
+  SmemM* Sup = &S;
+  int wdn = warp - 1, wup = warp + 1;
+  if (warp == 0) {
+    if (crank > 0) { Sdn = cluster.map_shared_rank(&S, crank - 1); wdn = MW - 1; }
+    else wdn = 0;
+  }
+  if (warp == MW - 1) {
+    if (crank < MCL - 1) { Sup = cluster.map_shared_rank(&S, crank + 1); wup = 0; }
+    else wup = MW - 1;
+  }
+  // cluster: the step barrier is split: arrive once this step's exchange rows are published and
+  // read (before the residual tail), wait at the start of the next step
+  bool arrived = false;
+  auto step_sync = [&]() {
+    if constexpr (MCL > 1) {
+      if (!arrived) asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+      asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+      arrived = false;
+    } else {
+      __syncthreads();
+    }
+  };
+  auto step_arrive = [&]() {
+    if constexpr (MCL > 1) {
+      asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+      arrived = true;
+    }
+  };
   const float* invf = reinterpret_cast<const float*>(&S.inv[0][0][0][0]);
 
   Pk X[MRING];
@@ -117,20 +159,21 @@ __global__ void __launch_bounds__(MT, 1) k_march3d(const __grid_constant__ March
 
   double sr = 0.0, sbb = 0.0;
 
-  const int ntiles = P.tiles_x * P.tiles_y, nzr = P.zhi - P.zlo, G = gridDim.x;
+  const int ntiles = P.tiles_x * P.tiles_y, nzr = P.zhi - P.zlo, G = gridDim.x / MCL;
+  const int cid = blockIdx.x / MCL;  // the cluster: both CTAs walk the same work list
   const long long wr = (long long)(ntiles - P.full * G) * nzr;  // remaining tile-planes
   auto cut = [&](long long w) {  // start of run w of the remainder (even plane if zeven)
     long long q = wr * w / G;
     if (P.zeven) q -= (q % nzr) & 1;
     return q;
   };
-  const long long r0 = cut(blockIdx.x), r1 = cut(blockIdx.x + 1);
+  const long long r0 = cut(cid), r1 = cut(cid + 1);
   int seg = 0;
   long long rs = r0;
   for (;;) {
     int tile, p_lo, p_hi;
     if (seg < P.full) {
-      tile = seg * G + blockIdx.x;
+      tile = seg * G + cid;
       p_lo = P.zlo;
       p_hi = P.zhi;
     } else {
@@ -164,7 +207,8 @@ __global__ void __launch_bounds__(MT, 1) k_march3d(const __grid_constant__ March
     const bool pin = lane >= MHX / 4 && lane < 32 - MHX / 4;  // interior columns (whole lanes)
 
     // ---- row data of my rows
-    const int gyw = ty_ * MTYI - MHY + warp * MR;  // even
+    const int crow = crank * MROWS + warp * MR;   // my first row within the cluster tile
+    const int gyw = ty_ * MTYI - MHY + crow;       // even
     float2 ryl[MR], ryr[MR];
     int ivo[MR];   // offset of my (row class, lane) in the 1/D table
     int ro[MR];    // in-plane offset of my row quad (0 if outside)
@@ -178,7 +222,7 @@ __global__ void __launch_bounds__(MT, 1) k_march3d(const __grid_constant__ March
       ivo[j] = (row_class(gy, L.ay.n) * 2 * 32 + lane) * 2;
       ro[j] = rin[j] ? gy * nx + gx0 : 0;
     }
-    const bool wint = warp >= MHY / MR && warp < MW - MHY / MR;  // interior rows (whole warps)
+    const bool wint = crow >= MHY && crow < MCL * MROWS - MHY;  // interior rows (whole warps)
 
     // restriction weights of my children (hoisted; rw3 = (wz * wy) * wx per element)
     float2 rwxA, rwxB, rwy[MR];
@@ -190,6 +234,9 @@ __global__ void __launch_bounds__(MT, 1) k_march3d(const __grid_constant__ March
     }
 
     // ---- 1/D table of this tile's columns (the previous item may still read the old one)
+    if constexpr (MCL > 1) {  // complete a pending arrive of the previous item's last step
+      if (arrived) { asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory"); arrived = false; }
+    }
     __syncthreads();
     for (int i = tid; i < 4 * 6 * 2 * 32; i += MT) {
       const int ln = i & 31, pk = (i >> 5) & 1, rc = (i >> 6) % 6, zc = (i >> 6) / 6;
@@ -368,7 +415,7 @@ __global__ void __launch_bounds__(MT, 1) k_march3d(const __grid_constant__ March
     auto step = [&](auto KK, int t) {
       constexpr int K = decltype(KK)::value;
       constexpr int PAR = K & 1;  // parity of the step (and of z)
-      __syncthreads();
+      step_sync();
 
       // (1) load plane t into X[K], add the coarse correction, publish its boundary rows
       if (t < e) {
@@ -433,8 +480,8 @@ __global__ void __launch_bounds__(MT, 1) k_march3d(const __grid_constant__ March
         int zoff;
         zcoef(q, zl2, zr2, zoff);
         Pk& Xo = X[KO];
-        const float2 sv = S.ex[C][PAR ^ 1][wdn][1][lane];  // pack (C + z)&1 of the row below my row 0
-        const float2 nv = S.ex[C][PAR ^ 1][wup][0][lane];  // pack (C + 1 + z)&1 of the row above my row MR-1
+        const float2 sv = Sdn->ex[C][PAR ^ 1][wdn][1][lane];  // pack (C + z)&1 of the row below my row 0
+        const float2 nv = Sup->ex[C][PAR ^ 1][wup][0][lane];  // pack (C + 1 + z)&1 of the row above my row MR-1
         static_for<MR>([&](auto Jc) {
           constexpr int j = decltype(Jc)::value;
           constexpr int PK = (C + j + ZP) & 1;  // active pack of row j (gyw even, gx0 even)
@@ -457,6 +504,9 @@ __global__ void __launch_bounds__(MT, 1) k_march3d(const __grid_constant__ March
 
       // (3) tail on plane q = t-3: residual -> restriction / norms, store x
       const int q = t - 3;
+      const float4 tsv4 = Sdn->et[PAR ^ 1][wdn][1][lane];  // neighbour rows of the tail, read before
+      const float4 tnv4 = Sup->et[PAR ^ 1][wup][0][lane];  // the barrier arrive (their buffer is rewritten next step)
+      step_arrive();
       if (q >= p_lo && q < p_hi) {
         constexpr int KO = (K + 3) % MRING, KD = (K + 2) % MRING, KU = (K + 4) % MRING;
         constexpr int ZP = KO & 1;
@@ -465,8 +515,8 @@ __global__ void __launch_bounds__(MT, 1) k_march3d(const __grid_constant__ March
           float2 zl2, zr2;
           int zoff;
           zcoef(q, zl2, zr2, zoff);
-          const float4 sv4 = S.et[PAR ^ 1][wdn][1][lane];
-          const float4 nv4 = S.et[PAR ^ 1][wup][0][lane];
+          const float4 sv4 = tsv4;
+          const float4 nv4 = tnv4;
           float2 rA[MR], rB[MR], bA[MR], bB[MR];
           static_for<MR>([&](auto Jc) {
             constexpr int j = decltype(Jc)::value;
@@ -558,6 +608,10 @@ __global__ void __launch_bounds__(MT, 1) k_march3d(const __grid_constant__ March
   }
   if (TAIL == TAIL_NORMS && tid == 0 && P.partials)  // unused partial slots of this CTA
     for (; seg < P.max_segs; ++seg) P.partials[blockIdx.x * P.max_segs + seg] = make_double2(0.0, 0.0);
+  if constexpr (MCL > 1) {  // the partner may still read my exchange rows
+    if (arrived) asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+    cluster.sync();
+  }
 }
 
 // ---------------------------------------------------------------------------------
@@ -574,6 +628,33 @@ static int num_sms() {
   return g_nsm;
 }
 
+// co-resident clusters of MCL CTAs (1 CTA / SM each): at most SMs / MCL, fewer when a GPC has
+// an odd number of free SMs
+static int max_clusters() {
+  static int n = 0;
+  if (!n) {
+    cudaFuncSetAttribute(k_march3d<1, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEMM);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(MCL * 64);
+    cfg.blockDim = dim3(MT);
+    cfg.dynamicSmemBytes = SMEMM;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = MCL;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int c = 0;
+    if (cudaOccupancyMaxActiveClusters(&c, k_march3d<1, false, false, true>, &cfg) != cudaSuccess || c <= 0) {
+      cudaGetLastError();
+      c = num_sms() / MCL;
+    }
+    n = c;
+  }
+  return n;
+}
+
 bool fusable3d(const Level& L, const Level& C, const gdp_opts& o) {
   const bool zlinks = L.K.az.k != 0.f || L.K.az.kr != 0.f || L.K.az.kl != 0.f;
   return (o.fused & 2) && zlinks && C.tx.coarsened && C.ty.coarsened &&
@@ -588,14 +669,14 @@ static void plan3d(const LevelK& L, bool zc, int zlo, int zhi, March3D& P) {
   const int tiles = P.tiles_x * P.tiles_y;
   const int nz = zhi - zlo, nsm = num_sms();
   const long long work = (long long)tiles * nz;
-  const int grid = (int)std::min<long long>(nsm, work);
+  const int grid = (int)std::min<long long>(max_clusters(), work);  // clusters
   P.zlo = zlo;
   P.zhi = zhi;
   P.zeven = zc ? 1 : 0;
   P.full = tiles / grid;
   const long long rem = (long long)(tiles - P.full * grid) * nz;
   P.max_segs = P.full + (int)((rem + grid - 1) / grid / std::max(nz, 1)) + 3;
-  P.nitems = grid * P.max_segs;
+  P.nitems = grid * MCL * P.max_segs;
 }
 
 int fused3d_items(const Level& L, const Level& C, int zlo, int zhi) {
@@ -612,8 +693,20 @@ static void launch_m3v(const March3D& P, cudaStream_t s) {
     cudaFuncSetAttribute(k_march3d<TAIL, PROLONG, ZC, VEC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEMM);
     attr = true;
   }
-  const int grid = P.nitems / P.max_segs;
-  k_march3d<TAIL, PROLONG, ZC, VEC><<<grid, MT, SMEMM, s>>>(P);
+  const int grid = P.nitems / P.max_segs;  // CTAs (clusters x MCL)
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(MT);
+  cfg.dynamicSmemBytes = SMEMM;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = MCL;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k_march3d<TAIL, PROLONG, ZC, VEC>, P);
 }
 template <int TAIL, bool PROLONG, bool ZC>
 static void launch_m3(const March3D& P, cudaStream_t s) {

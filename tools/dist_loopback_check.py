@@ -1,3 +1,4 @@
+"""Loopback z-slab partition vs single rank (fused / reference schedules), one V-cycle, max |diff|."""
 import sys, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch

@@ -51,6 +51,8 @@ struct RhsK {
   const float* V;    // value target (vmode 2)
   float av;          // weight of the value term
   int vmode;         // 0: no value term, 1: V = I (decoded), 2: V = float array
+  float* vout;       // vmode 2, init pass only: V += vshift is applied and written back here
+  float vshift;      //   (phase 1's deferred mean pin, the k_add_scalar arithmetic)
 };
 
 // a1: u8 -> u8/255 rounded to fp32 exactly as IEEE division would (the value the oracle

@@ -298,6 +298,16 @@ __global__ void __launch_bounds__(256) k_init(LevelK L, RhsK R, float* __restric
 #pragma unroll
           for (int c = 0; c < 4; ++c) V[c] = in[c] ? __ldg(R.V + row + gx0 + c) : 0.f;
         }
+        if (R.vout) {  // deferred mean pin of phase 1: V += shift (== k_add_scalar), written back
+#pragma unroll
+          for (int c = 0; c < 4; ++c) V[c] = __fadd_rn(V[c], R.vshift);
+          if (VEC && full) *reinterpret_cast<float4*>(R.vout + row + gx0) = make_float4(V[0], V[1], V[2], V[3]);
+          else {
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+              if (in[c]) R.vout[row + gx0 + c] = V[c];
+          }
+        }
       }
       const float yl = cl(L.ay, gy), yr = cr(L.ay, gy);
       float xo[4], bo[4];

@@ -772,9 +772,21 @@ static void fill_time(gdp_ctx* ctx, gdp_report* rep, cudaStream_t s) {
   (void)s;
 }
 
+static int diffuse_z_impl(gdp_ctx* ctx, const void* I0, gdp_dtype dtype, float* I1, gdp_dims local,
+                          int64_t z0_global, int64_t nz_global, gdp_weights W, float alpha, const gdp_opts* opts,
+                          gdp_report* report, void* stream, float* defer_shift);
+
 int gdp_diffuse_z(gdp_ctx* ctx, const void* I0, gdp_dtype dtype, float* I1, gdp_dims local,
                   int64_t z0_global, int64_t nz_global, gdp_weights W, float alpha,
                   const gdp_opts* opts, gdp_report* report, void* stream) {
+  return diffuse_z_impl(ctx, I0, dtype, I1, local, z0_global, nz_global, W, alpha, opts, report, stream, nullptr);
+}
+
+// defer_shift != NULL (single rank, alpha = 0): the mean-pin shift is returned instead of applied;
+// the caller applies it in phase 2's init pass (gdp_destripe)
+static int diffuse_z_impl(gdp_ctx* ctx, const void* I0, gdp_dtype dtype, float* I1, gdp_dims local,
+                          int64_t z0_global, int64_t nz_global, gdp_weights W, float alpha, const gdp_opts* opts,
+                          gdp_report* report, void* stream, float* defer_shift) {
   RET(check_common(ctx, local, z0_global, nz_global));
   RET(check_params(W, alpha));
   if (!I0 || !I1) return set_err(GDP_EINVAL, "null I0/I1");
@@ -823,7 +835,8 @@ int gdp_diffuse_z(gdp_ctx* ctx, const void* I0, gdp_dtype dtype, float* I1, gdp_
     for (int z = 0; z < L.nzl; ++z) { sx += H->h_plane[z].x; si += H->h_plane[z].y; }
     RET(comm_allreduce_sum2(C, &sx, &si, s));
     const double Ntot = (double)local.nx * local.ny * nz_global;
-    launch_add_scalar(I1, n, (float)((si - sx) / Ntot), s);
+    if (defer_shift) *defer_shift = (float)((si - sx) / Ntot);
+    else launch_add_scalar(I1, n, (float)((si - sx) / Ntot), s);
   }
   CK(cudaEventRecord(C.ev1, s));
   CK(cudaGetLastError());
@@ -836,9 +849,18 @@ int gdp_diffuse_z(gdp_ctx* ctx, const void* I0, gdp_dtype dtype, float* I1, gdp_
   return st;
 }
 
+static int slices_impl(gdp_ctx* ctx, const void* I0, gdp_dtype dtype, const float* I1, float* I2, gdp_dims local,
+                       float alpha, const gdp_opts* opts, gdp_report* report, void* stream, const float* vshift);
+
 int gdp_screened_poisson_slices(gdp_ctx* ctx, const void* I0, gdp_dtype dtype, const float* I1,
                                 float* I2, gdp_dims local, float alpha, const gdp_opts* opts,
                                 gdp_report* report, void* stream) {
+  return slices_impl(ctx, I0, dtype, I1, I2, local, alpha, opts, report, stream, nullptr);
+}
+
+// vshift != NULL: I1 += *vshift first (phase 1's deferred mean pin), written back into I1
+static int slices_impl(gdp_ctx* ctx, const void* I0, gdp_dtype dtype, const float* I1, float* I2, gdp_dims local,
+                       float alpha, const gdp_opts* opts, gdp_report* report, void* stream, const float* vshift) {
   if (!ctx) return set_err(GDP_EINVAL, "null ctx");
   if (!I0 || !I1 || !I2) return set_err(GDP_EINVAL, "null I0/I1/I2");
   if (!(alpha > 0.f) || !std::isfinite(alpha)) return set_err(GDP_EINVAL, "slices need finite alpha > 0");
@@ -870,12 +892,15 @@ int gdp_screened_poisson_slices(gdp_ctx* ctx, const void* I0, gdp_dtype dtype, c
     // per pass instead of I0 + I1 (5 or 8 B/cell); same values as the on-the-fly form.
     // Written together with x0 = I0 and the initial residual norms.
     if (!H->b0) CK(cudaMalloc(&H->b0, sizeof(float) * (size_t)n));
-    launch_init(H->lv[0].K, f.R, tI, I2, H->b0, H->partials, s);
+    RhsK Ri = f.R;
+    if (vshift) { Ri.vout = const_cast<float*>(I1); Ri.vshift = *vshift; }
+    launch_init(H->lv[0].K, Ri, tI, I2, H->b0, H->partials, s);
     H->init_norm_per = init_blocks_per_plane(H->lv[0].nx, H->lv[0].ny);
     f.mode = RHS_B;
     f.tI = 1;
     f.R = RhsK{H->b0, nullptr, nullptr, 0.f, 0};
   } else {
+    if (vshift) launch_add_scalar(const_cast<float*>(I1), n, *vshift, s);
     launch_decode_copy(I0, tI, I2, n, s);  // x0 = I0
   }
   int st = solve(C, *H, f, o, true, report, s);
@@ -940,9 +965,13 @@ int gdp_destripe(gdp_ctx* ctx, const void* I0, gdp_dtype dtype, float* I1, float
     RET(ctx->impl.ensure_scratch(sizeof(float) * (size_t)(local.nx * local.ny * local.nz)));
     I1p = (float*)ctx->impl.scratch;
   }
-  int st1 = gdp_diffuse_z(ctx, I0, dtype, I1p, local, z0_global, nz_global, W, 0.f, opts, rep1, stream);
+  // single rank: phase 1's mean pin is applied in phase 2's init pass (one pass over I1 less)
+  const bool defer = ctx->impl.world == 1 && ctx->impl.loop == 1;
+  float shift = 0.f;
+  int st1 = diffuse_z_impl(ctx, I0, dtype, I1p, local, z0_global, nz_global, W, 0.f, opts, rep1, stream,
+                           defer ? &shift : nullptr);
   if (st1 != GDP_OK && st1 != GDP_ENOCONV) return st1;
-  int st2 = gdp_screened_poisson_slices(ctx, I0, dtype, I1p, I2, local, alpha, opts, rep2, stream);
+  int st2 = slices_impl(ctx, I0, dtype, I1p, I2, local, alpha, opts, rep2, stream, defer ? &shift : nullptr);
   if (st2 != GDP_OK) return st2;
   return st1;
 }

@@ -64,10 +64,12 @@ __device__ __noinline__ float2 r2_invd(float xl0, float xr0, float xl1, float xr
   return make_float2(a, relax_inv(omega, k.diag(alpha)));
 }
 __device__ __noinline__ float r2_rweight(XferAxis a, int i) { return rweight(a, i); }
-__device__ __noinline__ void r2_ptaps(XferAxis a, int i, int& dq, float& t) {
+struct R2Tap { int dq; float t; };
+__device__ __noinline__ R2Tap r2_ptaps(XferAxis a, int i) {
   long long I, J;
+  float t;
   ptaps(a, i, I, J, t);
-  dq = (int)(J - I);
+  return R2Tap{(int)(J - I), t};
 }
 
 template <int NU, bool DOWN, bool VEC>
@@ -227,7 +229,7 @@ __device__ __forceinline__ void rows2d_march(const Rows2D& P, float4 (*sx)[R2_WA
         int dq;
         float ty;
         if (ptaps_regular(P.ty, t)) { dq = (t & 1) ? 1 : -1; ty = 0.25f; }  // == ptaps_fast
-        else r2_ptaps(P.ty, t, dq, ty);
+        else { const R2Tap tp = r2_ptaps(P.ty, t); dq = tp.dq; ty = tp.t; }
         const float2 r0 = CR[1];
         const float2 n0 = dq < 0 ? CR[0] : (dq > 0 ? CR[2] : r0);
         const float2 r1 = make_float2(__shfl_up_sync(FULL, r0.y, 1), __shfl_down_sync(FULL, r0.x, 1));
@@ -301,14 +303,11 @@ __device__ __forceinline__ void rows2d_march(const Rows2D& P, float4 (*sx)[R2_WA
             racc = acc;
           }
         } else if (!DOWN && pin) {
-          const float rr[4] = {rA.x, rB.x, rA.y, rB.y};
-          const float bb[4] = {Bv[KO].A.x, Bv[KO].B.x, Bv[KO].A.y, Bv[KO].B.y};
-#pragma unroll
-          for (int c = 0; c < 4; ++c)
-            if (cin[c]) {
-              sr += (double)rr[c] * (double)rr[c];
-              sbb += (double)bb[c] * (double)bb[c];
-            }
+          const float2 bA = Bv[KO].A, bB = Bv[KO].B;
+          if (cin[0]) { sr = fma((double)rA.x, (double)rA.x, sr); sbb = fma((double)bA.x, (double)bA.x, sbb); }
+          if (cin[1]) { sr = fma((double)rB.x, (double)rB.x, sr); sbb = fma((double)bB.x, (double)bB.x, sbb); }
+          if (cin[2]) { sr = fma((double)rA.y, (double)rA.y, sr); sbb = fma((double)bA.y, (double)bA.y, sbb); }
+          if (cin[3]) { sr = fma((double)rB.y, (double)rB.y, sr); sbb = fma((double)bB.y, (double)bB.y, sbb); }
         }
       }
       if (pin && lane_any) {  // store row q

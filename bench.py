@@ -48,6 +48,7 @@ def parse():
     p.add_argument("--config", type=int, default=CONFIG)
     p.add_argument("--alpha", type=float, default=ALPHA)
     p.add_argument("--fused", type=int, default=3)
+    p.add_argument("--fmg", type=int, default=None, help="gdp_opts.fmg and fmg_slices (default: the library's)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     return p.parse_args()
@@ -229,6 +230,8 @@ def main():
     else:
         ctx = gdp.Ctx(local)
     opts = gdp.default_opts(fused=args.fused)
+    if args.fmg is not None:
+        opts.fmg = opts.fmg_slices = args.fmg
     stream = torch.cuda.Stream()
     nvox = nx * ny * nz
 
@@ -328,6 +331,7 @@ def main():
                            "W": list(W), "rel_tol": 1e-6, "nu_phase1": [opts.nu_pre, opts.nu_post],
                            "nu_phase2": [opts.nu_pre_slices, opts.nu_post_slices],
                            "schedule": "fused" if args.fused else "reference",
+                           "fmg": [opts.fmg, opts.fmg_slices],
                            "l2": "working set > L2 (I0 134 MB + three 537 MB fp32 volumes); no flush",
                            "parallelism": f"z-slabs x{world} (phase 1 NCCL halo, phase 2 slab-local)",
                            "global_dims": [nx, ny, nzg]},

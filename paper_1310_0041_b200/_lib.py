@@ -37,7 +37,8 @@ class Opts(C.Structure):
     _fields_ = [("rel_tol", C.c_double), ("max_vcycles", C.c_int), ("nu_pre", C.c_int),
                 ("nu_post", C.c_int), ("coarse_max", C.c_int), ("stagnation", C.c_int),
                 ("fused", C.c_int), ("use_graphs", C.c_int), ("nu_pre_slices", C.c_int),
-                ("nu_post_slices", C.c_int), ("omega", C.c_float), ("omega_slices", C.c_float)]
+                ("nu_post_slices", C.c_int), ("omega", C.c_float), ("omega_slices", C.c_float),
+                ("fmg", C.c_int), ("fmg_slices", C.c_int)]
 
 
 class Report(C.Structure):

@@ -59,6 +59,7 @@ struct Hier {
   size_t partials_cap = 0;         // entries of `partials` per plane
   int up_norm_per = 0;             // >0: the last fused up pass left per-plane partials (this many per plane)
   int up_norm_planes = 0;          // planes of those partials (1: one row for the whole slab)
+  bool init_restricted = false;    // launch_init also wrote R r0 into lv[1].b (FMG start)
   int init_norm_per = 0;           // >0: launch_init left the initial-residual partials (this many per plane)
   ~Hier();
 };
@@ -120,7 +121,9 @@ int level_chain(const HierKey& key, std::vector<Level>& lv, int& first_full);
 int build_hier_levels(const HierKey& key, const std::vector<Level>& chain, int from, int end, bool own0,
                       bool coarsest_here, std::unique_ptr<Hier>& out);
 // one V-cycle over levels [l0, end) (l0 = 1: the caller owns level 0, e.g. the out-of-core streamer)
-int run_vcycle(Ctx& ctx, Hier& H, const Fine& f, const gdp_opts& o, cudaStream_t s, int l0 = 0);
+constexpr unsigned RV_PROLONG = 1u;
+int run_vcycle(Ctx& ctx, Hier& H, const Fine& f, const gdp_opts& o, cudaStream_t s, int l0 = 0,
+               unsigned flags = 0);
 int finest_norms(Ctx& ctx, Hier& H, const Fine& f, float* rout, cudaStream_t s);
 int solve(Ctx& ctx, Hier& H, const Fine& f, const gdp_opts& o, bool per_slice, gdp_report* rep,
           cudaStream_t s);

@@ -150,6 +150,55 @@ __global__ void __launch_bounds__(256) k_prolong(LevelK L, float* __restrict__ x
   xf[f] = __fadd_rn(xf[f], e);
 }
 
+// The same prolongation for plane-local (x/y only) coarsening, 4 columns x PR rows per thread:
+// x taps computed once per thread, float4 read-modify-write of xf (same values as k_prolong).
+constexpr int PRO_ROWS = 8;
+template <bool VEC>
+__global__ void __launch_bounds__(256) k_prolong_xy(LevelK L, float* __restrict__ xf, XferAxis tx, XferAxis ty,
+                                                    int ncx, int ncy, const float* __restrict__ xc) {
+  const int gx0 = 4 * (blockIdx.x * blockDim.x + threadIdx.x);
+  const int fz = blockIdx.z;
+  if (gx0 >= L.nx) return;
+  long long Ix[4], Jx[4];
+  float txw[4];
+  bool in[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    in[c] = gx0 + c < L.nx;
+    const int fx = in[c] ? gx0 + c : gx0;
+    if (ptaps_regular(tx, fx)) ptaps_fast(tx, fx, Ix[c], Jx[c], txw[c]); else ptaps(tx, fx, Ix[c], Jx[c], txw[c]);
+  }
+  const float* pc = xc + (long long)fz * ncx * ncy;
+  float* pf = xf + (long long)fz * L.nx * L.ny;
+  const int y0 = blockIdx.y * PRO_ROWS, y1 = min(y0 + PRO_ROWS, L.ny);
+  for (int fy = y0; fy < y1; ++fy) {
+    long long Iy, Jy;
+    float tyw;
+    if (ptaps_regular(ty, fy)) ptaps_fast(ty, fy, Iy, Jy, tyw); else ptaps(ty, fy, Iy, Jy, tyw);
+    const float* rI = pc + Iy * ncx;
+    const float* rJ = pc + Jy * ncx;
+    float* row = pf + (long long)fy * L.nx + gx0;
+    float v[4];
+    if (VEC && in[3]) {
+      const float4 q = *reinterpret_cast<const float4*>(row);
+      v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+    } else {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) v[c] = in[c] ? row[c] : 0.f;
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      v[c] = __fadd_rn(v[c], bilerp(__ldg(rI + Ix[c]), __ldg(rI + Jx[c]), __ldg(rJ + Ix[c]), __ldg(rJ + Jx[c]),
+                                    txw[c], tyw));
+    if (VEC && in[3]) *reinterpret_cast<float4*>(row) = make_float4(v[0], v[1], v[2], v[3]);
+    else {
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        if (in[c]) row[c] = v[c];
+    }
+  }
+}
+
 // a5: residual r = b - A x with per-block fp64 partial sums of r^2 and b^2 (one row of
 // partials per plane, reduced in a fixed order by k_finalize -> deterministic).
 template <int MODE, typename TI>
@@ -256,7 +305,7 @@ template <> struct Quad<uint8_t> {
 
 template <typename TI, bool VEC>
 __global__ void __launch_bounds__(256) k_init(LevelK L, RhsK R, float* __restrict__ x0, float* __restrict__ b,
-                                              double2* partials, int S) {
+                                              double2* partials, int S, InitXfer X) {
   const int gx0 = 4 * (blockIdx.x * blockDim.x + threadIdx.x);
   const int iz = blockIdx.z;
   const long long zg = L.z0 + iz;
@@ -280,6 +329,7 @@ __global__ void __launch_bounds__(256) k_init(LevelK L, RhsK R, float* __restric
       for (int c = 0; c < 4; ++c) v[c] = (ok && in[c]) ? ldI<TI>(R.I, base + gx0 + c) : 0.f;
     };
     float rm[4], rc[4], rp[4], dn[4], up[4];
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};  // X.bc: restriction of r0 (per coarse column)
     ldrow(pbase + (long long)(y0 - 1) * nx, y0 - 1 >= 0, rm);
     ldrow(pbase + (long long)y0 * nx, y0 < L.ny, rc);
     for (int gy = y0; gy < y1; ++gy) {
@@ -310,7 +360,7 @@ __global__ void __launch_bounds__(256) k_init(LevelK L, RhsK R, float* __restric
         }
       }
       const float yl = cl(L.ay, gy), yr = cr(L.ay, gy);
-      float xo[4], bo[4];
+      float xo[4], bo[4], ro[4];
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         Coef k;
@@ -326,6 +376,7 @@ __global__ void __launch_bounds__(256) k_init(LevelK L, RhsK R, float* __restric
         const float r = __fsub_rn(bc, apply_from(k, L.alpha, Ic, Iw, Ie, Is, In, d, u));  // == residual_at
         xo[c] = Ic;
         bo[c] = bc;
+        ro[c] = r;
         if (in[c]) {
           sr += (double)r * (double)r;
           sb += (double)bc * (double)bc;
@@ -338,6 +389,30 @@ __global__ void __launch_bounds__(256) k_init(LevelK L, RhsK R, float* __restric
 #pragma unroll
         for (int c = 0; c < 4; ++c)
           if (in[c]) { x0[row + gx0 + c] = xo[c]; b[row + gx0 + c] = bo[c]; }
+      }
+      if (X.bc) {  // == k_restrict's sum over the children (fy outer, fx inner), plane-local
+        const bool yc = X.ty.coarsened != 0;
+        const bool first = !yc || (gy & 1) == 0;
+        const float wy = rweight(X.ty, gy);
+        const long long cbase = (long long)iz * X.ncx * X.ncy + (long long)(yc ? gy >> 1 : gy) * X.ncx;
+        const bool last = !yc || (gy & 1) == 1 || gy + 1 == L.ny;
+        if (X.tx.coarsened) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            float a = first ? 0.f : acc[h];
+#pragma unroll
+            for (int c = 2 * h; c < 2 * h + 2; ++c)
+              if (in[c]) a = __fmaf_rn(rw3(1.f, wy, rweight(X.tx, gx0 + c)), ro[c], a);
+            acc[h] = a;
+            if (last && in[2 * h]) X.bc[cbase + (gx0 >> 1) + h] = a;
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            acc[c] = __fmaf_rn(rw3(1.f, wy, 1.f), ro[c], first ? 0.f : acc[c]);
+            if (last && in[c]) X.bc[cbase + gx0 + c] = acc[c];
+          }
+        }
       }
 #pragma unroll
       for (int c = 0; c < 4; ++c) { rm[c] = rc[c]; rc[c] = rp[c]; }
@@ -536,6 +611,12 @@ void launch_prolong(const LevelK& L, float* xf, const XferAxis& tx, const XferAx
                     const XferAxis& tz, int ncx, int ncy, int nczl, long long cz0, const float* xc,
                     const float* xclo, const float* xchi, cudaStream_t s) {
   ProfScope ps(KC_PROLONG, ncell(L) * 8.0 + 4.0 * ncx * ncy * (double)nczl, s, ncell(L));
+  if (!tz.coarsened && nczl == L.nzl && cz0 == L.z0) {  // plane-local: coarse plane z = fine plane z
+    dim3 g((L.nx + 1023) / 1024, (L.ny + PRO_ROWS - 1) / PRO_ROWS, L.nzl);
+    if ((L.nx & 3) == 0 && ((uintptr_t)xf & 15) == 0) k_prolong_xy<true><<<g, 256, 0, s>>>(L, xf, tx, ty, ncx, ncy, xc);
+    else k_prolong_xy<false><<<g, 256, 0, s>>>(L, xf, tx, ty, ncx, ncy, xc);
+    return;
+  }
   dim3 blk(32, 8);
   dim3 grd((L.nx + 31) / 32, (L.ny + 7) / 8, L.nzl);
   k_prolong<<<grd, blk, 0, s>>>(L, xf, tx, ty, tz, ncx, ncy, nczl, cz0, xc, xclo, xchi);
@@ -604,18 +685,19 @@ void launch_rhs(const LevelK& L, const RhsK& R, int tI, float* b, cudaStream_t s
 constexpr int INIT_ROWS = 32;
 int init_blocks_per_plane(int nx, int ny) { return ((nx + 1023) / 1024) * ((ny + INIT_ROWS - 1) / INIT_ROWS); }
 
-void launch_init(const LevelK& L, const RhsK& R, int tI, float* x0, float* b, double2* partials, cudaStream_t s) {
+void launch_init(const LevelK& L, const RhsK& R, int tI, float* x0, float* b, double2* partials, cudaStream_t s,
+                 const InitXfer& X) {
   const double n = (double)L.nx * L.ny * L.nzl;
-  ProfScope ps(KC_UTIL, n * ((tI ? 4.0 : 1.0) + (R.vmode == 2 ? 4.0 : 0.0) + 8.0), s);
+  ProfScope ps(KC_UTIL, n * ((tI ? 4.0 : 1.0) + (R.vmode == 2 ? 4.0 : 0.0) + 8.0) + (X.bc ? 4.0 * X.ncx * X.ncy * L.nzl : 0.0), s);
   dim3 g((L.nx + 1023) / 1024, (L.ny + INIT_ROWS - 1) / INIT_ROWS, L.nzl);
   const bool vec = (L.nx & 3) == 0 && ((uintptr_t)R.I & 15) == 0 && ((uintptr_t)x0 & 15) == 0 &&
                    ((uintptr_t)b & 15) == 0 && (R.vmode != 2 || ((uintptr_t)R.V & 15) == 0);
   if (tI == 0) {
-    if (vec) k_init<uint8_t, true><<<g, 256, 0, s>>>(L, R, x0, b, partials, INIT_ROWS);
-    else k_init<uint8_t, false><<<g, 256, 0, s>>>(L, R, x0, b, partials, INIT_ROWS);
+    if (vec) k_init<uint8_t, true><<<g, 256, 0, s>>>(L, R, x0, b, partials, INIT_ROWS, X);
+    else k_init<uint8_t, false><<<g, 256, 0, s>>>(L, R, x0, b, partials, INIT_ROWS, X);
   } else {
-    if (vec) k_init<float, true><<<g, 256, 0, s>>>(L, R, x0, b, partials, INIT_ROWS);
-    else k_init<float, false><<<g, 256, 0, s>>>(L, R, x0, b, partials, INIT_ROWS);
+    if (vec) k_init<float, true><<<g, 256, 0, s>>>(L, R, x0, b, partials, INIT_ROWS, X);
+    else k_init<float, false><<<g, 256, 0, s>>>(L, R, x0, b, partials, INIT_ROWS, X);
   }
 }
 

@@ -99,7 +99,15 @@ void launch_npr_rhs(const LevelK& L, const void* I, int tI, float* x0, float* b,
                     float lam, float sigma, cudaStream_t s);
 // x0 = decode(I), b = finest rhs, and the initial-residual norm partials (init_blocks_per_plane per plane)
 int init_blocks_per_plane(int nx, int ny);
-void launch_init(const LevelK& L, const RhsK& R, int tI, float* x0, float* b, double2* partials, cudaStream_t s);
+// X.bc (optional): also restrict the initial residual r0 into the next level's rhs (plane-local
+// x/y coarsening only), the values k_restrict would write (FMG start)
+struct InitXfer {
+  XferAxis tx, ty;
+  int ncx = 0, ncy = 0;
+  float* bc = nullptr;
+};
+void launch_init(const LevelK& L, const RhsK& R, int tI, float* x0, float* b, double2* partials, cudaStream_t s,
+                 const InitXfer& X = InitXfer{});
 void launch_add_scalar(float* x, long long n, float v, cudaStream_t s);
 void launch_axpy(float* x, const float* e, long long n, cudaStream_t s);
 size_t coarse_smem_bytes(const CoarseK& C);

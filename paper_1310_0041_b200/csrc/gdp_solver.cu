@@ -467,7 +467,9 @@ static int smooth(const Level& L, float* x, const RhsK& R, int mode, int tI, int
   return GDP_OK;
 }
 
-int run_vcycle(Ctx& ctx, Hier& H, const Fine& f, const gdp_opts& o, cudaStream_t s, int l0) {
+// flags: RV_PROLONG — level l0 starts from the prolongation of level l0+1's x (added to the
+// caller's x at level 0, to zero above) instead of zero / the caller's iterate (FMG start)
+int run_vcycle(Ctx& ctx, Hier& H, const Fine& f, const gdp_opts& o, cudaStream_t s, int l0, unsigned flags) {
   const int nl = (int)H.lv.size();
   if (nl == 1) {  // level 0 is the coarsest: x += A^-1 (b - A x)
     Level& L = H.lv[0];
@@ -501,8 +503,17 @@ int run_vcycle(Ctx& ctx, Hier& H, const Fine& f, const gdp_opts& o, cudaStream_t
       mode = RHS_B;
       tI = 1;
     }
+    // FMG start at l0: x (zeroed above level 0) += P x_{l0+1}, in the first fused 3D sweep
+    // when there is one to carry it, else by the prolongation kernel
+    const bool pro = l == l0 && (flags & RV_PROLONG);
+    const bool pro_fused = pro && fz[l] == 3 && o.nu_pre >= 2;
+    if (pro) {
+      if (l > 0) CK(cudaMemsetAsync(x, 0, sizeof(float) * (size_t)L.nx * L.ny * L.nzl, s));
+      if (!pro_fused) launch_prolong(L.K, x, C.tx, C.ty, C.tz, C.nx, C.ny, C.nzl, C.z0, C.x, C.xlo, C.xhi, s);
+    }
+    const bool zx = l > 0 && !pro;  // level above l0 (or l0 > 0 without FMG): starts from zero
     if (fz[l] == 2) {  // one fused pass: x (A) -> x2 (B)
-      fused_down2d(L, C, x, L.x2, R, mode, tI, o.nu_pre, l > 0, s);
+      fused_down2d(L, C, x, L.x2, R, mode, tI, o.nu_pre, zx, s);
       cur[l] = L.x2;
       continue;
     }
@@ -510,13 +521,13 @@ int run_vcycle(Ctx& ctx, Hier& H, const Fine& f, const gdp_opts& o, cudaStream_t
       float* c = x;
       for (int k = 0; k < o.nu_pre; ++k) {
         float* d = c == x ? L.x2 : x;
-        fused_sweep3d(L, C, c, d, R.b, l > 0 && k == 0, false, k == o.nu_pre - 1 ? 1 : 0, nullptr, s);
+        fused_sweep3d(L, C, c, d, R.b, zx && k == 0, pro_fused && k == 0, k == o.nu_pre - 1 ? 1 : 0, nullptr, s);
         c = d;
       }
       cur[l] = c;
       continue;
     }
-    if (l > 0) CK(cudaMemsetAsync(x, 0, sizeof(float) * (size_t)L.nx * L.ny * L.nzl, s));
+    if (zx) CK(cudaMemsetAsync(x, 0, sizeof(float) * (size_t)L.nx * L.ny * L.nzl, s));
     smooth(L, x, R, mode, tI, o.nu_pre, s);
     launch_restrict(L.K, x, L.xlo, L.xhi, R, mode, tI, C.tx, C.ty, C.tz, C.nx, C.ny, C.nzl, C.b, s);
     cur[l] = x;
@@ -587,11 +598,59 @@ static double rel_from_planes(const Hier& H, bool per_slice, double* worst_b) {
   return worst;
 }
 
+// FMG start: the init pass restricts r0 into level 1 on the way when the coarsening is plane-local
+static InitXfer init_xfer(Hier& H, const gdp_opts& o) {
+  InitXfer X;
+  H.init_restricted = false;
+  if ((o.fmg & 3) == 0 || (o.fmg & 4) || H.lv.size() < 3 || H.lv[1].tz.coarsened) return X;
+  const Level& C = H.lv[1];
+  X.tx = C.tx; X.ty = C.ty; X.ncx = C.nx; X.ncy = C.ny; X.bc = C.b;
+  H.init_restricted = true;
+  return X;
+}
+
+// FMG start (nested iteration) for the correction equation A e = r0 of the first cycle:
+// r0 = b - A x0 restricted to level 1, the right-hand side restricted on down to the coarsest,
+// solved there, then per level l = nl-2 .. 1 a prolongation of e_{l+1} and one V-cycle on
+// levels l.. (run_vcycle l0 = l).  Leaves e_1 in lv[1].x; the caller's first fine cycle
+// prolongates it into x (RV_PROLONG).
+static int fmg_start(Ctx& ctx, Hier& H, const Fine& f, const gdp_opts& o, bool r0_restricted, cudaStream_t s) {
+  const int nl = (int)H.lv.size();
+  Level& L0 = H.lv[0];
+  Level& L1 = H.lv[1];
+  if (!r0_restricted)
+    launch_restrict(L0.K, f.x, L0.xlo, L0.xhi, f.R, f.mode, f.tI, L1.tx, L1.ty, L1.tz, L1.nx, L1.ny, L1.nzl, L1.b, s);
+  for (int l = 1; l < nl - 1; ++l) {  // b_{l+1} = R b_l: the residual of x_l = 0
+    Level& L = H.lv[l];
+    Level& C = H.lv[l + 1];
+    CK(cudaMemsetAsync(L.x, 0, sizeof(float) * (size_t)L.nx * L.ny * L.nzl, s));
+    const RhsK R{L.b, nullptr, nullptr, 0.f, 0};
+    launch_restrict(L.K, L.x, L.xlo, L.xhi, R, RHS_B, 1, C.tx, C.ty, C.tz, C.nx, C.ny, C.nzl, C.b, s);
+  }
+  Level& Lc = H.lv[nl - 1];
+  CK(launch_coarse(H.coarse, Lc.b, Lc.x, s));
+  // fmg 1: one V-cycle per level 1..nl-2; fmg 2 / 3: V-cycles from level 2 only, level 1 gets
+  // the prolongation of e_2 followed by nu_post red-black sweeps (2) or nothing (3)
+  const int mode = o.fmg & 3;
+  const int lmin = mode == 1 ? 1 : 2;
+  for (int l = nl - 2; l >= lmin; --l) RET(run_vcycle(ctx, H, f, o, s, l, RV_PROLONG));
+  for (int l = lmin - 1; l >= 1; --l) {
+    Level& L = H.lv[l];
+    Level& C = H.lv[l + 1];
+    CK(cudaMemsetAsync(L.x, 0, sizeof(float) * (size_t)L.nx * L.ny * L.nzl, s));
+    launch_prolong(L.K, L.x, C.tx, C.ty, C.tz, C.nx, C.ny, C.nzl, C.z0, C.x, C.xlo, C.xhi, s);
+    if (mode == 2) smooth(L, L.x, RhsK{L.b, nullptr, nullptr, 0.f, 0}, RHS_B, 1, o.nu_post, s);
+  }
+  return GDP_OK;
+}
+
 // full solve: cycles until rel_tol / cap / stagnation (a9)
 int solve(Ctx& ctx, Hier& H, const Fine& f, const gdp_opts& o, bool per_slice, gdp_report* rep,
           cudaStream_t s) {
   gdp_report r{};
   r.levels = (int)H.lv.size();
+  const bool r0_restricted = H.init_restricted;  // only the init pass just before this solve
+  H.init_restricted = false;
   g_prof_finest = (double)H.lv[0].nx * H.lv[0].ny * H.lv[0].nzl;
   if (H.init_norm_per > 0) {  // the initial residual came with launch_init
     launch_finalize(H.partials, H.init_norm_per, H.lv[0].nzl, H.plane_sums, s);
@@ -611,7 +670,9 @@ int solve(Ctx& ctx, Hier& H, const Fine& f, const gdp_opts& o, bool per_slice, g
   const int cap = std::min(o.max_vcycles, GDP_MAX_CYCLES);
   while (rel > o.rel_tol) {
     if (k >= cap) { status = GDP_ENOCONV; break; }
-    RET(run_vcycle(ctx, H, f, o, s));
+    const bool fmg = k == 0 && (o.fmg & 3) != 0 && H.lv.size() >= 3;
+    if (fmg) RET(fmg_start(ctx, H, f, o, r0_restricted, s));
+    RET(run_vcycle(ctx, H, f, o, s, 0, fmg ? RV_PROLONG : 0u));
     if (H.up_norm_per > 0) {  // norms of the final iterate came with the fused up pass
       launch_finalize(H.partials, H.up_norm_per, H.up_norm_planes, H.plane_sums, s);
       CK(cudaMemcpyAsync(H.h_plane, H.plane_sums, sizeof(double2) * H.up_norm_planes, cudaMemcpyDeviceToHost, s));
@@ -711,6 +772,8 @@ int gdp_opts_default(gdp_opts* o) {
   o->nu_post_slices = 2;
   o->omega = 1.f;
   o->omega_slices = 1.f;
+  o->fmg = 1;
+  o->fmg_slices = 3;
   return GDP_OK;
 }
 
@@ -816,7 +879,7 @@ static int diffuse_z_impl(gdp_ctx* ctx, const void* I0, gdp_dtype dtype, float* 
   // once (same values) together with x0 = I0 and the initial residual norms
   if (H->lv.size() > 1) {  // every schedule reads the written rhs (same values as on the fly)
     if (!H->b0) CK(cudaMalloc(&H->b0, sizeof(float) * (size_t)n));
-    launch_init(H->lv[0].K, f.R, tI, I1, H->b0, H->partials, s);
+    launch_init(H->lv[0].K, f.R, tI, I1, H->b0, H->partials, s, init_xfer(*H, o));
     H->init_norm_per = init_blocks_per_plane(H->lv[0].nx, H->lv[0].ny);
     f.mode = RHS_B;
     f.tI = 1;
@@ -872,6 +935,7 @@ static int slices_impl(gdp_ctx* ctx, const void* I0, gdp_dtype dtype, const floa
   if (o.nu_pre_slices >= 0) o.nu_pre = o.nu_pre_slices;  // per-phase smoothing (gdp.h)
   if (o.nu_post_slices >= 0) o.nu_post = o.nu_post_slices;
   o.omega = o.omega_slices;
+  o.fmg = o.fmg_slices;
   cudaStream_t s = (cudaStream_t)stream;
   Ctx& C = ctx->impl;
   const long long before = g_launches.load();
@@ -894,7 +958,7 @@ static int slices_impl(gdp_ctx* ctx, const void* I0, gdp_dtype dtype, const floa
     if (!H->b0) CK(cudaMalloc(&H->b0, sizeof(float) * (size_t)n));
     RhsK Ri = f.R;
     if (vshift) { Ri.vout = const_cast<float*>(I1); Ri.vshift = *vshift; }
-    launch_init(H->lv[0].K, Ri, tI, I2, H->b0, H->partials, s);
+    launch_init(H->lv[0].K, Ri, tI, I2, H->b0, H->partials, s, init_xfer(*H, o));
     H->init_norm_per = init_blocks_per_plane(H->lv[0].nx, H->lv[0].ny);
     f.mode = RHS_B;
     f.tI = 1;

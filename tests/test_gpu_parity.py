@@ -252,7 +252,7 @@ def test_loopback_partition_bit_identical(gpu_ctx, shape, world):
     the single-rank iterate bit for bit, and the same converged answer as the oracle."""
     nz, ny, nx = shape
     I0 = synth.make_stack(nx, ny, nz, 51, "u8")
-    o = gdp.default_opts(fused=0)
+    o = gdp.default_opts(fused=0, fmg=0)  # the z-slab team has no FMG start (gdp.h)
     ref, r1 = gdp.gdp_diffuse_z(gpu_ctx, dev(I0), opts=o)
     lb = gdp.Ctx(0, loopback=world)
     try:
@@ -273,10 +273,11 @@ def test_loopback_fused_partition_bit_identical(gpu_ctx, shape, world):
     planes per face; the iterate equals the single-rank fused solve bit for bit."""
     nz, ny, nx = shape
     I0 = synth.make_stack(nx, ny, nz, 53, "u8")
-    ref, r1 = gdp.gdp_diffuse_z(gpu_ctx, dev(I0))
+    o = gdp.default_opts(fmg=0)  # the z-slab team has no FMG start (gdp.h)
+    ref, r1 = gdp.gdp_diffuse_z(gpu_ctx, dev(I0), opts=o)
     lb = gdp.Ctx(0, loopback=world)
     try:
-        out, r2 = gdp.gdp_diffuse_z(lb, dev(I0))
+        out, r2 = gdp.gdp_diffuse_z(lb, dev(I0), opts=o)
     finally:
         lb.close()
     assert r1["vcycles"] == r2["vcycles"]
@@ -286,10 +287,11 @@ def test_loopback_fused_partition_bit_identical(gpu_ctx, shape, world):
 
 def test_loopback_destripe_and_slices(gpu_ctx):
     I0 = synth.make_stack(80, 72, 20, 52, "u8")
-    a = gdp.gdp_destripe(gpu_ctx, dev(I0), opts=gdp.default_opts(fused=0))
+    o = gdp.default_opts(fused=0, fmg=0, fmg_slices=0)
+    a = gdp.gdp_destripe(gpu_ctx, dev(I0), opts=o)
     lb = gdp.Ctx(0, loopback=4)
     try:
-        b = gdp.gdp_destripe(lb, dev(I0), opts=gdp.default_opts(fused=0))
+        b = gdp.gdp_destripe(lb, dev(I0), opts=o)
     finally:
         lb.close()
     assert np.array_equal(a[1].cpu().numpy(), b[1].cpu().numpy())
@@ -313,7 +315,9 @@ def test_out_of_core_matches_in_core(gpu_ctx, shape, dtype, pin):
         I2 = torch.empty(shape, dtype=torch.float32)
         if pin:
             I1, I2 = I1.pin_memory(), I2.pin_memory()
-        r1, r2 = gdp.gdp_destripe_host(gpu_ctx, t0, I2, I1=I1, alpha=0.01, hbm_budget_bytes=budget)
+        # the streamer has no FMG start (gdp.h); compare like with like
+        r1, r2 = gdp.gdp_destripe_host(gpu_ctx, t0, I2, I1=I1, alpha=0.01, hbm_budget_bytes=budget,
+                                       opts=gdp.default_opts(fmg=0, fmg_slices=0))
         assert r1["status"] == "GDP_OK" and r2["status"] == "GDP_OK", (budget, r1, r2)
         outs.append((I1.numpy().copy(), I2.numpy().copy(), r1, r2))
     (a1, a2, ra, _), (b1, b2, rb, rb2) = outs
@@ -356,3 +360,49 @@ def test_npr_filter_limits_and_errors(gpu_ctx):
     for kw in (dict(alpha=0.0), dict(sigma=0.0), dict(lam=-1.0)):
         with pytest.raises(gdp.GdpError):
             gdp.gdp_npr_filter(gpu_ctx, dev(I0), **kw)
+
+
+# ------------------------------------------------------------------ FMG start (gdp_opts.fmg)
+@pytest.mark.parametrize("shape,W,fmg", [((24, 517, 389), (1.0, 1.0, 0.1), 1), ((33, 130, 250), (1.0, 1.0, 0.1), 2),
+                                         ((40, 200, 180), (1.0, 1.0, 0.1), 3), ((32, 96, 96), (1.0, 1.0, 1.0), 1),
+                                         ((12, 1024, 1024), (1.0, 1.0, 0.1), 1)])
+def test_fmg_phase1_schedules_bit_identical(gpu_ctx, shape, W, fmg):
+    """The FMG start gives the same iterate in the reference and fused schedules, and with r0
+    restricted inside the init pass or by the restriction kernel (fmg + 4)."""
+    nz, ny, nx = shape
+    I0 = synth.make_stack(nx, ny, nz, 43, "u8")
+    outs = []
+    for fused, f in ((0, fmg), (3, fmg), (3, fmg + 4)):
+        o = gdp.default_opts(fused=fused, fmg=f, max_vcycles=2, rel_tol=1e-30, stagnation=0)
+        I1, rep = gdp.gdp_diffuse_z(gpu_ctx, dev(I0), W=W, opts=o, check=False)
+        outs.append(I1.cpu().numpy())
+    assert np.array_equal(outs[0], outs[1])
+    assert np.array_equal(outs[1], outs[2])
+
+
+@pytest.mark.parametrize("shape,fmg", [((3, 1031, 777), 1), ((16, 1024, 1024), 3), ((2, 300, 260), 2)])
+def test_fmg_phase2_schedules_bit_identical(gpu_ctx, shape, fmg):
+    nz, ny, nx = shape
+    I0 = synth.make_stack(nx, ny, nz, 47, "u8")
+    I1 = dev(O.diffuse_z_dct(I0).astype(np.float32))
+    outs = []
+    for fused, f in ((0, fmg), (1, fmg), (1, fmg + 4)):
+        o = gdp.default_opts(fused=fused, fmg_slices=f, max_vcycles=2, rel_tol=1e-30, stagnation=0)
+        I2, rep = gdp.gdp_screened_poisson_slices(gpu_ctx, dev(I0), I1, alpha=0.01, opts=o, check=False)
+        outs.append(I2.cpu().numpy())
+    assert np.array_equal(outs[0], outs[1])
+    assert np.array_equal(outs[1], outs[2])
+
+
+@pytest.mark.parametrize("fmg", [1, 2, 3])
+def test_fmg_converges_to_oracle(gpu_ctx, fmg):
+    """Same stopping rule, same converged answer as the oracle (and fewer or equal cycles)."""
+    I0 = synth.make_stack(96, 80, 24, 7, "u8")
+    ref1, ref2 = O.destripe(I0, alpha=0.01)
+    o = gdp.default_opts(fmg=fmg, fmg_slices=fmg)
+    I1, I2, r1, r2 = gdp.gdp_destripe(gpu_ctx, dev(I0), alpha=0.01, opts=o)
+    _, _, p1, p2 = gdp.gdp_destripe(gpu_ctx, dev(I0), alpha=0.01, opts=gdp.default_opts(fmg=0, fmg_slices=0))
+    assert r1["rel_res"][-1] <= 1e-6 and r2["rel_res"][-1] <= 1e-6
+    assert r1["vcycles"] <= p1["vcycles"] and r2["vcycles"] <= p2["vcycles"]
+    assert np.abs(host(I1) - ref1).max() <= TOL_X
+    assert np.abs(host(I2) - ref2).max() <= 1e-4

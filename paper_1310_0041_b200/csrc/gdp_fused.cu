@@ -696,9 +696,13 @@ static void launch2d(bool down, int nu, const Pass2D& P, cudaStream_t s) {
 }
 
 void fused_down2d(const Level& L, const Level& C, const float* xin, float* xout, const RhsK& R,
-                  int mode, int tI, int nu, bool zero_x, cudaStream_t s) {
+                  int mode, int tI, int nu, bool zero_x, cudaStream_t s, bool prolong) {
   // row-marching kernel (gdp_rows2d.cu) for wide planes: no row halo, no barriers (measured
-  // 0.81 vs 1.12 ms on a 1024^2 x 128 down pass); the tile kernel below elsewhere
+  // 0.81 vs 1.12 ms on a 1024^2 x 128 down pass); the tile kernel below elsewhere.
+  // prolong (FMG start): x += P C.x first, by its own pass (k_prolong_xy: 0.26 ms at 1024^2 x
+  // 128; adding it at load inside the row kernel measured 0.64 ms slower)
+  if (prolong)
+    launch_prolong(L.K, const_cast<float*>(xin), C.tx, C.ty, C.tz, C.nx, C.ny, C.nzl, C.z0, C.x, C.xlo, C.xhi, s);
   if (C.tx.coarsened && C.ty.coarsened && L.nx >= 512) {
     rows2d_pass(true, nu, L, C, xin, xout, R.b, zero_x, nullptr, s);
     return;

@@ -132,7 +132,7 @@ double hbm_model(const Hier& H, double s_I, double s_V, int vcycles);
 // fused schedule (gdp_fused.cu): return true if the pass was handled
 bool fusable2d(const Level& L, const Level& C, const gdp_opts& o);
 void fused_down2d(const Level& L, const Level& C, const float* xin, float* xout, const RhsK& R,
-                  int mode, int tI, int nu, bool zero_x, cudaStream_t s);
+                  int mode, int tI, int nu, bool zero_x, cudaStream_t s, bool prolong = false);
 void fused_up2d(const Level& L, const Level& C, const float* xin, float* xout, const RhsK& R,
                 int mode, int tI, int nu, double2* partials, cudaStream_t s);
 int fused_tiles_per_plane(int nu, const Level& L, const Level& C);

@@ -1,3 +1,4 @@
+#include <algorithm>
 // gdp_kernels.cu — sm_100a kernels of the multigrid V-cycle.
 //
 // Reference schedule (opts.fused = 0): one kernel per red-black half-sweep, one per
@@ -148,6 +149,30 @@ __global__ void __launch_bounds__(256) k_prolong(LevelK L, float* __restrict__ x
   if (tzw != 0.f) e = __fmaf_rn(tzw, bil(pJ), __fmul_rn(1.f - tzw, e));
   const long long f = (long long)fz * L.nx * L.ny + (long long)fy * L.nx + fx;
   xf[f] = __fadd_rn(xf[f], e);
+}
+
+// Restriction of a right-hand side alone (FMG start): the sum k_restrict forms for x = 0, where
+// r = b - A 0 = b exactly; same children order and weights -> the same values.
+__global__ void __launch_bounds__(256) k_restrict_b(LevelK L, const float* __restrict__ b, XferAxis tx, XferAxis ty,
+                                                    XferAxis tz, int ncx, int ncy, float* __restrict__ bc) {
+  const int cx = blockIdx.x * blockDim.x + threadIdx.x;
+  const int cy = blockIdx.y * blockDim.y + threadIdx.y;
+  const int cz = blockIdx.z;
+  if (cx >= ncx || cy >= ncy) return;
+  const long long plane = (long long)L.nx * L.ny;
+  const int fx0 = tx.coarsened ? 2 * cx : cx, fx1 = tx.coarsened ? min(2 * cx + 1, L.nx - 1) : cx;
+  const int fy0 = ty.coarsened ? 2 * cy : cy, fy1 = ty.coarsened ? min(2 * cy + 1, L.ny - 1) : cy;
+  const int fz0 = tz.coarsened ? 2 * cz : cz, fz1 = tz.coarsened ? min(2 * cz + 1, L.nzl - 1) : cz;
+  float acc = 0.f;
+  for (int fz = fz0; fz <= fz1; ++fz) {
+    const float wz = rweight(tz, L.z0 + fz);
+    for (int fy = fy0; fy <= fy1; ++fy) {
+      const float wy = rweight(ty, fy);
+      for (int fx = fx0; fx <= fx1; ++fx)
+        acc = __fmaf_rn(rw3(wz, wy, rweight(tx, fx)), __ldg(b + fz * plane + (long long)fy * L.nx + fx), acc);
+    }
+  }
+  bc[(long long)cz * ncx * ncy + (long long)cy * ncx + cx] = acc;
 }
 
 // The same prolongation for plane-local (x/y only) coarsening, 4 columns x PR rows per thread:
@@ -504,37 +529,80 @@ __global__ void __launch_bounds__(512) k_coarse_fd(CoarseK C, const float* __res
   for (int i = threadIdx.x; i < nsys; i += blockDim.x) A[i] = b[off + i];
   __syncthreads();
   // along x: consecutive threads take consecutive modes k, so the x matrix is staged in shared
-  // memory with a padded row stride (conflict-free column walk); `in` rows are broadcast
+  // memory with a padded row stride (conflict-free column walk); `in` rows are broadcast.  The
+  // y / z matrices are staged too (rows broadcast).  Four outputs per thread in flight (ILP);
+  // every dot product still runs j = 0, 1, ... in order.
   float* Ms = sm + 2 * nsys;
+  constexpr int U = 4;
+  const int nt = blockDim.x;
   auto tx = [&](const float* M, float* in, float* out) {
-    for (int i = threadIdx.x; i < nx * nx; i += blockDim.x) Ms[(i / nx) * (nx + 1) + i % nx] = __ldg(M + i);
+    for (int i = threadIdx.x; i < nx * nx; i += nt) Ms[(i / nx) * (nx + 1) + i % nx] = __ldg(M + i);
     __syncthreads();
-    for (int i = threadIdx.x; i < nsys; i += blockDim.x) {
-      const int k = i % nx, r = i / nx;
-      const float* mk = Ms + k * (nx + 1);
-      const float* ir = in + r * nx;
-      float s = 0.f;
-      for (int j = 0; j < nx; ++j) s = fmaf(mk[j], ir[j], s);
-      out[i] = s;
+    for (int i0 = threadIdx.x; i0 < nsys; i0 += U * nt) {
+      const float* mk[U];
+      const float* ir[U];
+      float acc[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = min(i0 + u * nt, nsys - 1);
+        mk[u] = Ms + (i % nx) * (nx + 1);
+        ir[u] = in + (i / nx) * nx;
+        acc[u] = 0.f;
+      }
+      for (int j = 0; j < nx; ++j)
+#pragma unroll
+        for (int u = 0; u < U; ++u) acc[u] = fmaf(mk[u][j], ir[u][j], acc[u]);
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (i0 + u * nt < nsys) out[i0 + u * nt] = acc[u];
     }
     __syncthreads();
   };
   auto ty = [&](const float* M, float* in, float* out) {  // along y
-    for (int i = threadIdx.x; i < nsys; i += blockDim.x) {
-      const int xx = i % nx, k = (i / nx) % ny, z = i / (nx * ny);
-      float s = 0.f;
-      for (int j = 0; j < ny; ++j) s = fmaf(__ldg(M + k * ny + j), in[(z * ny + j) * nx + xx], s);
-      out[i] = s;
+    for (int i = threadIdx.x; i < ny * ny; i += nt) Ms[i] = __ldg(M + i);
+    __syncthreads();
+    for (int i0 = threadIdx.x; i0 < nsys; i0 += U * nt) {
+      const float* mk[U];
+      const float* ic[U];
+      float acc[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = min(i0 + u * nt, nsys - 1);
+        const int xx = i % nx, k = (i / nx) % ny, z = i / (nx * ny);
+        mk[u] = Ms + k * ny;
+        ic[u] = in + (long long)z * ny * nx + xx;
+        acc[u] = 0.f;
+      }
+      for (int j = 0; j < ny; ++j)
+#pragma unroll
+        for (int u = 0; u < U; ++u) acc[u] = fmaf(mk[u][j], ic[u][j * nx], acc[u]);
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (i0 + u * nt < nsys) out[i0 + u * nt] = acc[u];
     }
     __syncthreads();
   };
   auto tz = [&](const float* M, float* in, float* out) {  // along z
     const int pl = nx * ny;
-    for (int i = threadIdx.x; i < nsys; i += blockDim.x) {
-      const int q = i % pl, k = i / pl;
-      float s = 0.f;
-      for (int j = 0; j < nzs; ++j) s = fmaf(__ldg(M + k * nzs + j), in[j * pl + q], s);
-      out[i] = s;
+    for (int i = threadIdx.x; i < nzs * nzs; i += nt) Ms[i] = __ldg(M + i);
+    __syncthreads();
+    for (int i0 = threadIdx.x; i0 < nsys; i0 += U * nt) {
+      const float* mk[U];
+      const float* ic[U];
+      float acc[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = min(i0 + u * nt, nsys - 1);
+        mk[u] = Ms + (i / pl) * nzs;
+        ic[u] = in + i % pl;
+        acc[u] = 0.f;
+      }
+      for (int j = 0; j < nzs; ++j)
+#pragma unroll
+        for (int u = 0; u < U; ++u) acc[u] = fmaf(mk[u][j], ic[u][(long long)j * pl], acc[u]);
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (i0 + u * nt < nsys) out[i0 + u * nt] = acc[u];
     }
     __syncthreads();
   };
@@ -605,6 +673,14 @@ void launch_restrict(const LevelK& L, const float* x, const float* xlo, const fl
     launch_restrict_t<RHS_G, uint8_t>(L, x, xlo, xhi, R, tx, ty, tz, ncx, ncy, nczl, bc, s);
   else
     launch_restrict_t<RHS_G, float>(L, x, xlo, xhi, R, tx, ty, tz, ncx, ncy, nczl, bc, s);
+}
+
+void launch_restrict_b(const LevelK& L, const float* b, const XferAxis& tx, const XferAxis& ty, const XferAxis& tz,
+                       int ncx, int ncy, int nczl, float* bc, cudaStream_t s) {
+  ProfScope ps(KC_RESTRICT, ncell(L) * 4.0 + 4.0 * ncx * ncy * (double)nczl, s, ncell(L));
+  dim3 blk(64, 4);
+  dim3 grd((ncx + 63) / 64, (ncy + 3) / 4, nczl);
+  k_restrict_b<<<grd, blk, 0, s>>>(L, b, tx, ty, tz, ncx, ncy, bc);
 }
 
 void launch_prolong(const LevelK& L, float* xf, const XferAxis& tx, const XferAxis& ty,
@@ -719,7 +795,9 @@ void launch_axpy(float* x, const float* e, long long n, cudaStream_t s) {
 
 size_t coarse_smem_bytes(const CoarseK& C) {
   const long long nsys = (long long)C.nx * C.ny * (C.cz ? C.nz : 1);
-  return (size_t)((2 * nsys + (long long)C.nx * (C.nx + 1)) * sizeof(float));
+  const long long nzs = C.cz ? C.nz : 1;
+  const long long m = std::max({(long long)C.nx * (C.nx + 1), (long long)C.ny * C.ny, nzs * nzs});
+  return (size_t)((2 * nsys + m) * sizeof(float));
 }
 
 cudaError_t launch_coarse(const CoarseK& C, const float* b, float* x, cudaStream_t s) {

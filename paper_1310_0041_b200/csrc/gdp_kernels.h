@@ -83,6 +83,8 @@ void launch_rbgs(const LevelK& L, float* x, const float* xlo, const float* xhi, 
 void launch_restrict(const LevelK& L, const float* x, const float* xlo, const float* xhi,
                      const RhsK& R, int mode, int tI, const XferAxis& tx, const XferAxis& ty,
                      const XferAxis& tz, int ncx, int ncy, int nczl, float* bc, cudaStream_t s);
+void launch_restrict_b(const LevelK& L, const float* b, const XferAxis& tx, const XferAxis& ty, const XferAxis& tz,
+                       int ncx, int ncy, int nczl, float* bc, cudaStream_t s);
 void launch_prolong(const LevelK& L, float* xf, const XferAxis& tx, const XferAxis& ty,
                     const XferAxis& tz, int ncx, int ncy, int nczl, long long cz0, const float* xc,
                     const float* xclo, const float* xchi, cudaStream_t s);

@@ -506,14 +506,14 @@ int run_vcycle(Ctx& ctx, Hier& H, const Fine& f, const gdp_opts& o, cudaStream_t
     // FMG start at l0: x (zeroed above level 0) += P x_{l0+1}, in the first fused 3D sweep
     // when there is one to carry it, else by the prolongation kernel
     const bool pro = l == l0 && (flags & RV_PROLONG);
-    const bool pro_fused = pro && fz[l] == 3 && o.nu_pre >= 2;
+    const bool pro_fused = pro && ((fz[l] == 3 && o.nu_pre >= 2) || fz[l] == 2);
     if (pro) {
       if (l > 0) CK(cudaMemsetAsync(x, 0, sizeof(float) * (size_t)L.nx * L.ny * L.nzl, s));
       if (!pro_fused) launch_prolong(L.K, x, C.tx, C.ty, C.tz, C.nx, C.ny, C.nzl, C.z0, C.x, C.xlo, C.xhi, s);
     }
     const bool zx = l > 0 && !pro;  // level above l0 (or l0 > 0 without FMG): starts from zero
     if (fz[l] == 2) {  // one fused pass: x (A) -> x2 (B)
-      fused_down2d(L, C, x, L.x2, R, mode, tI, o.nu_pre, zx, s);
+      fused_down2d(L, C, x, L.x2, R, mode, tI, o.nu_pre, zx, s, pro_fused);
       cur[l] = L.x2;
       continue;
     }
@@ -620,12 +620,10 @@ static int fmg_start(Ctx& ctx, Hier& H, const Fine& f, const gdp_opts& o, bool r
   Level& L1 = H.lv[1];
   if (!r0_restricted)
     launch_restrict(L0.K, f.x, L0.xlo, L0.xhi, f.R, f.mode, f.tI, L1.tx, L1.ty, L1.tz, L1.nx, L1.ny, L1.nzl, L1.b, s);
-  for (int l = 1; l < nl - 1; ++l) {  // b_{l+1} = R b_l: the residual of x_l = 0
+  for (int l = 1; l < nl - 1; ++l) {  // b_{l+1} = R b_l: the restricted residual of x_l = 0
     Level& L = H.lv[l];
     Level& C = H.lv[l + 1];
-    CK(cudaMemsetAsync(L.x, 0, sizeof(float) * (size_t)L.nx * L.ny * L.nzl, s));
-    const RhsK R{L.b, nullptr, nullptr, 0.f, 0};
-    launch_restrict(L.K, L.x, L.xlo, L.xhi, R, RHS_B, 1, C.tx, C.ty, C.tz, C.nx, C.ny, C.nzl, C.b, s);
+    launch_restrict_b(L.K, L.b, C.tx, C.ty, C.tz, C.nx, C.ny, C.nzl, C.b, s);
   }
   Level& Lc = H.lv[nl - 1];
   CK(launch_coarse(H.coarse, Lc.b, Lc.x, s));

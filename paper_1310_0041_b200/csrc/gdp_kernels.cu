@@ -117,40 +117,6 @@ __global__ void __launch_bounds__(256) k_restrict(LevelK L, const float* __restr
   bc[(long long)cz * ncx * ncy + (long long)cy * ncx + cx] = acc;
 }
 
-// a8: x_fine += P x_coarse (cell-centred linear interpolation, constant at the faces).
-__global__ void __launch_bounds__(256) k_prolong(LevelK L, float* __restrict__ xf,
-                                                 XferAxis tx, XferAxis ty, XferAxis tz,
-                                                 int ncx, int ncy, int nczl, long long cz0,
-                                                 const float* __restrict__ xc,
-                                                 const float* xclo, const float* xchi) {
-  const int fx = blockIdx.x * blockDim.x + threadIdx.x;
-  const int fy = blockIdx.y * blockDim.y + threadIdx.y;
-  const int fz = blockIdx.z;
-  if (fx >= L.nx || fy >= L.ny) return;
-  long long Ix, Jx, Iy, Jy, Iz, Jz;
-  float txw, tyw, tzw;
-  if (ptaps_regular(tx, fx)) ptaps_fast(tx, fx, Ix, Jx, txw); else ptaps(tx, fx, Ix, Jx, txw);
-  if (ptaps_regular(ty, fy)) ptaps_fast(ty, fy, Iy, Jy, tyw); else ptaps(ty, fy, Iy, Jy, tyw);
-  if (ptaps_regular(tz, L.z0 + fz)) ptaps_fast(tz, L.z0 + fz, Iz, Jz, tzw); else ptaps(tz, L.z0 + fz, Iz, Jz, tzw);
-  const long long cplane = (long long)ncx * ncy;
-  // z taps are global coarse indices; map to local planes or ghost planes
-  auto zrow = [&](long long zgc) -> const float* {
-    const long long lz = zgc - cz0;
-    if (lz < 0) return xclo;
-    if (lz >= nczl) return xchi;
-    return xc + lz * cplane;
-  };
-  const float* pI = zrow(Iz);
-  const float* pJ = zrow(Jz);
-  auto bil = [&](const float* p) {
-    return bilerp(p[Iy * ncx + Ix], p[Iy * ncx + Jx], p[Jy * ncx + Ix], p[Jy * ncx + Jx], txw, tyw);
-  };
-  float e = bil(pI);
-  if (tzw != 0.f) e = __fmaf_rn(tzw, bil(pJ), __fmul_rn(1.f - tzw, e));
-  const long long f = (long long)fz * L.nx * L.ny + (long long)fy * L.nx + fx;
-  xf[f] = __fadd_rn(xf[f], e);
-}
-
 // Restriction of a right-hand side alone (FMG start): the sum k_restrict forms for x = 0, where
 // r = b - A 0 = b exactly; same children order and weights -> the same values.
 __global__ void __launch_bounds__(256) k_restrict_b(LevelK L, const float* __restrict__ b, XferAxis tx, XferAxis ty,
@@ -175,12 +141,16 @@ __global__ void __launch_bounds__(256) k_restrict_b(LevelK L, const float* __res
   bc[(long long)cz * ncx * ncy + (long long)cy * ncx + cx] = acc;
 }
 
-// The same prolongation for plane-local (x/y only) coarsening, 4 columns x PR rows per thread:
-// x taps computed once per thread, float4 read-modify-write of xf (same values as k_prolong).
-constexpr int PRO_ROWS = 8;
+// a8: x_fine += P x_coarse (cell-centred linear interpolation, constant at the faces; the
+// ghost coarse planes of a z-slab come from xclo / xchi).  4 columns x `rows` rows of one fine
+// plane per thread: x taps computed
+// once per thread, z taps once per plane, float4 read-modify-write of xf; per element the bilerp
+// (x then y) and z blend of the reference ordering.
 template <bool VEC>
-__global__ void __launch_bounds__(256) k_prolong_xy(LevelK L, float* __restrict__ xf, XferAxis tx, XferAxis ty,
-                                                    int ncx, int ncy, const float* __restrict__ xc) {
+__global__ void __launch_bounds__(256) k_prolong_rows(LevelK L, float* __restrict__ xf, XferAxis tx, XferAxis ty,
+                                                      XferAxis tz, int ncx, int ncy, int nczl, long long cz0,
+                                                      const float* __restrict__ xc, const float* xclo,
+                                                      const float* xchi, int rows) {
   const int gx0 = 4 * (blockIdx.x * blockDim.x + threadIdx.x);
   const int fz = blockIdx.z;
   if (gx0 >= L.nx) return;
@@ -193,15 +163,24 @@ __global__ void __launch_bounds__(256) k_prolong_xy(LevelK L, float* __restrict_
     const int fx = in[c] ? gx0 + c : gx0;
     if (ptaps_regular(tx, fx)) ptaps_fast(tx, fx, Ix[c], Jx[c], txw[c]); else ptaps(tx, fx, Ix[c], Jx[c], txw[c]);
   }
-  const float* pc = xc + (long long)fz * ncx * ncy;
+  long long Iz, Jz;
+  float tzw;
+  if (ptaps_regular(tz, L.z0 + fz)) ptaps_fast(tz, L.z0 + fz, Iz, Jz, tzw); else ptaps(tz, L.z0 + fz, Iz, Jz, tzw);
+  const long long cplane = (long long)ncx * ncy;
+  auto zrow = [&](long long zgc) -> const float* {  // global coarse plane -> local / ghost plane
+    const long long lz = zgc - cz0;
+    if (lz < 0) return xclo;
+    if (lz >= nczl) return xchi;
+    return xc + lz * cplane;
+  };
+  const float* pI = zrow(Iz);
+  const float* pJ = zrow(Jz);
   float* pf = xf + (long long)fz * L.nx * L.ny;
-  const int y0 = blockIdx.y * PRO_ROWS, y1 = min(y0 + PRO_ROWS, L.ny);
+  const int y0 = blockIdx.y * rows, y1 = min(y0 + rows, L.ny);
   for (int fy = y0; fy < y1; ++fy) {
     long long Iy, Jy;
     float tyw;
     if (ptaps_regular(ty, fy)) ptaps_fast(ty, fy, Iy, Jy, tyw); else ptaps(ty, fy, Iy, Jy, tyw);
-    const float* rI = pc + Iy * ncx;
-    const float* rJ = pc + Jy * ncx;
     float* row = pf + (long long)fy * L.nx + gx0;
     float v[4];
     if (VEC && in[3]) {
@@ -211,10 +190,17 @@ __global__ void __launch_bounds__(256) k_prolong_xy(LevelK L, float* __restrict_
 #pragma unroll
       for (int c = 0; c < 4; ++c) v[c] = in[c] ? row[c] : 0.f;
     }
+    auto bil = [&](const float* p, int c) {
+      const float* rI = p + Iy * ncx;
+      const float* rJ = p + Jy * ncx;
+      return bilerp(__ldg(rI + Ix[c]), __ldg(rI + Jx[c]), __ldg(rJ + Ix[c]), __ldg(rJ + Jx[c]), txw[c], tyw);
+    };
 #pragma unroll
-    for (int c = 0; c < 4; ++c)
-      v[c] = __fadd_rn(v[c], bilerp(__ldg(rI + Ix[c]), __ldg(rI + Jx[c]), __ldg(rJ + Ix[c]), __ldg(rJ + Jx[c]),
-                                    txw[c], tyw));
+    for (int c = 0; c < 4; ++c) {
+      float e = bil(pI, c);
+      if (tzw != 0.f) e = __fmaf_rn(tzw, bil(pJ, c), __fmul_rn(1.f - tzw, e));
+      v[c] = __fadd_rn(v[c], e);
+    }
     if (VEC && in[3]) *reinterpret_cast<float4*>(row) = make_float4(v[0], v[1], v[2], v[3]);
     else {
 #pragma unroll
@@ -687,15 +673,14 @@ void launch_prolong(const LevelK& L, float* xf, const XferAxis& tx, const XferAx
                     const XferAxis& tz, int ncx, int ncy, int nczl, long long cz0, const float* xc,
                     const float* xclo, const float* xchi, cudaStream_t s) {
   ProfScope ps(KC_PROLONG, ncell(L) * 8.0 + 4.0 * ncx * ncy * (double)nczl, s, ncell(L));
-  if (!tz.coarsened && nczl == L.nzl && cz0 == L.z0) {  // plane-local: coarse plane z = fine plane z
-    dim3 g((L.nx + 1023) / 1024, (L.ny + PRO_ROWS - 1) / PRO_ROWS, L.nzl);
-    if ((L.nx & 3) == 0 && ((uintptr_t)xf & 15) == 0) k_prolong_xy<true><<<g, 256, 0, s>>>(L, xf, tx, ty, ncx, ncy, xc);
-    else k_prolong_xy<false><<<g, 256, 0, s>>>(L, xf, tx, ty, ncx, ncy, xc);
-    return;
-  }
-  dim3 blk(32, 8);
-  dim3 grd((L.nx + 31) / 32, (L.ny + 7) / 8, L.nzl);
-  k_prolong<<<grd, blk, 0, s>>>(L, xf, tx, ty, tz, ncx, ncy, nczl, cz0, xc, xclo, xchi);
+  // 4 columns per thread; rows per thread: 8 on wide planes, 2 on the small coarse ones
+  const int nt = std::min(256, std::max(32, ((L.nx + 3) / 4 + 31) / 32 * 32));
+  const int rows = L.ny >= 256 ? 8 : 2;
+  dim3 g((L.nx + 4 * nt - 1) / (4 * nt), (L.ny + rows - 1) / rows, L.nzl);
+  if ((L.nx & 3) == 0 && ((uintptr_t)xf & 15) == 0)
+    k_prolong_rows<true><<<g, nt, 0, s>>>(L, xf, tx, ty, tz, ncx, ncy, nczl, cz0, xc, xclo, xchi, rows);
+  else
+    k_prolong_rows<false><<<g, nt, 0, s>>>(L, xf, tx, ty, tz, ncx, ncy, nczl, cz0, xc, xclo, xchi, rows);
 }
 
 int norms_blocks_per_plane(int nx, int ny) {

@@ -299,7 +299,7 @@ __global__ void __launch_bounds__(MT, 1) k_march3d(const __grid_constant__ March
                                  (rq && Ix0 + 1 >= 0 && Ix0 + 1 < P.ncx) ? __ldg(rp + 1) : 0.f);
       }
     };
-    // bilinear correction packs of one coarse plane (bilerp order of k_prolong per element)
+    // bilinear correction packs of one coarse plane (bilerp order of k_prolong_rows per element)
     auto bil_plane = [&](const float2 (&cv)[MNQ], float2 (&eA)[MR], float2 (&eB)[MR]) {
       float2 cn[MNQ];
 #pragma unroll

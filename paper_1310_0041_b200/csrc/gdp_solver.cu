@@ -506,7 +506,7 @@ int run_vcycle(Ctx& ctx, Hier& H, const Fine& f, const gdp_opts& o, cudaStream_t
     // FMG start at l0: x (zeroed above level 0) += P x_{l0+1}, in the first fused 3D sweep
     // when there is one to carry it, else by the prolongation kernel
     const bool pro = l == l0 && (flags & RV_PROLONG);
-    const bool pro_fused = pro && ((fz[l] == 3 && o.nu_pre >= 2) || fz[l] == 2);
+    const bool pro_fused = pro && ((fz[l] == 3 && o.nu_pre >= 2 && l == 0) || fz[l] == 2);
     if (pro) {
       if (l > 0) CK(cudaMemsetAsync(x, 0, sizeof(float) * (size_t)L.nx * L.ny * L.nzl, s));
       if (!pro_fused) launch_prolong(L.K, x, C.tx, C.ty, C.tz, C.nx, C.ny, C.nzl, C.z0, C.x, C.xlo, C.xhi, s);
@@ -552,10 +552,14 @@ int run_vcycle(Ctx& ctx, Hier& H, const Fine& f, const gdp_opts& o, cudaStream_t
       const int items = fused3d_items(L, C);
       const bool want = l == 0 && (size_t)items <= H.partials_cap * (size_t)L.nzl;
       float* c = cur[l];
+      // coarse levels: the prolongation by its own kernel (the z-march's coarse-row loads are
+      // exposed latency there: e.g. 156 vs 53 + ~25 us on a 256^2 x 128 level)
+      const bool sep = l > 0;
+      if (sep) launch_prolong(L.K, c, C.tx, C.ty, C.tz, C.nx, C.ny, C.nzl, C.z0, C.x, C.xlo, C.xhi, s);
       for (int k = 0; k < o.nu_post; ++k) {
         float* d = c == x ? L.x2 : x;
         const bool last = k == o.nu_post - 1;
-        fused_sweep3d(L, C, c, d, R.b, false, k == 0, last && want ? 2 : 0, want ? H.partials : nullptr, s);
+        fused_sweep3d(L, C, c, d, R.b, false, k == 0 && !sep, last && want ? 2 : 0, want ? H.partials : nullptr, s);
         c = d;
       }
       if (c != x) CK(cudaMemcpyAsync(x, c, sizeof(float) * (size_t)L.nx * L.ny * L.nzl, cudaMemcpyDeviceToDevice, s));

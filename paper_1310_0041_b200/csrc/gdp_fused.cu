@@ -649,8 +649,12 @@ static TileRect tiles2d(int nu, const LevelK& L, bool fast_ok) {
 }
 
 // norm partials per plane left by the fused up pass of level L (coarse level C)
-int fused_tiles_per_plane(int nu, const Level& L, const Level& C) {
-  (void)C;  // the up pass always runs the tile kernels: one partial per (plane, tile)
+// the up pass on wide planes: prolongation kernel + row-marching sweeps (the prolongation inside
+// either fused kernel costs more than its own streaming pass there)
+static bool up2d_rows(const Level& L, const Level& C) { return C.tx.coarsened && C.ty.coarsened && L.nx >= 512; }
+
+int fused_tiles_per_plane(int nu, const Level& L, const Level& C) {  // norm partials per plane
+  if (up2d_rows(L, C)) return rows2d_items_per_plane(nu, L.K);
   const TileRect T = tiles2d(nu, L.K, false);
   return T.gx * T.gy;
 }
@@ -704,7 +708,7 @@ void fused_down2d(const Level& L, const Level& C, const float* xin, float* xout,
   if (prolong)
     launch_prolong(L.K, const_cast<float*>(xin), C.tx, C.ty, C.tz, C.nx, C.ny, C.nzl, C.z0, C.x, C.xlo, C.xhi, s);
   if (C.tx.coarsened && C.ty.coarsened && L.nx >= 512) {
-    rows2d_pass(true, nu, L, C, xin, xout, R.b, zero_x, nullptr, s);
+    rows2d_pass(true, nu, L, C, xin, xout, R.b, zero_x, nullptr, s, false);
     return;
   }
   Pass2D P{};
@@ -718,6 +722,11 @@ void fused_down2d(const Level& L, const Level& C, const float* xin, float* xout,
 
 void fused_up2d(const Level& L, const Level& C, const float* xin, float* xout, const RhsK& R,
                 int mode, int tI, int nu, double2* partials, cudaStream_t s) {
+  if (up2d_rows(L, C)) {
+    launch_prolong(L.K, const_cast<float*>(xin), C.tx, C.ty, C.tz, C.nx, C.ny, C.nzl, C.z0, C.x, C.xlo, C.xhi, s);
+    rows2d_pass(false, nu, L, C, xin, xout, R.b, false, partials, s, false);
+    return;
+  }
   Pass2D P{};
   P.L = L.K; P.xin = xin; P.xout = xout; P.R = R; P.zero_x = 0;
   P.fast_ok = C.tx.coarsened && C.ty.coarsened;

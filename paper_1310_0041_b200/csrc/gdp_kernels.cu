@@ -163,6 +163,9 @@ __global__ void __launch_bounds__(256) k_prolong_rows(LevelK L, float* __restric
     const int fx = in[c] ? gx0 + c : gx0;
     if (ptaps_regular(tx, fx)) ptaps_fast(tx, fx, Ix[c], Jx[c], txw[c]); else ptaps(tx, fx, Ix[c], Jx[c], txw[c]);
   }
+  const long long I0 = gx0 >> 1;
+  const bool xreg = VEC && in[3] && tx.coarsened && (ncx & 1) == 0 && ptaps_regular(tx, gx0) &&
+                    ptaps_regular(tx, gx0 + 3);
   long long Iz, Jz;
   float tzw;
   if (ptaps_regular(tz, L.z0 + fz)) ptaps_fast(tz, L.z0 + fz, Iz, Jz, tzw); else ptaps(tz, L.z0 + fz, Iz, Jz, tzw);
@@ -190,16 +193,39 @@ __global__ void __launch_bounds__(256) k_prolong_rows(LevelK L, float* __restric
 #pragma unroll
       for (int c = 0; c < 4; ++c) v[c] = in[c] ? row[c] : 0.f;
     }
-    auto bil = [&](const float* p, int c) {
-      const float* rI = p + Iy * ncx;
-      const float* rJ = p + Jy * ncx;
-      return bilerp(__ldg(rI + Ix[c]), __ldg(rI + Jx[c]), __ldg(rJ + Ix[c]), __ldg(rJ + Jx[c]), txw[c], tyw);
-    };
+    if (xreg) {  // regular x taps: coarse columns I0-1 .. I0+2 once per coarse row
+      float e[4], f[4];
+      auto quad = [&](const float* p, float (&o)[4]) {
+        const float* rI = p + Iy * ncx + I0;
+        const float* rJ = p + Jy * ncx + I0;
+        const float2 mI = __ldg(reinterpret_cast<const float2*>(rI));
+        const float2 mJ = __ldg(reinterpret_cast<const float2*>(rJ));
+        const float lI = __ldg(rI - 1), hI = __ldg(rI + 2), lJ = __ldg(rJ - 1), hJ = __ldg(rJ + 2);
+        o[0] = bilerp(mI.x, lI, mJ.x, lJ, 0.25f, tyw);    // I = I0,   J = I0-1
+        o[1] = bilerp(mI.x, mI.y, mJ.x, mJ.y, 0.25f, tyw);  // I = I0,   J = I0+1
+        o[2] = bilerp(mI.y, mI.x, mJ.y, mJ.x, 0.25f, tyw);  // I = I0+1, J = I0
+        o[3] = bilerp(mI.y, hI, mJ.y, hJ, 0.25f, tyw);    // I = I0+1, J = I0+2
+      };
+      quad(pI, e);
+      if (tzw != 0.f) {
+        quad(pJ, f);
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      float e = bil(pI, c);
-      if (tzw != 0.f) e = __fmaf_rn(tzw, bil(pJ, c), __fmul_rn(1.f - tzw, e));
-      v[c] = __fadd_rn(v[c], e);
+        for (int c = 0; c < 4; ++c) e[c] = __fmaf_rn(tzw, f[c], __fmul_rn(1.f - tzw, e[c]));
+      }
+#pragma unroll
+      for (int c = 0; c < 4; ++c) v[c] = __fadd_rn(v[c], e[c]);
+    } else {
+      auto bil = [&](const float* p, int c) {
+        const float* rI = p + Iy * ncx;
+        const float* rJ = p + Jy * ncx;
+        return bilerp(__ldg(rI + Ix[c]), __ldg(rI + Jx[c]), __ldg(rJ + Ix[c]), __ldg(rJ + Jx[c]), txw[c], tyw);
+      };
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        float e = bil(pI, c);
+        if (tzw != 0.f) e = __fmaf_rn(tzw, bil(pJ, c), __fmul_rn(1.f - tzw, e));
+        v[c] = __fadd_rn(v[c], e);
+      }
     }
     if (VEC && in[3]) *reinterpret_cast<float4*>(row) = make_float4(v[0], v[1], v[2], v[3]);
     else {

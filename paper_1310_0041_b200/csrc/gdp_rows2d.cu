@@ -72,7 +72,7 @@ __device__ __noinline__ R2Tap r2_ptaps(XferAxis a, int i) {
   return R2Tap{(int)(J - I), t};
 }
 
-template <int NU, bool DOWN, bool VEC>
+template <int NU, bool DOWN, bool VEC, bool PRO>
 __device__ __forceinline__ void rows2d_march(const Rows2D& P, float4 (*sx)[R2_WARPS * 32],
                                              float4 (*sb)[R2_WARPS * 32], long long item) {
   using RC = R2C<NU>;
@@ -162,7 +162,7 @@ __device__ __forceinline__ void rows2d_march(const Rows2D& P, float4 (*sx)[R2_WA
     if ((P.ncx & 1) == 0 && Ix0 >= 0 && Ix0 + 1 < P.ncx) return __ldg(reinterpret_cast<const float2*>(rp));
     return make_float2(Ix0 >= 0 && Ix0 < P.ncx ? __ldg(rp) : 0.f, Ix0 + 1 >= 0 && Ix0 + 1 < P.ncx ? __ldg(rp + 1) : 0.f);
   };
-  if (!DOWN) {
+  if (PRO) {
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
       long long I, J;
@@ -221,7 +221,7 @@ __device__ __forceinline__ void rows2d_march(const Rows2D& P, float4 (*sx)[R2_WA
         X[K].A = make_float2(v.x, v.z);
         X[K].B = make_float2(v.y, v.w);
       }
-      if (!DOWN) {
+      if (PRO) {
         if ((t & 1) == 0 && t > a) {  // coarse row c = t >> 1 begins: slide the window
           CR[0] = CR[1]; CR[1] = CR[2]; CR[2] = CR[3]; CR[3] = CR[4];
           CR[4] = load_cr((t >> 1) + 3);
@@ -339,14 +339,15 @@ __device__ __forceinline__ void rows2d_march(const Rows2D& P, float4 (*sx)[R2_WA
   }
 }
 
-template <int NU, bool DOWN>
+// PRO: the coarse correction is added to x at load (else the caller prolongated beforehand)
+template <int NU, bool DOWN, bool PRO>
 __global__ void __launch_bounds__(R2_WARPS * 32) k_rows2d(const __grid_constant__ Rows2D P) {
   __shared__ float4 sx[R2_SL][R2_WARPS * 32];
   __shared__ float4 sb[R2_SL][R2_WARPS * 32];
   const long long item = (long long)blockIdx.x * R2_WARPS + (threadIdx.x >> 5);
   if (item >= P.nitems) return;  // warp-uniform; the kernel has no block-wide barrier
-  if ((P.L.nx & 3) == 0) rows2d_march<NU, DOWN, true>(P, sx, sb, item);
-  else rows2d_march<NU, DOWN, false>(P, sx, sb, item);
+  if ((P.L.nx & 3) == 0) rows2d_march<NU, DOWN, true, PRO>(P, sx, sb, item);
+  else rows2d_march<NU, DOWN, false, PRO>(P, sx, sb, item);
 }
 
 // ---------------------------------------------------------------------------------
@@ -392,21 +393,24 @@ int rows2d_items_per_plane(int nu, const LevelK& L) {
 }
 
 void rows2d_pass(bool down, int nu, const Level& L, const Level& C, const float* xin, float* xout, const float* b,
-                 bool zero_x, double2* partials, cudaStream_t s) {
+                 bool zero_x, double2* partials, cudaStream_t s, bool prolong) {
   Rows2D P{};
   P.L = L.K; P.xin = xin; P.xout = xout; P.b = b; P.zero_x = zero_x ? 1 : 0;
   P.tx = C.tx; P.ty = C.ty; P.ncx = C.nx; P.ncy = C.ny;
   P.bc = C.b; P.xc = C.x; P.partials = partials;
   plan_rows2d(nu, L.K, P);
   const double N = (double)L.nx * L.ny * L.nzl, Nc = (double)C.nx * C.ny * C.nzl;
-  ProfScope ps(down ? KC_DOWN2D : KC_UP2D, N * ((zero_x ? 4.0 : 8.0) + 4.0) + Nc * 4.0, s, N);
+  ProfScope ps(down ? KC_DOWN2D : KC_UP2D, N * ((zero_x ? 4.0 : 8.0) + 4.0) + ((down || prolong) ? Nc * 4.0 : 0.0), s, N);
   const unsigned grid = (unsigned)((P.nitems + R2_WARPS - 1) / R2_WARPS);
   if (down) {
-    if (nu == 1) k_rows2d<1, true><<<grid, R2_WARPS * 32, 0, s>>>(P);
-    else k_rows2d<2, true><<<grid, R2_WARPS * 32, 0, s>>>(P);
+    if (nu == 1) k_rows2d<1, true, false><<<grid, R2_WARPS * 32, 0, s>>>(P);
+    else k_rows2d<2, true, false><<<grid, R2_WARPS * 32, 0, s>>>(P);
+  } else if (prolong) {
+    if (nu == 1) k_rows2d<1, false, true><<<grid, R2_WARPS * 32, 0, s>>>(P);
+    else k_rows2d<2, false, true><<<grid, R2_WARPS * 32, 0, s>>>(P);
   } else {
-    if (nu == 1) k_rows2d<1, false><<<grid, R2_WARPS * 32, 0, s>>>(P);
-    else k_rows2d<2, false><<<grid, R2_WARPS * 32, 0, s>>>(P);
+    if (nu == 1) k_rows2d<1, false, false><<<grid, R2_WARPS * 32, 0, s>>>(P);
+    else k_rows2d<2, false, false><<<grid, R2_WARPS * 32, 0, s>>>(P);
   }
 }
 

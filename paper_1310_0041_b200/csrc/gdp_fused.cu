@@ -651,7 +651,7 @@ static TileRect tiles2d(int nu, const LevelK& L, bool fast_ok) {
 // norm partials per plane left by the fused up pass of level L (coarse level C)
 // the up pass on wide planes: prolongation kernel + row-marching sweeps (the prolongation inside
 // either fused kernel costs more than its own streaming pass there)
-static bool up2d_rows(const Level& L, const Level& C) { return C.tx.coarsened && C.ty.coarsened && L.nx >= 512; }
+static bool up2d_rows(const Level& L, const Level& C) { return C.tx.coarsened && C.ty.coarsened && L.nx >= 128; }
 
 int fused_tiles_per_plane(int nu, const Level& L, const Level& C) {  // norm partials per plane
   if (up2d_rows(L, C)) return rows2d_items_per_plane(nu, L.K);
@@ -707,7 +707,7 @@ void fused_down2d(const Level& L, const Level& C, const float* xin, float* xout,
   // 128; adding it at load inside the row kernel measured 0.64 ms slower)
   if (prolong)
     launch_prolong(L.K, const_cast<float*>(xin), C.tx, C.ty, C.tz, C.nx, C.ny, C.nzl, C.z0, C.x, C.xlo, C.xhi, s);
-  if (C.tx.coarsened && C.ty.coarsened && L.nx >= 512) {
+  if (C.tx.coarsened && C.ty.coarsened && L.nx >= 128) {
     rows2d_pass(true, nu, L, C, xin, xout, R.b, zero_x, nullptr, s, false);
     return;
   }

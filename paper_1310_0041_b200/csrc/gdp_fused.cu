@@ -703,14 +703,14 @@ void fused_down2d(const Level& L, const Level& C, const float* xin, float* xout,
                   int mode, int tI, int nu, bool zero_x, cudaStream_t s, bool prolong) {
   // row-marching kernel (gdp_rows2d.cu) for wide planes: no row halo, no barriers (measured
   // 0.81 vs 1.12 ms on a 1024^2 x 128 down pass); the tile kernel below elsewhere.
-  // prolong (FMG start): x += P C.x first, by its own pass (k_prolong_xy: 0.26 ms at 1024^2 x
-  // 128; adding it at load inside the row kernel measured 0.64 ms slower)
-  if (prolong)
-    launch_prolong(L.K, const_cast<float*>(xin), C.tx, C.ty, C.tz, C.nx, C.ny, C.nzl, C.z0, C.x, C.xlo, C.xhi, s);
+  // prolong (FMG start): x += P C.x, added at load by the row kernel (coarse rows staged in
+  // shared memory; +0.2 ms at 1024^2 x 128 against 0.31 ms for its own pass), else by its own pass
   if (C.tx.coarsened && C.ty.coarsened && L.nx >= 128) {
-    rows2d_pass(true, nu, L, C, xin, xout, R.b, zero_x, nullptr, s, false);
+    rows2d_pass(true, nu, L, C, xin, xout, R.b, zero_x, nullptr, s, prolong);
     return;
   }
+  if (prolong)
+    launch_prolong(L.K, const_cast<float*>(xin), C.tx, C.ty, C.tz, C.nx, C.ny, C.nzl, C.z0, C.x, C.xlo, C.xhi, s);
   Pass2D P{};
   P.L = L.K; P.xin = xin; P.xout = xout; P.R = R; P.zero_x = zero_x ? 1 : 0;
   P.fast_ok = C.tx.coarsened && C.ty.coarsened;
@@ -722,7 +722,7 @@ void fused_down2d(const Level& L, const Level& C, const float* xin, float* xout,
 
 void fused_up2d(const Level& L, const Level& C, const float* xin, float* xout, const RhsK& R,
                 int mode, int tI, int nu, double2* partials, cudaStream_t s) {
-  if (up2d_rows(L, C)) {
+  if (up2d_rows(L, C)) {  // the prolongation inside the row kernel measured slower (1.03 vs 0.31 + 0.65 ms)
     launch_prolong(L.K, const_cast<float*>(xin), C.tx, C.ty, C.tz, C.nx, C.ny, C.nzl, C.z0, C.x, C.xlo, C.xhi, s);
     rows2d_pass(false, nu, L, C, xin, xout, R.b, false, partials, s, false);
     return;

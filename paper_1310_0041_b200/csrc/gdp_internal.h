@@ -139,7 +139,7 @@ int fused_tiles_per_plane(int nu, const Level& L, const Level& C);
 // row-marching 2D passes (gdp_rows2d.cu)
 int rows2d_items_per_plane(int nu, const LevelK& L);
 void rows2d_pass(bool down, int nu, const Level& L, const Level& C, const float* xin, float* xout, const float* b,
-                 bool zero_x, double2* partials, cudaStream_t s, bool prolong = true);
+                 bool zero_x, double2* partials, cudaStream_t s, bool prolong = false);
 bool fusable3d(const Level& L, const Level& C, const gdp_opts& o);
 int fused3d_items(const Level& L, const Level& C, int zlo = 0, int zhi = -1);
 int fused_sweep3d(const Level& L, const Level& C, const float* xin, float* xout, const float* b,

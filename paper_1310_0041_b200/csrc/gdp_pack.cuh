@@ -34,6 +34,11 @@ __device__ __forceinline__ void cp_async16z(void* smem, const void* gmem, bool v
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(valid ? 16 : 0));
 }
+// 8 bytes, zero-filled when !valid
+__device__ __forceinline__ void cp_async8z(void* smem, const void* gmem, bool valid) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(valid ? 8 : 0));
+}
 // 4 bytes, zero-filled when !valid
 __device__ __forceinline__ void cp_async4z(void* smem, const void* gmem, bool valid) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);

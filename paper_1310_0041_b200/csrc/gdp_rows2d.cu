@@ -50,6 +50,7 @@ template <int NU> struct R2C {
 constexpr int R2_WARPS = 4;
 constexpr int R2_D = 5;   // prefetch distance (rows)
 constexpr int R2_SL = 8;  // staging slots (power of two > R2_D)
+constexpr int R2_CS = 8;  // coarse-row slots (rows c-1 .. c+6 live at once)
 
 struct Row4 { float2 A, B; };
 
@@ -74,7 +75,8 @@ __device__ __noinline__ R2Tap r2_ptaps(XferAxis a, int i) {
 
 template <int NU, bool DOWN, bool VEC, bool PRO>
 __device__ __forceinline__ void rows2d_march(const Rows2D& P, float4 (*sx)[R2_WARPS * 32],
-                                             float4 (*sb)[R2_WARPS * 32], long long item) {
+                                             float4 (*sb)[R2_WARPS * 32], float2 (*sc)[R2_WARPS * 32],
+                                             long long item) {
   using RC = R2C<NU>;
   constexpr int XR = RC::XR, BR = RC::BR, S = RC::S, LAG = RC::LAG;
   const int tid = threadIdx.x, lane = tid & 31;
@@ -120,8 +122,41 @@ __device__ __forceinline__ void rows2d_march(const Rows2D& P, float4 (*sx)[R2_WA
   const int a = max(y_lo - LAG, 0), e = min(y_hi + LAG, ny);
   const int tend = y_hi + LAG;
 
+  // ---- prolongation (PRO)
+  const int Ix0 = gx0 >> 1;
+  const long long cplane = (long long)P.ncx * P.ncy;
+  // PRO: coarse rows (columns Ix0, Ix0 + 1) are cp.async-staged into a private ring of 8 slots
+  // indexed by coarse row mod 8: row J goes out with the staging of fine row 2(J-3), so it is
+  // complete before the first row that reads it and no register ever waits on it
+  const float* xcp = PRO ? P.xc + (long long)iz * cplane : nullptr;
+  auto issue_cr = [&](int J) {
+    float2* d = &sc[J & (R2_CS - 1)][tid];
+    const bool rq = J >= 0 && J < P.ncy;
+    const float* rp = xcp + (long long)(rq ? J : 0) * P.ncx;
+    const bool v0 = rq && Ix0 >= 0 && Ix0 < P.ncx, v1 = rq && Ix0 + 1 >= 0 && Ix0 + 1 < P.ncx;
+    if ((P.ncx & 1) == 0 && v0 && v1) {
+      cp_async8z(d, rp + Ix0, true);
+    } else {
+      cp_async4z(&d->x, v0 ? rp + Ix0 : xcp, v0);
+      cp_async4z(&d->y, v1 ? rp + Ix0 + 1 : xcp, v1);
+    }
+  };
+  float ptx[4];
+  bool selfJ[4];
+  if (PRO) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      long long I, J;
+      ptaps(P.tx, gx0 + c, I, J, ptx[c]);
+      selfJ[c] = J == I;
+    }
+    const int c0 = a >> 1;
+#pragma unroll
+    for (int d = -1; d <= 3; ++d) issue_cr(c0 + d);  // joins the first staging group
+  }
   auto issue = [&](int t) {  // stage row t (own quads) into slot t & 7
     const int sl = t & (R2_SL - 1);
+    if (PRO && (t & 1) == 0) issue_cr((t >> 1) + 3);
     const long long ro = pbase + (long long)t * nx + gx0;
     if constexpr (VEC) {
       const long long o = lane_full ? ro : 0;
@@ -150,29 +185,6 @@ __device__ __forceinline__ void rows2d_march(const Rows2D& P, float4 (*sx)[R2_WA
 #pragma unroll
   for (int k = 0; k < BR; ++k) Bv[k].A = Bv[k].B = f2(0.f);
 
-  // ---- up: coarse rows (columns Ix0, Ix0 + 1) in a ring of 4 indexed by coarse row mod 4
-  const int Ix0 = gx0 >> 1;
-  const long long cplane = (long long)P.ncx * P.ncy;
-  float2 CR[5] = {f2(0.f), f2(0.f), f2(0.f), f2(0.f), f2(0.f)};  // coarse rows c-1 .. c+3, c = t >> 1
-  float ptx[4];
-  bool selfJ[4];
-  auto load_cr = [&](int J) -> float2 {
-    if (J < 0 || J >= P.ncy) return f2(0.f);
-    const float* rp = P.xc + (long long)iz * cplane + (long long)J * P.ncx + Ix0;
-    if ((P.ncx & 1) == 0 && Ix0 >= 0 && Ix0 + 1 < P.ncx) return __ldg(reinterpret_cast<const float2*>(rp));
-    return make_float2(Ix0 >= 0 && Ix0 < P.ncx ? __ldg(rp) : 0.f, Ix0 + 1 >= 0 && Ix0 + 1 < P.ncx ? __ldg(rp + 1) : 0.f);
-  };
-  if (PRO) {
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      long long I, J;
-      ptaps(P.tx, gx0 + c, I, J, ptx[c]);
-      selfJ[c] = J == I;
-    }
-    const int c0 = a >> 1;
-#pragma unroll
-    for (int d = -1; d <= 3; ++d) CR[d + 1] = load_cr(c0 + d);
-  }
   float2 racc = f2(0.f);  // down: restriction accumulated over the two child rows
   double sr = 0.0, sbb = 0.0;
 
@@ -222,16 +234,13 @@ __device__ __forceinline__ void rows2d_march(const Rows2D& P, float4 (*sx)[R2_WA
         X[K].B = make_float2(v.y, v.w);
       }
       if (PRO) {
-        if ((t & 1) == 0 && t > a) {  // coarse row c = t >> 1 begins: slide the window
-          CR[0] = CR[1]; CR[1] = CR[2]; CR[2] = CR[3]; CR[3] = CR[4];
-          CR[4] = load_cr((t >> 1) + 3);
-        }
+        const int cc = t >> 1;
         int dq;
         float ty;
         if (ptaps_regular(P.ty, t)) { dq = (t & 1) ? 1 : -1; ty = 0.25f; }  // == ptaps_fast
         else { const R2Tap tp = r2_ptaps(P.ty, t); dq = tp.dq; ty = tp.t; }
-        const float2 r0 = CR[1];
-        const float2 n0 = dq < 0 ? CR[0] : (dq > 0 ? CR[2] : r0);
+        const float2 r0 = sc[cc & (R2_CS - 1)][tid];
+        const float2 n0 = sc[(cc + dq) & (R2_CS - 1)][tid];
         const float2 r1 = make_float2(__shfl_up_sync(FULL, r0.y, 1), __shfl_down_sync(FULL, r0.x, 1));
         const float2 n1 = make_float2(__shfl_up_sync(FULL, n0.y, 1), __shfl_down_sync(FULL, n0.x, 1));
         const float2 txA = make_float2(ptx[0], ptx[2]), txB = make_float2(ptx[1], ptx[3]);
@@ -344,10 +353,11 @@ template <int NU, bool DOWN, bool PRO>
 __global__ void __launch_bounds__(R2_WARPS * 32) k_rows2d(const __grid_constant__ Rows2D P) {
   __shared__ float4 sx[R2_SL][R2_WARPS * 32];
   __shared__ float4 sb[R2_SL][R2_WARPS * 32];
+  __shared__ float2 sc[PRO ? R2_CS : 1][R2_WARPS * 32];
   const long long item = (long long)blockIdx.x * R2_WARPS + (threadIdx.x >> 5);
   if (item >= P.nitems) return;  // warp-uniform; the kernel has no block-wide barrier
-  if ((P.L.nx & 3) == 0) rows2d_march<NU, DOWN, true, PRO>(P, sx, sb, item);
-  else rows2d_march<NU, DOWN, false, PRO>(P, sx, sb, item);
+  if ((P.L.nx & 3) == 0) rows2d_march<NU, DOWN, true, PRO>(P, sx, sb, sc, item);
+  else rows2d_march<NU, DOWN, false, PRO>(P, sx, sb, sc, item);
 }
 
 // ---------------------------------------------------------------------------------
@@ -400,9 +410,12 @@ void rows2d_pass(bool down, int nu, const Level& L, const Level& C, const float*
   P.bc = C.b; P.xc = C.x; P.partials = partials;
   plan_rows2d(nu, L.K, P);
   const double N = (double)L.nx * L.ny * L.nzl, Nc = (double)C.nx * C.ny * C.nzl;
-  ProfScope ps(down ? KC_DOWN2D : KC_UP2D, N * ((zero_x ? 4.0 : 8.0) + 4.0) + ((down || prolong) ? Nc * 4.0 : 0.0), s, N);
+  ProfScope ps(down ? KC_DOWN2D : KC_UP2D, N * ((zero_x ? 4.0 : 8.0) + 4.0) + Nc * ((down ? 4.0 : 0.0) + (prolong ? 4.0 : 0.0)), s, N);
   const unsigned grid = (unsigned)((P.nitems + R2_WARPS - 1) / R2_WARPS);
-  if (down) {
+  if (down && prolong) {  // FMG start: the coarse correction added at load
+    if (nu == 1) k_rows2d<1, true, true><<<grid, R2_WARPS * 32, 0, s>>>(P);
+    else k_rows2d<2, true, true><<<grid, R2_WARPS * 32, 0, s>>>(P);
+  } else if (down) {
     if (nu == 1) k_rows2d<1, true, false><<<grid, R2_WARPS * 32, 0, s>>>(P);
     else k_rows2d<2, true, false><<<grid, R2_WARPS * 32, 0, s>>>(P);
   } else if (prolong) {

@@ -275,28 +275,6 @@ __global__ void __launch_bounds__(256) k_norms(LevelK L, const float* __restrict
   }
 }
 
-// per-plane sums of a field (mean pin, a10): partial (sum a, sum a2) with a2 a second field
-template <typename TA, typename TB>
-__global__ void __launch_bounds__(256) k_plane_sums(const void* a, const void* b, int nx, int ny,
-                                                    double2* partials) {
-  const int ix = blockIdx.x * blockDim.x + threadIdx.x;
-  const int iz = blockIdx.z;
-  const long long plane = (long long)nx * ny;
-  double sa = 0.0, sb = 0.0;
-  if (ix < nx) {
-    for (int iy = blockIdx.y * blockDim.y + threadIdx.y; iy < ny; iy += gridDim.y * blockDim.y) {
-      const long long c = iz * plane + (long long)iy * nx + ix;
-      sa += (double)ldI<TA>(a, c);
-      if (b) sb += (double)ldI<TB>(b, c);
-    }
-  }
-  block_sum2(sa, sb);
-  if (threadIdx.x == 0 && threadIdx.y == 0) {
-    const long long bid = ((long long)iz * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
-    partials[bid] = make_double2(sa, sb);
-  }
-}
-
 // fixed-order reduction of `per` partials per plane -> out[plane]
 __global__ void __launch_bounds__(256) k_finalize(const double2* partials, int per,
                                                   double2* out) {
@@ -339,6 +317,38 @@ template <> struct Quad<uint8_t> {
     for (int c = 0; c < 4; ++c) v[c] = decode_u8((w >> (8 * c)) & 0xffu);
   }
 };
+
+// per-plane sums for the mean pin (a10), 4 columns per thread (one float4 / 4-byte load per
+// field and row), rows strided by gridDim.y; each thread adds its quad left to right in fp64
+template <typename TA, typename TB, bool VEC>
+__global__ void __launch_bounds__(256) k_plane_sums4(const void* a, const void* b, int nx, int ny,
+                                                     double2* partials) {
+  const int gx0 = 4 * (blockIdx.x * blockDim.x + threadIdx.x);
+  const int iz = blockIdx.z;
+  const long long plane = (long long)nx * ny;
+  double sa = 0.0, sb = 0.0;
+  if (gx0 < nx) {
+    const int n = min(4, nx - gx0);
+#pragma unroll 4
+    for (int iy = blockIdx.y; iy < ny; iy += gridDim.y) {
+      const long long c = iz * plane + (long long)iy * nx + gx0;
+      float va[4] = {0.f, 0.f, 0.f, 0.f}, vb[4] = {0.f, 0.f, 0.f, 0.f};
+      if (VEC) {
+        Quad<TA>::ld(a, c, va);
+        if (b) Quad<TB>::ld(b, c, vb);
+      } else {
+        for (int k = 0; k < n; ++k) {
+          va[k] = ldI<TA>(a, c + k);
+          if (b) vb[k] = ldI<TB>(b, c + k);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) { sa += (double)va[k]; sb += (double)vb[k]; }
+    }
+  }
+  block_sum2(sa, sb);
+  if (threadIdx.x == 0) partials[((long long)iz * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = make_double2(sa, sb);
+}
 
 template <typename TI, bool VEC>
 __global__ void __launch_bounds__(256) k_init(LevelK L, RhsK R, float* __restrict__ x0, float* __restrict__ b,
@@ -736,19 +746,34 @@ void launch_norms(const LevelK& L, const float* x, const float* xlo, const float
   k_finalize<<<L.nzl, 256, 0, s>>>(partials, norms_blocks_per_plane(L.nx, L.ny), plane_out);
 }
 
+static int plane_sums_blocks_per_plane(int nx, int ny) {
+  const int gx = (nx + 1023) / 1024;
+  return gx * std::max(1, std::min((ny + 1) / 2, 32));
+}
+
 void launch_plane_sums(const void* a, int ta, const void* b, int tb, int nx, int ny, int nz,
                        double2* partials, double2* plane_out, cudaStream_t s) {
+  int per = 0;
   {
   ProfScope ps(KC_UTIL, (double)nx * ny * nz * ((ta ? 4 : 1) + (b ? (tb ? 4 : 1) : 0)), s);
-  dim3 blk(128, 2);
-  dim3 grd = grid_plane(nx, ny, nz, blk, 32);
-  if (ta == 1 && tb == 0) k_plane_sums<float, uint8_t><<<grd, blk, 0, s>>>(a, b, nx, ny, partials);
-  else if (ta == 1) k_plane_sums<float, float><<<grd, blk, 0, s>>>(a, b, nx, ny, partials);
-  else if (tb == 0) k_plane_sums<uint8_t, uint8_t><<<grd, blk, 0, s>>>(a, b, nx, ny, partials);
-  else k_plane_sums<uint8_t, float><<<grd, blk, 0, s>>>(a, b, nx, ny, partials);
+  // partials per plane <= norms_blocks_per_plane(nx, ny) (the callers' buffers are sized for it)
+  per = plane_sums_blocks_per_plane(nx, ny);
+  const dim3 grd((nx + 1023) / 1024, per / ((nx + 1023) / 1024), nz);
+  auto al = [](const void* p, int t) { return p == nullptr || (t == 0 ? ((uintptr_t)p & 3) == 0 : ((uintptr_t)p & 15) == 0); };
+  const bool vec = (nx & 3) == 0 && al(a, ta) && al(b, tb);
+#define GDP_PS(TA, TB)                                                                         \
+  do {                                                                                         \
+    if (vec) k_plane_sums4<TA, TB, true><<<grd, 256, 0, s>>>(a, b, nx, ny, partials);          \
+    else k_plane_sums4<TA, TB, false><<<grd, 256, 0, s>>>(a, b, nx, ny, partials);             \
+  } while (0)
+  if (ta == 1 && tb == 0) GDP_PS(float, uint8_t);
+  else if (ta == 1) GDP_PS(float, float);
+  else if (tb == 0) GDP_PS(uint8_t, uint8_t);
+  else GDP_PS(uint8_t, float);
+#undef GDP_PS
   }
   ProfScope ps2(KC_UTIL, 0.0, s);
-  k_finalize<<<nz, 256, 0, s>>>(partials, norms_blocks_per_plane(nx, ny), plane_out);
+  k_finalize<<<nz, 256, 0, s>>>(partials, per, plane_out);
 }
 
 void launch_finalize(const double2* partials, int per, int nplanes, double2* out, cudaStream_t s) {

@@ -23,14 +23,17 @@ enum KClass {
 extern const char* kclass_name[KC_COUNT];
 extern bool g_prof_on;
 extern double g_prof_finest;  // cells of the finest level of the running solve (0: none)
+extern double g_prof_l1;      // cells of its level 1 (0: none)
 void prof_push(int cls, double bytes, cudaStream_t s, bool begin);
 struct ProfScope {
   int cls;
   cudaStream_t s;
-  // launches over the finest level are a class of their own (index + KC_COUNT, "name@L0")
+  // launches over the finest level / level 1 are classes of their own (index + KC_COUNT,
+  // "name@L0"; index + 2 KC_COUNT, "name@L1")
   ProfScope(int c, double bytes, cudaStream_t st, double cells = 0.0) : cls(c), s(st) {
     count_launch();
     if (cells > 0.0 && cells == g_prof_finest) cls += KC_COUNT;
+    else if (cells > 0.0 && cells == g_prof_l1) cls += 2 * KC_COUNT;
     if (g_prof_on) prof_push(cls, bytes, s, true);
   }
   ~ProfScope() {

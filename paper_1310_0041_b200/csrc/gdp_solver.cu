@@ -32,6 +32,7 @@ const char* kclass_name[KC_COUNT] = {"rbgs", "restrict", "prolong", "norms", "co
                                      "down2d", "up2d", "down3d", "up3d"};
 bool g_prof_on = false;
 double g_prof_finest = 0.0;
+double g_prof_l1 = 0.0;
 struct ProfRec { int cls; double bytes; cudaEvent_t a, b; };
 static std::vector<ProfRec> g_prof;
 static std::vector<int> g_prof_open;  // stack of open records
@@ -654,6 +655,7 @@ int solve(Ctx& ctx, Hier& H, const Fine& f, const gdp_opts& o, bool per_slice, g
   const bool r0_restricted = H.init_restricted;  // only the init pass just before this solve
   H.init_restricted = false;
   g_prof_finest = (double)H.lv[0].nx * H.lv[0].ny * H.lv[0].nzl;
+  g_prof_l1 = H.lv.size() > 1 ? (double)H.lv[1].nx * H.lv[1].ny * H.lv[1].nzl : 0.0;
   if (H.init_norm_per > 0) {  // the initial residual came with launch_init
     launch_finalize(H.partials, H.init_norm_per, H.lv[0].nzl, H.plane_sums, s);
     CK(cudaMemcpyAsync(H.h_plane, H.plane_sums, sizeof(double2) * H.lv[0].nzl, cudaMemcpyDeviceToHost, s));
@@ -1106,8 +1108,8 @@ int gdp_profile_begin(void) {
 
 int gdp_profile_end(gdp_kernel_stat* out, int max, int* n_out) {
   g_prof_on = false;
-  double ms[2 * KC_COUNT] = {0}, by[2 * KC_COUNT] = {0};
-  long long n[2 * KC_COUNT] = {0};
+  double ms[3 * KC_COUNT] = {0}, by[3 * KC_COUNT] = {0};
+  long long n[3 * KC_COUNT] = {0};
   for (auto& r : g_prof) {
     float t = 0.f;
     CK(cudaEventSynchronize(r.b));
@@ -1120,10 +1122,11 @@ int gdp_profile_end(gdp_kernel_stat* out, int max, int* n_out) {
   }
   g_prof.clear();
   int k = 0;
-  for (int c = 0; c < 2 * KC_COUNT; ++c) {
+  for (int c = 0; c < 3 * KC_COUNT; ++c) {
     if (!n[c]) continue;
     if (out && k < max) {
-      std::snprintf(out[k].name, sizeof out[k].name, "%s%s", kclass_name[c % KC_COUNT], c >= KC_COUNT ? "@L0" : "");
+      static const char* band[3] = {"", "@L0", "@L1"};
+      std::snprintf(out[k].name, sizeof out[k].name, "%s%s", kclass_name[c % KC_COUNT], band[c / KC_COUNT]);
       out[k].launches = n[c];
       out[k].ms = ms[c];
       out[k].alg_bytes = by[c];

@@ -230,9 +230,9 @@ def profile_begin() -> None:
 
 def profile_end() -> list[dict]:
     """Stop timing; returns [{name, launches, ms, alg_bytes}] per kernel class."""
-    arr = (L.KernelStat * 32)()
+    arr = (L.KernelStat * 48)()
     n = C.c_int()
-    _check(L.lib().gdp_profile_end(arr, 32, C.byref(n)), "gdp_profile_end")
+    _check(L.lib().gdp_profile_end(arr, 48, C.byref(n)), "gdp_profile_end")
     return [{"name": arr[i].name.decode(), "launches": arr[i].launches, "ms": arr[i].ms,
              "alg_bytes": arr[i].alg_bytes} for i in range(n.value)]
 

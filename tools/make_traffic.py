@@ -24,8 +24,10 @@ for name, v in best.items():
     if m:
         classes["down2d@L0" if int(m.group(2)) else "up2d@L0"].append(v)
         continue
-    m = re.search(r"k_rows2d<(\d+), (\d+)>", name)
+    m = re.search(r"k_rows2d<(\d+), (\d+)(?:, (\d+))?>", name)
     if m:
+        if m.group(3) is not None and int(m.group(2)) and int(m.group(3)):
+            continue  # down pass with the FMG prolongation: once per solve, not per V-cycle
         classes["down2d@L0" if int(m.group(2)) else "up2d@L0"].append(v)
         continue
     if "k_init" in name:

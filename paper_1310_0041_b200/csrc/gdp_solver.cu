@@ -636,7 +636,12 @@ static int fmg_start(Ctx& ctx, Hier& H, const Fine& f, const gdp_opts& o, bool r
   // the prolongation of e_2 followed by nu_post red-black sweeps (2) or nothing (3)
   const int mode = o.fmg & 3;
   const int lmin = mode == 1 ? 1 : 2;
-  for (int l = nl - 2; l >= lmin; --l) RET(run_vcycle(ctx, H, f, o, s, l, RV_PROLONG));
+  // the nested cycles take one post-smoothing sweep fewer (phase 1: V(2,1) instead of V(2,2),
+  // 0.33 ms less on config 1, final rel-res 6.2e-7 instead of 5.9e-7 after the same 3 cycles;
+  // V(1,1) saves 0.84 ms but ends at 8.1e-7, too close to the gate: tools/fmg_nu.py)
+  gdp_opts on = o;
+  on.nu_post = std::max(1, o.nu_post - 1);
+  for (int l = nl - 2; l >= lmin; --l) RET(run_vcycle(ctx, H, f, on, s, l, RV_PROLONG));
   for (int l = lmin - 1; l >= 1; --l) {
     Level& L = H.lv[l];
     Level& C = H.lv[l + 1];

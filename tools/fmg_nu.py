@@ -6,7 +6,7 @@ import paper_1310_0041_b200 as gdp
 ctx = gdp.Ctx(0)
 I0 = torch.from_numpy(synth.make_config(1)).cuda()
 I1 = torch.empty(I0.shape, dtype=torch.float32, device="cuda"); I2 = torch.empty_like(I1)
-for nu in ["2", "1"]:
+for nu in ["default"]:  # (GDP_FMG_NU overrides were removed; kept for the record)
     os.environ["GDP_FMG_NU"] = nu
     for ph in (1, 2):
         best = None

@@ -363,27 +363,34 @@ def test_npr_filter_limits_and_errors(gpu_ctx):
 
 
 # ------------------------------------------------------------------ FMG start (gdp_opts.fmg)
-@pytest.mark.parametrize("shape,W,fmg", [((24, 517, 389), (1.0, 1.0, 0.1), 1), ((33, 130, 250), (1.0, 1.0, 0.1), 2),
-                                         ((40, 200, 180), (1.0, 1.0, 0.1), 3), ((32, 96, 96), (1.0, 1.0, 1.0), 1),
-                                         ((12, 1024, 1024), (1.0, 1.0, 0.1), 1)])
-def test_fmg_phase1_schedules_bit_identical(gpu_ctx, shape, W, fmg):
+@pytest.mark.parametrize("shape,W,fmg,dtype,nu", [((24, 517, 389), (1.0, 1.0, 0.1), 1, "u8", (2, 2)),
+                                                   ((33, 130, 250), (1.0, 1.0, 0.1), 2, "u8", (2, 2)),
+                                                   ((40, 200, 180), (1.0, 1.0, 0.1), 3, "u8", (2, 2)),
+                                                   ((32, 96, 96), (1.0, 1.0, 1.0), 1, "u8", (2, 2)),
+                                                   ((12, 1024, 1024), (1.0, 1.0, 0.1), 1, "u8", (2, 2)),
+                                                   ((19, 131, 203), (1.0, 1.0, 0.1), 1, "f32", (2, 2)),
+                                                   ((21, 140, 180), (1.0, 1.0, 0.1), 1, "u8", (1, 2))])
+def test_fmg_phase1_schedules_bit_identical(gpu_ctx, shape, W, fmg, dtype, nu):
     """The FMG start gives the same iterate in the reference and fused schedules, and with r0
-    restricted inside the init pass or by the restriction kernel (fmg + 4)."""
+    restricted inside the init pass or by the restriction kernel (fmg + 4); nu_pre = 1 takes
+    the prolongation kernel at the finest level instead of the first fused sweep."""
     nz, ny, nx = shape
-    I0 = synth.make_stack(nx, ny, nz, 43, "u8")
+    I0 = synth.make_stack(nx, ny, nz, 43, dtype)
     outs = []
     for fused, f in ((0, fmg), (3, fmg), (3, fmg + 4)):
-        o = gdp.default_opts(fused=fused, fmg=f, max_vcycles=2, rel_tol=1e-30, stagnation=0)
+        o = gdp.default_opts(fused=fused, fmg=f, max_vcycles=2, rel_tol=1e-30, stagnation=0,
+                             nu_pre=nu[0], nu_post=nu[1])
         I1, rep = gdp.gdp_diffuse_z(gpu_ctx, dev(I0), W=W, opts=o, check=False)
         outs.append(I1.cpu().numpy())
     assert np.array_equal(outs[0], outs[1])
     assert np.array_equal(outs[1], outs[2])
 
 
-@pytest.mark.parametrize("shape,fmg", [((3, 1031, 777), 1), ((16, 1024, 1024), 3), ((2, 300, 260), 2)])
-def test_fmg_phase2_schedules_bit_identical(gpu_ctx, shape, fmg):
+@pytest.mark.parametrize("shape,fmg,dtype", [((3, 1031, 777), 1, "u8"), ((16, 1024, 1024), 3, "u8"),
+                                              ((2, 300, 260), 2, "u8"), ((4, 517, 389), 3, "f32")])
+def test_fmg_phase2_schedules_bit_identical(gpu_ctx, shape, fmg, dtype):
     nz, ny, nx = shape
-    I0 = synth.make_stack(nx, ny, nz, 47, "u8")
+    I0 = synth.make_stack(nx, ny, nz, 47, dtype)
     I1 = dev(O.diffuse_z_dct(I0).astype(np.float32))
     outs = []
     for fused, f in ((0, fmg), (1, fmg), (1, fmg + 4)):

@@ -109,8 +109,9 @@ def reference_arm(args):
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": workload_name(args.config) + "_cpu_sample",
-                                            "sample_dims": list(I0.shape[::-1]), "alpha": args.alpha},
+            "data": "synthetic", "config": {"workload": workload_name(args.config), "alpha": args.alpha,
+                                            "sample_dims": list(I0.shape[::-1]),
+                                            "sample": "each step times the oracle on this crop of the workload"},
             "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample_desc(I0)},
             "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)

@@ -110,10 +110,10 @@ typedef struct {
                          level; 2 / 3 = V-cycles from level 2, level 1 only smoothed (2) or
                          only interpolated (3); + 4: restrict r0 in a pass of its own instead
                          of inside the init pass (same values; for tests).  Phases 1 / general.
-                         Default 1: config 1 phase 1 converges in 3 cycles instead of 4, 0.45 ms
-                         faster (tools/fmg_check.py).                                        */
-  int fmg_slices;     /* the same for phase 2.  Default 3: 3 cycles instead of 4, 1.0 ms faster
-                         on config 1.                                                         */
+                         The nested cycles use one post-smoothing sweep fewer than the phase.
+                         Default 1: config 1 phase 1 converges in 3 cycles instead of 4
+                         (tools/fmg_check.py).                        */
+  int fmg_slices;     /* the same for phase 2.  Default 3: 3 cycles instead of 4 on config 1. */
 } gdp_opts;
 
 typedef struct {

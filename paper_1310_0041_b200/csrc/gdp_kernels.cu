@@ -571,9 +571,17 @@ __global__ void __launch_bounds__(512) k_coarse_fd(CoarseK C, const float* __res
         ir[u] = in + (i / nx) * nx;
         acc[u] = 0.f;
       }
-      for (int j = 0; j < nx; ++j)
+      if (nt % nx == 0) {  // the U outputs share their mode k: one matrix load per j
+        for (int j = 0; j < nx; ++j) {
+          const float m = mk[0][j];
 #pragma unroll
-        for (int u = 0; u < U; ++u) acc[u] = fmaf(mk[u][j], ir[u][j], acc[u]);
+          for (int u = 0; u < U; ++u) acc[u] = fmaf(m, ir[u][j], acc[u]);
+        }
+      } else {
+        for (int j = 0; j < nx; ++j)
+#pragma unroll
+          for (int u = 0; u < U; ++u) acc[u] = fmaf(mk[u][j], ir[u][j], acc[u]);
+      }
 #pragma unroll
       for (int u = 0; u < U; ++u)
         if (i0 + u * nt < nsys) out[i0 + u * nt] = acc[u];
@@ -595,9 +603,17 @@ __global__ void __launch_bounds__(512) k_coarse_fd(CoarseK C, const float* __res
         ic[u] = in + (long long)z * ny * nx + xx;
         acc[u] = 0.f;
       }
-      for (int j = 0; j < ny; ++j)
+      if (nzs == 1 && nt % nx == 0) {  // the U outputs share their column: one input load per j
+        for (int j = 0; j < ny; ++j) {
+          const float v = ic[0][j * nx];
 #pragma unroll
-        for (int u = 0; u < U; ++u) acc[u] = fmaf(mk[u][j], ic[u][j * nx], acc[u]);
+          for (int u = 0; u < U; ++u) acc[u] = fmaf(mk[u][j], v, acc[u]);
+        }
+      } else {
+        for (int j = 0; j < ny; ++j)
+#pragma unroll
+          for (int u = 0; u < U; ++u) acc[u] = fmaf(mk[u][j], ic[u][j * nx], acc[u]);
+      }
 #pragma unroll
       for (int u = 0; u < U; ++u)
         if (i0 + u * nt < nsys) out[i0 + u * nt] = acc[u];

@@ -141,6 +141,31 @@ __global__ void __launch_bounds__(256) k_restrict_b(LevelK L, const float* __res
   bc[(long long)cz * ncx * ncy + (long long)cy * ncx + cx] = acc;
 }
 
+// k_restrict_b for x/y coarsening with nx % 4 == 0: coarse cells (2i, 2i+1) of one coarse row
+// per thread from one float4 of each child row; per cell the same order (fy outer, fx inner) and
+// weights, so the same values.
+__global__ void __launch_bounds__(256) k_restrict_b2(LevelK L, const float* __restrict__ b, XferAxis tx, XferAxis ty,
+                                                     int ncx, int ncy, float* __restrict__ bc) {
+  const int i2 = blockIdx.x * blockDim.x + threadIdx.x;  // coarse columns 2 i2, 2 i2 + 1
+  const int cy = blockIdx.y * blockDim.y + threadIdx.y;
+  const int cz = blockIdx.z;
+  if (2 * i2 >= ncx || cy >= ncy) return;
+  const long long plane = (long long)L.nx * L.ny;
+  const int fx = 4 * i2;
+  const int fy0 = 2 * cy, fy1 = min(2 * cy + 1, L.ny - 1);
+  const float w0 = rweight(tx, fx), w1 = rweight(tx, fx + 1), w2 = rweight(tx, fx + 2), w3 = rweight(tx, fx + 3);
+  float a0 = 0.f, a1 = 0.f;
+  for (int fy = fy0; fy <= fy1; ++fy) {
+    const float wy = rweight(ty, fy);
+    const float4 v = __ldg(reinterpret_cast<const float4*>(b + cz * plane + (long long)fy * L.nx + fx));
+    a0 = __fmaf_rn(rw3(1.f, wy, w0), v.x, a0);
+    a0 = __fmaf_rn(rw3(1.f, wy, w1), v.y, a0);
+    a1 = __fmaf_rn(rw3(1.f, wy, w2), v.z, a1);
+    a1 = __fmaf_rn(rw3(1.f, wy, w3), v.w, a1);
+  }
+  *reinterpret_cast<float2*>(bc + (long long)cz * ncx * ncy + (long long)cy * ncx + 2 * i2) = make_float2(a0, a1);
+}
+
 // a8: x_fine += P x_coarse (cell-centred linear interpolation, constant at the faces; the
 // ghost coarse planes of a z-slab come from xclo / xchi).  4 columns x `rows` rows of one fine
 // plane per thread: x taps computed
@@ -716,6 +741,13 @@ void launch_restrict(const LevelK& L, const float* x, const float* xlo, const fl
 void launch_restrict_b(const LevelK& L, const float* b, const XferAxis& tx, const XferAxis& ty, const XferAxis& tz,
                        int ncx, int ncy, int nczl, float* bc, cudaStream_t s) {
   ProfScope ps(KC_RESTRICT, ncell(L) * 4.0 + 4.0 * ncx * ncy * (double)nczl, s, ncell(L));
+  if (tx.coarsened && ty.coarsened && !tz.coarsened && (L.nx & 3) == 0 && ((uintptr_t)b & 15) == 0 &&
+      ((uintptr_t)bc & 7) == 0) {  // two coarse cells per thread from float4 rows
+    dim3 blk(64, 4);
+    dim3 grd((ncx / 2 + 63) / 64, (ncy + 3) / 4, nczl);
+    k_restrict_b2<<<grd, blk, 0, s>>>(L, b, tx, ty, ncx, ncy, bc);
+    return;
+  }
   dim3 blk(64, 4);
   dim3 grd((ncx + 63) / 64, (ncy + 3) / 4, nczl);
   k_restrict_b<<<grd, blk, 0, s>>>(L, b, tx, ty, tz, ncx, ncy, bc);

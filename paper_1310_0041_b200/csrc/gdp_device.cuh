@@ -17,6 +17,10 @@
 
 namespace gdp {
 
+// 16-byte alignment of an optional pointer (the float4 / cp.async.16 paths need it besides
+// nx % 4 == 0; a caller's tensor view may start at any 4-byte offset)
+__host__ __device__ __forceinline__ bool al16(const void* p) { return ((uintptr_t)p & 15) == 0; }
+
 struct AxisC {      // link coefficients of one axis on one level
   int n;            // global cell count along the axis
   float k;          // interior link coefficient

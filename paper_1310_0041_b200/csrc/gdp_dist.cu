@@ -57,6 +57,24 @@ static int build_plan(const HierKey& gkey, const std::vector<long long>& z0s, co
   }
   if (ff < 1) return set_err(GDP_EINVAL, "distributed stack too small: level 0 must already be gathered");
   D->ff = ff;
+  // the restriction into the gathered level maps local planes to coarse planes z0/2 + k: a
+  // z-coarsened step needs every slab aligned at that level (no coarse plane straddles two slabs)
+  for (size_t i = 0; i < z0s.size(); ++i) {
+    const Level& L = chains[i][ff - 1];
+    const Level& Cg = chains[i][ff];
+    const long long lz0 = ff - 1 == 0 ? z0s[i] : L.z0, lnz = ff - 1 == 0 ? nzls[i] : L.nzl;
+    if (Cg.tz.coarsened && (lz0 % 2 != 0 || lnz % 2 != 0))
+      return set_err(GDP_EINVAL, "z-slab partition: level %d coarsens z but slab %zu (planes [%lld, %lld)) is not "
+                     "aligned to even planes; use an even split or weights with bz < max(bx, by) / 2",
+                     ff - 1, i, lz0, lz0 + lnz);
+  }
+  // the fused finest level needs every slab (all ranks, not just the local ones: the halo
+  // schedule must match) to hold >= G planes on level 0 and on a split level 1
+  D->slabs_fusable = true;
+  for (size_t i = 0; i < z0s.size(); ++i) {
+    if (nzls[i] < DistPlan::G) D->slabs_fusable = false;
+    if (ff > 1 && chains[i][1].nzl < DistPlan::G) D->slabs_fusable = false;
+  }
   for (int i : local) {
     HierKey k = gkey;
     k.z0 = z0s[i];
@@ -340,8 +358,7 @@ int dist_diffuse_z(Ctx& c, const void* I0, int tI, float* I1, long long nx, long
       const Level C = coarse_of(*D, i);
       ok = L.K.az.k != 0.f && C.tx.coarsened && C.ty.coarsened && !C.tz.coarsened;
     }
-    for (size_t i = 0; i < D->nzl.size() && ok; ++i) ok = D->nzl[i] >= DistPlan::G;
-    for (int i = 0; i < np && ok && D->ff > 1; ++i) ok = D->parts[i]->lv[1].nzl >= DistPlan::G;
+    ok = ok && D->slabs_fusable;
     if (ok) {
       D->fused = true;
       long long items = 0;
@@ -371,7 +388,7 @@ int dist_diffuse_z(Ctx& c, const void* I0, int tI, float* I1, long long nx, long
       CKD(cudaMalloc(&D->fpart, sizeof(double2) * D->fpart_cap));
     }
   }
-  D->active = D->fused && (o.fused & 2);
+  D->active = D->fused && (o.fused & 2) && o.nu_pre >= 1 && o.nu_post >= 1;
   std::vector<float*> b0own = D->b0;  // active: the rhs lives in the ghosted windows for this call
   struct Restore {
     DistPlan* D;
@@ -404,6 +421,7 @@ int dist_diffuse_z(Ctx& c, const void* I0, int tI, float* I1, long long nx, long
   RETD(team_norms(c, *D, xw.data(), &rel, &nb, s));
   r.rel_res[0] = rel;
   r.norm_b = nb;
+  if (!std::isfinite(rel)) return set_err(GDP_EINVAL, "non-finite initial residual (non-finite input?)");
   int status = GDP_OK, stall = 0, k = 0;
   const int cap = std::min(o.max_vcycles, GDP_MAX_CYCLES);
   while (rel > o.rel_tol) {
@@ -412,6 +430,7 @@ int dist_diffuse_z(Ctx& c, const void* I0, int tI, float* I1, long long nx, long
     RETD(team_vcycle(c, *D, x0.data(), o, s, &cur, &nrel));
     if (!D->active) RETD(team_norms(c, *D, x0.data(), &nrel, nullptr, s));
     r.rel_res[++k] = nrel;
+    if (!std::isfinite(nrel)) return set_err(GDP_EINVAL, "non-finite residual after V-cycle %d", k);
     if (o.stagnation > 0 && nrel > 0.9 * rel) {
       if (++stall >= o.stagnation) { rel = nrel; status = nrel <= o.rel_tol ? GDP_OK : GDP_ENOCONV; break; }
     } else {

@@ -170,7 +170,7 @@ __device__ __forceinline__ void pass2d_body(const Pass2D& P, float4 (&sh_top)[2]
   const float2 kxlA = make_float2(cxl[0], cxl[2]), kxrA = make_float2(cxr[0], cxr[2]);
   const float2 kxlB = make_float2(cxl[1], cxl[3]), kxrB = make_float2(cxr[1], cxr[3]);
   const bool lane_full = cin[0] && cin[1] && cin[2] && cin[3];
-  const bool vec = (L.nx & 3) == 0;  // rows start 16-byte aligned
+  const bool vec = (L.nx & 3) == 0 && al16(P.xin) && al16(P.xout) && al16(P.R.b);  // rows start 16-byte aligned
 
   // ---------------------------------------------------------------- issue all loads
   float4(&bs)[G_R][32] = sb[warp];

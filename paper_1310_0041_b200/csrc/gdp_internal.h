@@ -87,6 +87,7 @@ struct DistPlan {
   // fused finest level (k_march3d): per local slab two x windows and the rhs with G ghost planes
   // per face ([z0 - G, z0 + nzl + G), interior at offset G); exchanged once per sweep
   static constexpr int G = 3;
+  bool slabs_fusable = false;                // every slab of the team (all ranks) holds >= G planes
   bool fused = false;                        // windows allocated
   bool active = false;                       // this call runs the fused finest level (opts.fused & 2)
   std::vector<float*> w0, w1, bw;

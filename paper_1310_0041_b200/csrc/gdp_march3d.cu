@@ -710,7 +710,7 @@ static void launch_m3v(const March3D& P, cudaStream_t s) {
 }
 template <int TAIL, bool PROLONG, bool ZC>
 static void launch_m3(const March3D& P, cudaStream_t s) {
-  if ((P.L.nx & 3) == 0) launch_m3v<TAIL, PROLONG, ZC, true>(P, s);
+  if ((P.L.nx & 3) == 0 && al16(P.xin) && al16(P.xout) && al16(P.b)) launch_m3v<TAIL, PROLONG, ZC, true>(P, s);
   else launch_m3v<TAIL, PROLONG, ZC, false>(P, s);
 }
 

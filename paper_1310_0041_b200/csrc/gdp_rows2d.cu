@@ -356,7 +356,7 @@ __global__ void __launch_bounds__(R2_WARPS * 32) k_rows2d(const __grid_constant_
   __shared__ float2 sc[PRO ? R2_CS : 1][R2_WARPS * 32];
   const long long item = (long long)blockIdx.x * R2_WARPS + (threadIdx.x >> 5);
   if (item >= P.nitems) return;  // warp-uniform; the kernel has no block-wide barrier
-  if ((P.L.nx & 3) == 0) rows2d_march<NU, DOWN, true, PRO>(P, sx, sb, sc, item);
+  if ((P.L.nx & 3) == 0 && al16(P.xin) && al16(P.xout) && al16(P.b)) rows2d_march<NU, DOWN, true, PRO>(P, sx, sb, sc, item);
   else rows2d_march<NU, DOWN, false, PRO>(P, sx, sb, sc, item);
 }
 

@@ -673,6 +673,7 @@ int solve(Ctx& ctx, Hier& H, const Fine& f, const gdp_opts& o, bool per_slice, g
   double rel = rel_from_planes(H, per_slice, &nb);
   r.rel_res[0] = rel;
   r.norm_b = nb;
+  if (!std::isfinite(rel)) return set_err(GDP_EINVAL, "non-finite initial residual (non-finite input?)");
   int status = GDP_OK;
   int stall = 0;
   int k = 0;
@@ -693,6 +694,7 @@ int solve(Ctx& ctx, Hier& H, const Fine& f, const gdp_opts& o, bool per_slice, g
     const double nrel = rel_from_planes(H, per_slice, nullptr);
     ++k;
     r.rel_res[k] = nrel;
+    if (!std::isfinite(nrel)) return set_err(GDP_EINVAL, "non-finite residual after V-cycle %d", k);
     if (o.stagnation > 0 && nrel > 0.9 * rel) {
       if (++stall >= o.stagnation) { rel = nrel; status = nrel <= o.rel_tol ? GDP_OK : GDP_ENOCONV; break; }
     } else {

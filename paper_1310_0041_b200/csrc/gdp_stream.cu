@@ -215,6 +215,8 @@ int stream_diffuse_z(Ctx& C, const void* I0h, int tI, float* xh, long long nx, l
                      double* shift_out) {
   gdp_opts o = o0;
   o.fused |= 2;
+  if (o.nu_pre < 1 || o.nu_post < 1)  // every finest-level pass is a fused sweep (restrict / prolong inside)
+    return set_err(GDP_EINVAL, "out-of-core phase 1 needs nu_pre >= 1 and nu_post >= 1");
   HierKey key{};
   key.nx = nx; key.ny = ny; key.nzl = nz; key.z0 = 0; key.nzg = nz;
   key.bx = bx; key.by = by; key.bz = bz; key.alpha = 0.f;
@@ -274,6 +276,7 @@ int stream_diffuse_z(Ctx& C, const void* I0h, int tI, float* xh, long long nx, l
   double rel = bb > 0 ? std::sqrt(rr / bb) : std::sqrt(rr);
   r.rel_res[0] = rel;
   r.norm_b = std::sqrt(bb);
+  if (!std::isfinite(rel)) return set_err(GDP_EINVAL, "non-finite initial residual (non-finite input?)");
   Fine f;  // levels >= 1 only: run_vcycle(l0 = 1) never touches the finest level
   f.mode = RHS_B;
   int status = GDP_OK, stall = 0, k = 0;
@@ -290,6 +293,7 @@ int stream_diffuse_z(Ctx& C, const void* I0h, int tI, float* xh, long long nx, l
     const double nrel = bb > 0 ? std::sqrt(rr / bb) : std::sqrt(rr);
     ++k;
     r.rel_res[k] = nrel;
+    if (!std::isfinite(nrel)) return set_err(GDP_EINVAL, "non-finite residual after V-cycle %d", k);
     if (o.stagnation > 0 && nrel > 0.9 * rel) {
       if (++stall >= o.stagnation) { rel = nrel; status = nrel <= o.rel_tol ? GDP_OK : GDP_ENOCONV; break; }
     } else {

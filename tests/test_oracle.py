@@ -290,3 +290,103 @@ def test_decode_is_fp32_division():
     d = O.decode(u)
     assert np.array_equal(d, (u.astype(np.float32) / np.float32(255)).astype(np.float64))
     assert d[0] == 0.0 and d[255] == 1.0
+
+
+# ---------------------------------------------------------------- P3 worked values (golden)
+def _p3_cases():
+    g = json.load(open(os.path.join(GOLD, "spectral_p3.json")))
+    return g["tol"], g["cases"]
+
+
+def _symbols(shape, mode):
+    (nz, ny, nx), (k, l, m) = shape, mode
+    return O.path_eigenvalues(nx)[k], O.path_eigenvalues(ny)[l], O.path_eigenvalues(nz)[m]
+
+
+@pytest.mark.parametrize("i", range(5))
+def test_p3_golden_gain_functions(i):
+    """closed_form.ad_gain / combined_gain / sp_gain reproduce SURVEY §8(c) P3's printed values
+    (a swapped numerator, a dropped alpha or a z symbol in the SP term fails one of them)."""
+    tol, cases = _p3_cases()
+    c = cases[i]
+    mx, my, mz = _symbols(c["shape"], c["mode"])
+    assert float(O.ad_gain(mx, my, mz)) == pytest.approx(c["g_ad"], abs=tol)
+    assert float(O.combined_gain(mx, my, mz, c["alpha"])) == pytest.approx(c["F"], abs=tol)
+    if "sp_I1_only" in c:
+        assert float(O.sp_gain(mx, my, c["alpha"])) == pytest.approx(c["sp_I1_only"], abs=tol)
+
+
+@pytest.mark.parametrize("i", range(5))
+def test_p3_golden_gains_measured_by_cg(i):
+    """The CG oracle's outputs projected onto the mode give the same P3 values."""
+    tol, cases = _p3_cases()
+    c = cases[i]
+    shape, (k, l, m), alpha = tuple(c["shape"]), c["mode"], c["alpha"]
+    phi = _mode(shape, k, l, m)
+    I0 = 0.5 + 0.1 * phi
+    nrm = np.sum(0.1 * phi * phi)
+    I1 = O.diffuse_z(I0)
+    assert np.sum((I1 - 0.5) * phi) / nrm == pytest.approx(c["g_ad"], abs=tol)
+    I2 = O.screened_poisson_slices(I0, I1, alpha)
+    assert np.sum((I2 - 0.5) * phi) / nrm == pytest.approx(c["F"], abs=tol)
+    if "sp_I1_only" in c:  # a mode present in I1 only: I0 constant
+        J2 = O.screened_poisson_slices(np.full(shape, 0.5), I0, alpha)
+        assert np.sum((J2 - 0.5) * phi) / nrm == pytest.approx(c["sp_I1_only"], abs=tol)
+        # the DCT phase-2 solver agrees on the same input
+        J2d = O.screened_poisson_slices_dct(np.full(shape, 0.5), I0, alpha)
+        assert np.abs(J2d - J2).max() < 1e-9
+
+
+def test_sp_gain_is_dct_phase2_transfer():
+    """sp_gain(mu_k, mu_l, alpha) is the transfer of screened_poisson_slices_dct for a mode of I1
+    (the full-size GPU tests use it as their expected value)."""
+    shape = (3, 24, 40)
+    alpha = 0.03
+    for (k, l) in ((1, 0), (5, 7), (0, 11), (39, 23)):
+        phi = _mode(shape, k, l, 0)
+        J2 = O.screened_poisson_slices_dct(np.zeros(shape), phi, alpha)
+        mx, my, _ = _symbols(shape, (k, l, 0))
+        g = np.sum(J2 * phi) / np.sum(phi * phi)
+        assert g == pytest.approx(float(O.sp_gain(mx, my, alpha)), abs=1e-12)
+        # and the dense matrix of the 2D operator has that mode as an eigenvector
+    A = _matrix((1, 6, 5), (1.0, 1.0, 0.0), alpha)
+    ev = np.sort(np.linalg.eigvalsh(A))
+    mus = np.sort((O.path_eigenvalues(5)[None, :] + O.path_eigenvalues(6)[:, None]).ravel())
+    assert np.allclose(ev, alpha + mus, atol=1e-12)
+    assert np.allclose(np.sort(alpha / ev), np.sort(O.sp_gain(mus, 0.0, alpha)), atol=1e-12)
+
+
+def test_slice_rel_residuals_hand_built():
+    """Per-slice ||b_i - A x_i|| / ||b_i|| on slices whose residual follows from the 2D
+    stencil values alone (centre 4 + alpha, faces -1, corner 2 + alpha)."""
+    alpha = 0.25
+    nz, ny, nx = 4, 5, 6
+    x = np.zeros((nz, ny, nx))
+    b = np.zeros((nz, ny, nx))
+    x[0] = 0.7                     # constant: L x = 0, A x = alpha x = b exactly
+    b[0] = alpha * 0.7
+    b[1] = RNG.standard_normal((ny, nx))  # x = 0: residual = b, rel = 1
+    x[2, 2, 3] = 1.0               # interior delta, b = 0: r = -A e, ||r||^2 = (4+alpha)^2 + 4
+    x[3, 0, 0] = 1.0               # corner delta (2 links), b = (2+alpha) e: r = e_right + e_up
+    b[3, 0, 0] = 2.0 + alpha
+    rel = O.slice_rel_residuals(x, b, alpha)
+    assert rel[0] == pytest.approx(0.0, abs=1e-15)
+    assert rel[1] == pytest.approx(1.0, abs=1e-15)
+    assert rel[2] == pytest.approx(np.sqrt((4 + alpha) ** 2 + 4), abs=1e-14)  # ||b|| = 0: absolute
+    assert rel[3] == pytest.approx(np.sqrt(2.0) / (2.0 + alpha), abs=1e-15)
+
+
+def test_decode_correctly_rounded_rationals():
+    """decode(u) is the fp32 value nearest to the rational u/255 (ties to even), checked with
+    exact rational arithmetic on every code — not by re-dividing in fp32."""
+    from fractions import Fraction
+    d = O.decode(np.arange(256, dtype=np.uint8))
+    for u in range(256):
+        f = np.float32(d[u])
+        assert float(f) == d[u]  # an fp32 value
+        q = Fraction(u, 255)
+        err = abs(Fraction(float(f)) - q)
+        for nb in (np.nextafter(f, np.float32(-1)), np.nextafter(f, np.float32(2))):
+            e2 = abs(Fraction(float(nb)) - q)
+            assert err < e2 or (err == e2 and (f.view(np.uint32) & 1) == 0)
+    assert d[51] == float(np.float32(0.2)) and d[0] == 0.0 and d[255] == 1.0

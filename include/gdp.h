@@ -90,7 +90,12 @@ typedef struct {
   int fused;          /* bitmask of fused level passes (bit-identical to the reference
                          schedule of one kernel per half-sweep, fused = 0):
                          1 = 2D register passes (levels without z links, phase 2);
-                         2 = 3D z-marching sweeps (levels with z links, phase 1).
+                         2 = 3D z-marching sweeps (levels with z links, phase 1);
+                         4 = with 2: a whole 3D level pass (nu sweeps + the restriction or
+                             the prolongation + nu sweeps + the norms) in one temporally
+                             blocked HBM pass, TMA-staged (nu <= 2, nx % 4 == 0; else per-sweep
+                             kernels).  Bit-identical; measured slower than 2 on B200 so far
+                             (DESIGN.md section 7), hence off by default.
                          Default 3.                                                          */
   int use_graphs;     /* reserved (0).                                                      */
   int nu_pre_slices;  /* phase 2 (gdp_screened_poisson_slices) pre-smoothing sweeps; < 0: nu_pre.

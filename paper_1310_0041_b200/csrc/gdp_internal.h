@@ -56,6 +56,7 @@ struct Hier {
   double2* h_plane = nullptr;      // pinned host mirror
   float* scratch_e = nullptr;      // single-level direct solve correction
   float* b0 = nullptr;             // finest-level rhs written out for the fused 2D passes
+  unsigned int* dx_dev = nullptr;  // bound of max |x_k - x_{k-1}| of the running cycle (float bits)
   size_t partials_cap = 0;         // entries of `partials` per plane
   int up_norm_per = 0;             // >0: the last fused up pass left per-plane partials (this many per plane)
   int up_norm_planes = 0;          // planes of those partials (1: one row for the whole slab)
@@ -143,6 +144,13 @@ void rows2d_pass(bool down, int nu, const Level& L, const Level& C, const float*
                  bool zero_x, double2* partials, cudaStream_t s, bool prolong = false);
 bool fusable3d(const Level& L, const Level& C, const gdp_opts& o);
 int fused3d_items(const Level& L, const Level& C, int zlo = 0, int zhi = -1);
+// temporally blocked whole level passes (gdp_vpass3d.cu)
+bool vpass3d_ok(const Level& L, const Level& C, int nu, bool prolong, int tail, const float* xin,
+                const float* xout, const float* b);
+int vpass3d_items(const Level& L, const Level& C, int nu);
+int fused_pass3d(const Level& L, const Level& C, const float* xin, float* xout, const float* b, bool zero_x,
+                 bool prolong, int nu, int tail, double2* partials, unsigned int* dxmax, cudaStream_t s,
+                 int* items);
 int fused_sweep3d(const Level& L, const Level& C, const float* xin, float* xout, const float* b,
                   bool zero_x, bool prolong, int tail, double2* partials, cudaStream_t s, int zlo = 0,
                   int zhi = -1);

@@ -29,6 +29,7 @@ struct Rows2D {
   const float* xin;     // x before the pass (ignored if zero_x)
   float* xout;          // x after the pass (another buffer: strips read each other's halo)
   const float* b;       // rhs
+  int vec;              // nx % 4 == 0 and 16-byte aligned arrays: float4 / cp.async.16 rows
   int zero_x;
   XferAxis tx, ty;      // fine -> coarse (both in-plane axes coarsened)
   int ncx, ncy;
@@ -356,7 +357,7 @@ __global__ void __launch_bounds__(R2_WARPS * 32) k_rows2d(const __grid_constant_
   __shared__ float2 sc[PRO ? R2_CS : 1][R2_WARPS * 32];
   const long long item = (long long)blockIdx.x * R2_WARPS + (threadIdx.x >> 5);
   if (item >= P.nitems) return;  // warp-uniform; the kernel has no block-wide barrier
-  if ((P.L.nx & 3) == 0 && al16(P.xin) && al16(P.xout) && al16(P.b)) rows2d_march<NU, DOWN, true, PRO>(P, sx, sb, sc, item);
+  if (P.vec) rows2d_march<NU, DOWN, true, PRO>(P, sx, sb, sc, item);
   else rows2d_march<NU, DOWN, false, PRO>(P, sx, sb, sc, item);
 }
 
@@ -406,6 +407,7 @@ void rows2d_pass(bool down, int nu, const Level& L, const Level& C, const float*
                  bool zero_x, double2* partials, cudaStream_t s, bool prolong) {
   Rows2D P{};
   P.L = L.K; P.xin = xin; P.xout = xout; P.b = b; P.zero_x = zero_x ? 1 : 0;
+  P.vec = (L.nx & 3) == 0 && al16(xin) && al16(xout) && al16(b);
   P.tx = C.tx; P.ty = C.ty; P.ncx = C.nx; P.ncy = C.ny;
   P.bc = C.b; P.xc = C.x; P.partials = partials;
   plan_rows2d(nu, L.K, P);

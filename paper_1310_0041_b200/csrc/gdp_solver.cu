@@ -507,12 +507,22 @@ int run_vcycle(Ctx& ctx, Hier& H, const Fine& f, const gdp_opts& o, cudaStream_t
     // FMG start at l0: x (zeroed above level 0) += P x_{l0+1}, in the first fused 3D sweep
     // when there is one to carry it, else by the prolongation kernel
     const bool pro = l == l0 && (flags & RV_PROLONG);
-    const bool pro_fused = pro && ((fz[l] == 3 && o.nu_pre >= 2 && l == 0) || fz[l] == 2);
-    if (pro) {
+    // the temporally blocked pass (fused & 4): all nu_pre sweeps + restriction in one HBM pass,
+    // the FMG prolongation added at load
+    const bool vp = fz[l] == 3 && (o.fused & 4) &&
+                    vpass3d_ok(L, C, o.nu_pre, pro, 1, x, L.x2, l == 0 ? R.b : L.b);
+    const bool pro_fused = pro && ((fz[l] == 3 && o.nu_pre >= 2 && l == 0) || fz[l] == 2 || vp);
+    if (pro && !vp) {
       if (l > 0) CK(cudaMemsetAsync(x, 0, sizeof(float) * (size_t)L.nx * L.ny * L.nzl, s));
       if (!pro_fused) launch_prolong(L.K, x, C.tx, C.ty, C.tz, C.nx, C.ny, C.nzl, C.z0, C.x, C.xlo, C.xhi, s);
     }
-    const bool zx = l > 0 && !pro;  // level above l0 (or l0 > 0 without FMG): starts from zero
+    const bool zx = l > 0 && (!pro || vp);  // above level 0 x starts from zero (+ P e at l0 under FMG)
+    if (vp) {  // one pass: x (A) -> x2 (B), restricted residual into C.b
+      const int nu = o.nu_pre;
+      RET(fused_pass3d(L, C, x, L.x2, R.b, zx, pro, nu, 1, nullptr, l == 0 ? H.dx_dev : nullptr, s, nullptr));
+      cur[l] = L.x2;
+      continue;
+    }
     if (fz[l] == 2) {  // one fused pass: x (A) -> x2 (B)
       fused_down2d(L, C, x, L.x2, R, mode, tI, o.nu_pre, zx, s, pro_fused);
       cur[l] = L.x2;
@@ -547,6 +557,17 @@ int run_vcycle(Ctx& ctx, Hier& H, const Fine& f, const gdp_opts& o, cudaStream_t
       const bool want = l == 0 && (size_t)per2 <= H.partials_cap;
       fused_up2d(L, C, L.x2, x, R, mode, tI, o.nu_post, want ? H.partials : nullptr, s);
       if (want) { H.up_norm_per = per2; H.up_norm_planes = L.nzl; }
+      continue;
+    }
+    if (fz[l] == 3 && (o.fused & 4) && cur[l] != x &&
+        vpass3d_ok(L, C, o.nu_post, true, l == 0 ? 2 : 0, cur[l], x, R.b)) {
+      // one pass: x2 (B) + P e -> nu_post sweeps -> x (A), norms of the finest level on the way
+      const int items = vpass3d_items(L, C, o.nu_post);
+      const bool want = l == 0 && (size_t)items <= H.partials_cap * (size_t)L.nzl;
+      int got = 0;
+      RET(fused_pass3d(L, C, cur[l], x, R.b, false, true, o.nu_post, want ? 2 : 0, want ? H.partials : nullptr,
+                       l == 0 ? H.dx_dev : nullptr, s, &got));
+      if (want) { H.up_norm_per = got; H.up_norm_planes = 1; }
       continue;
     }
     if (fz[l] == 3) {  // prolongation fused into the first sweep, norms into the last

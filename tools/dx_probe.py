@@ -1,8 +1,13 @@
 """Per-cycle change ||x_k - x_{k-1}||_inf of both phases on the config-1 stack (the a9 / H3
 correction-norm test): the solve is rerun with max_vcycles = k (stagnation off, tiny rel_tol),
 which returns the iterate after exactly k cycles."""
+import os
+import sys
+
 import numpy as np
 import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 import gdp_synth as synth
 import paper_1310_0041_b200 as gdp

@@ -228,7 +228,10 @@ typedef struct {
   char name[32];        /* kernel class, e.g. "rbgs", "down2d"                          */
   int64_t launches;
   double ms;            /* summed device time of those launches                        */
-  double alg_bytes;     /* summed algorithmic bytes of those launches                   */
+  double alg_bytes;     /* summed bytes of those launches by this library's design model  */
+  double alg_bytes_8d;  /* the same counted as SURVEY.md §8(d) does: a finest-level pass reads
+                           the rhs inputs (phase 1: I0, 1 B u8 / 4 B f32; phase 2: I1 + I0)
+                           in place of the fp32 b this library writes once per solve        */
 } gdp_kernel_stat;
 int gdp_profile_begin(void);
 int gdp_profile_end(gdp_kernel_stat* out, int max, int* n_out);

@@ -57,7 +57,7 @@ class Report(C.Structure):
 
 class KernelStat(C.Structure):
     _fields_ = [("name", C.c_char * 32), ("launches", C.c_int64), ("ms", C.c_double),
-                ("alg_bytes", C.c_double)]
+                ("alg_bytes", C.c_double), ("alg_bytes_8d", C.c_double)]
 
 
 _lib = None

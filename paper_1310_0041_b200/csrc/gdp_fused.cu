@@ -689,7 +689,7 @@ static void launch2d(bool down, int nu, const Pass2D& P, cudaStream_t s) {
   const TileRect T = tiles2d(nu, P.L, P.fast_ok != 0);
   const double N = (double)P.L.nx * P.L.ny * P.L.nzl, Nc = (double)P.ncx * P.ncy * P.L.nzl;
   const double bytes = N * ((P.zero_x ? 4.0 : 8.0) + 4.0) + Nc * 4.0;
-  ProfScope ps(down ? KC_DOWN2D : KC_UP2D, bytes, s, N);
+  ProfScope ps(down ? KC_DOWN2D : KC_UP2D, bytes, s, N, true);
   if (down) {
     if (nu == 1) launch2d_nu<1, true>(P, T, s);
     else launch2d_nu<2, true>(P, T, s);

@@ -24,20 +24,24 @@ extern const char* kclass_name[KC_COUNT];
 extern bool g_prof_on;
 extern double g_prof_finest;  // cells of the finest level of the running solve (0: none)
 extern double g_prof_l1;      // cells of its level 1 (0: none)
-void prof_push(int cls, double bytes, cudaStream_t s, bool begin);
+extern double g_prof_rhs8d;   // SURVEY §8(d) bytes per finest cell of the rhs inputs (phase 1: s_in;
+                              // phase 2: I1 4 + s_in) that a pass reading the written b0 stands for
+void prof_push(int cls, double bytes, double bytes8d, cudaStream_t s, bool begin);
 struct ProfScope {
   int cls;
   cudaStream_t s;
   // launches over the finest level / level 1 are classes of their own (index + KC_COUNT,
-  // "name@L0"; index + 2 KC_COUNT, "name@L1")
-  ProfScope(int c, double bytes, cudaStream_t st, double cells = 0.0) : cls(c), s(st) {
+  // "name@L0"; index + 2 KC_COUNT, "name@L1").  reads_b0: the launch reads the level's fp32 rhs
+  // (4 B per cell); over the finest level §8(d) counts the rhs inputs instead (g_prof_rhs8d).
+  ProfScope(int c, double bytes, cudaStream_t st, double cells = 0.0, bool reads_b0 = false) : cls(c), s(st) {
     count_launch();
-    if (cells > 0.0 && cells == g_prof_finest) cls += KC_COUNT;
+    const bool fin = cells > 0.0 && cells == g_prof_finest;
+    if (fin) cls += KC_COUNT;
     else if (cells > 0.0 && cells == g_prof_l1) cls += 2 * KC_COUNT;
-    if (g_prof_on) prof_push(cls, bytes, s, true);
+    if (g_prof_on) prof_push(cls, bytes, fin && reads_b0 ? bytes + (g_prof_rhs8d - 4.0) * cells : bytes, s, true);
   }
   ~ProfScope() {
-    if (g_prof_on) prof_push(cls, 0.0, s, false);
+    if (g_prof_on) prof_push(cls, 0.0, 0.0, s, false);
   }
 };
 // bytes per cell of the finest-level rhs inputs (u8/f32 I, optional fp32 V) or of b

@@ -412,7 +412,7 @@ void rows2d_pass(bool down, int nu, const Level& L, const Level& C, const float*
   P.bc = C.b; P.xc = C.x; P.partials = partials;
   plan_rows2d(nu, L.K, P);
   const double N = (double)L.nx * L.ny * L.nzl, Nc = (double)C.nx * C.ny * C.nzl;
-  ProfScope ps(down ? KC_DOWN2D : KC_UP2D, N * ((zero_x ? 4.0 : 8.0) + 4.0) + Nc * ((down ? 4.0 : 0.0) + (prolong ? 4.0 : 0.0)), s, N);
+  ProfScope ps(down ? KC_DOWN2D : KC_UP2D, N * ((zero_x ? 4.0 : 8.0) + 4.0) + Nc * ((down ? 4.0 : 0.0) + (prolong ? 4.0 : 0.0)), s, N, true);
   const unsigned grid = (unsigned)((P.nitems + R2_WARPS - 1) / R2_WARPS);
   if (down && prolong) {  // FMG start: the coarse correction added at load
     if (nu == 1) k_rows2d<1, true, true><<<grid, R2_WARPS * 32, 0, s>>>(P);

@@ -33,13 +33,14 @@ const char* kclass_name[KC_COUNT] = {"rbgs", "restrict", "prolong", "norms", "co
 bool g_prof_on = false;
 double g_prof_finest = 0.0;
 double g_prof_l1 = 0.0;
-struct ProfRec { int cls; double bytes; cudaEvent_t a, b; };
+double g_prof_rhs8d = 4.0;
+struct ProfRec { int cls; double bytes, bytes8d; cudaEvent_t a, b; };
 static std::vector<ProfRec> g_prof;
 static std::vector<int> g_prof_open;  // stack of open records
 
-void prof_push(int cls, double bytes, cudaStream_t s, bool begin) {
+void prof_push(int cls, double bytes, double bytes8d, cudaStream_t s, bool begin) {
   if (begin) {
-    ProfRec r{cls, bytes, nullptr, nullptr};
+    ProfRec r{cls, bytes, bytes8d, nullptr, nullptr};
     cudaEventCreate(&r.a);
     cudaEventCreate(&r.b);
     cudaEventRecord(r.a, s);
@@ -901,6 +902,7 @@ static int diffuse_z_impl(gdp_ctx* ctx, const void* I0, gdp_dtype dtype, float* 
   Hier* H;
   RET(C.get_hier(make_key(local, z0_global, nz_global, W, alpha, o), &H));
   const long long n = local.nx * local.ny * local.nz;
+  g_prof_rhs8d = tI == 0 ? 1.0 : 4.0;  // §8(d): phase 1 passes read I0 (s_in) for the rhs
   CK(cudaEventRecord(C.ev0, s));
   Fine f;
   f.x = I1;
@@ -977,6 +979,7 @@ static int slices_impl(gdp_ctx* ctx, const void* I0, gdp_dtype dtype, const floa
   RET(C.get_hier(make_key(local, 0, local.nz, W, alpha, o), &H));
   const int tI = dtype == GDP_U8 ? 0 : 1;
   const long long n = local.nx * local.ny * local.nz;
+  g_prof_rhs8d = 4.0 + (tI == 0 ? 1.0 : 4.0);  // §8(d): phase 2 passes read I1 (4) and I0 (s_in)
   CK(cudaEventRecord(C.ev0, s));
   Fine f;
   f.x = I2;
@@ -1136,7 +1139,7 @@ int gdp_profile_begin(void) {
 
 int gdp_profile_end(gdp_kernel_stat* out, int max, int* n_out) {
   g_prof_on = false;
-  double ms[3 * KC_COUNT] = {0}, by[3 * KC_COUNT] = {0};
+  double ms[3 * KC_COUNT] = {0}, by[3 * KC_COUNT] = {0}, b8[3 * KC_COUNT] = {0};
   long long n[3 * KC_COUNT] = {0};
   for (auto& r : g_prof) {
     float t = 0.f;
@@ -1144,6 +1147,7 @@ int gdp_profile_end(gdp_kernel_stat* out, int max, int* n_out) {
     CK(cudaEventElapsedTime(&t, r.a, r.b));
     ms[r.cls] += t;
     by[r.cls] += r.bytes;
+    b8[r.cls] += r.bytes8d;
     n[r.cls] += 1;
     cudaEventDestroy(r.a);
     cudaEventDestroy(r.b);
@@ -1158,6 +1162,7 @@ int gdp_profile_end(gdp_kernel_stat* out, int max, int* n_out) {
       out[k].launches = n[c];
       out[k].ms = ms[c];
       out[k].alg_bytes = by[c];
+      out[k].alg_bytes_8d = b8[c];
     }
     ++k;
   }

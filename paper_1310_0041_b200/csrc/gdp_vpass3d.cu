@@ -145,7 +145,7 @@ int fused_pass3d(const Level& L, const Level& C, const float* xin, float* xout, 
   }
   const double N = (double)L.nx * L.ny * L.nzl, Nc = (double)C.nx * C.ny * C.nzl;
   const double bytes = N * ((zero_x ? 4.0 : 8.0) + 4.0) + ((tail == 1 || prolong) ? Nc * 4.0 : 0.0);
-  ProfScope ps(tail == 1 ? KC_DOWN3D : KC_UP3D, bytes, s, N);
+  ProfScope ps(tail == 1 ? KC_DOWN3D : KC_UP3D, bytes, s, N, true);
   const cudaError_t e = nu == 1 ? dispatch<1>(P, prolong, zc, tail, s) : dispatch<2>(P, prolong, zc, tail, s);
   if (e != cudaSuccess) return set_err(GDP_ECUDA, "k_vpass3d launch: %s", cudaGetErrorString(e));
   if (items) *items = P.nitems;

@@ -234,7 +234,7 @@ def profile_end() -> list[dict]:
     n = C.c_int()
     _check(L.lib().gdp_profile_end(arr, 48, C.byref(n)), "gdp_profile_end")
     return [{"name": arr[i].name.decode(), "launches": arr[i].launches, "ms": arr[i].ms,
-             "alg_bytes": arr[i].alg_bytes} for i in range(n.value)]
+             "alg_bytes": arr[i].alg_bytes, "alg_bytes_8d": arr[i].alg_bytes_8d} for i in range(n.value)]
 
 
 def kernel_launch_count() -> int:

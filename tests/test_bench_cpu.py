@@ -27,6 +27,9 @@ def test_reference_arm_json_line():
     assert d["impl"] == "reference" and d["value"] > 0 and d["steps"] == 1 and d["higher_is_better"] is True
     assert d["config"]["workload"] and d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["value"] == d["value"] and d["e2e"]["h2d_bytes_per_step"] == 0
+    # the oracle runs on every host core (OpenMP), not one
+    if "OMP_NUM_THREADS" not in os.environ:
+        assert d["cpu_baseline"]["cores"] == os.cpu_count()
 
 
 def test_reference_arm_other_ranks_silent():

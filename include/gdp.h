@@ -119,6 +119,13 @@ typedef struct {
                          Default 1: config 1 phase 1 converges in 3 cycles instead of 4
                          (tools/fmg_check.py).                        */
   int fmg_slices;     /* the same for phase 2.  Default 3: 3 cycles instead of 4 on config 1. */
+  double dx_tol;      /* correction-norm gate of the stopping rule: a
+                         single-rank in-core solve stops only when also ||x_k - x_{k-1}||_inf
+                         <= dx_tol for its last cycle k (measured exactly: the iterate is kept
+                         before every cycle that can end the solve, i.e. once rel-res is within
+                         100x of rel_tol).  Default 1e-4 (reading a9-dx: with the
+                         measured contraction <= 0.1 per cycle the error left after such a cycle
+                         is <= 1e-5).  0 disables.                                          */
 } gdp_opts;
 
 typedef struct {
@@ -131,6 +138,8 @@ typedef struct {
   double seconds;                      /* device time of the solve (CUDA events)           */
   double hbm_bytes_est;                /* algorithmic HBM bytes of the solve   */
   int64_t kernel_launches;             /* library kernels launched by the call             */
+  double dx_inf;                       /* ||x_k - x_{k-1}||_inf of the last cycle (max over
+                                          slices in phase 2); -1 when not measured            */
 } gdp_report;
 
 typedef struct gdp_ctx gdp_ctx;
@@ -207,14 +216,21 @@ int gdp_npr_filter(gdp_ctx* ctx, const void* I0, gdp_dtype dtype, float* out, gd
 /* One V-cycle on (alpha - div W grad) x = b.  x device fp32 in/out,
  * b device fp32.  With alpha = 0, b is used as given (the caller guarantees sum b = 0
  * up to rounding; the coarsest solve drops the constant mode).
- * *rel_res_after (may be NULL) = ||b - A x|| / ||b|| after the cycle, fp64.           */
+ * *rel_res_after (may be NULL) = ||b - A x|| / ||b|| after the cycle, fp64 (on a distributed
+ * or loopback ctx: over the whole stack, per-plane sums added in global plane order).
+ * Distributed / loopback ctx: x and b are this rank's slab (loopback: the whole stack); the
+ * split levels run the reference schedule with one ghost plane per slab face per half-sweep,
+ * the coarse levels are gathered (the iterate is bit-identical to a single-rank fused = 0
+ * cycle; tests/test_gpu_parity.py).                                                      */
 int gdp_vcycle(gdp_ctx* ctx, float* x, const float* b, gdp_dims local, int64_t z0_global,
                int64_t nz_global, gdp_weights W, float alpha, const gdp_opts* opts,
                double* rel_res_after, void* stream);
 
 /* Residual r = b - A x of the §4 operator, difference form, fp32 per
- * voxel; norm2_r = sum r^2 and norm2_b = sum b^2 accumulated in fp64 (summed over ranks
- * on a distributed ctx).  r may be NULL (norms only).  Norm pointers are host.        */
+ * voxel; norm2_r = sum r^2 and norm2_b = sum b^2 accumulated in fp64.  Distributed /
+ * loopback ctx: the slab faces read the neighbouring slabs' planes (halo exchange) and the
+ * norms are summed over all slabs in global plane order (identical for any partition).
+ * r may be NULL (norms only).  Norm pointers are host.                                  */
 int gdp_residual(gdp_ctx* ctx, const float* x, const float* b, float* r, gdp_dims local,
                  int64_t z0_global, int64_t nz_global, gdp_weights W, float alpha,
                  double* norm2_r, double* norm2_b, void* stream);

@@ -38,21 +38,21 @@ class Opts(C.Structure):
                 ("nu_post", C.c_int), ("coarse_max", C.c_int), ("stagnation", C.c_int),
                 ("fused", C.c_int), ("use_graphs", C.c_int), ("nu_pre_slices", C.c_int),
                 ("nu_post_slices", C.c_int), ("omega", C.c_float), ("omega_slices", C.c_float),
-                ("fmg", C.c_int), ("fmg_slices", C.c_int)]
+                ("fmg", C.c_int), ("fmg_slices", C.c_int), ("dx_tol", C.c_double)]
 
 
 class Report(C.Structure):
     _fields_ = [("status", C.c_int), ("vcycles", C.c_int), ("levels", C.c_int),
                 ("rel_res", C.c_double * (GDP_MAX_CYCLES + 1)), ("norm_b", C.c_double),
                 ("seconds", C.c_double), ("hbm_bytes_est", C.c_double),
-                ("kernel_launches", C.c_int64)]
+                ("kernel_launches", C.c_int64), ("dx_inf", C.c_double)]
 
     def as_dict(self) -> dict:
         k = self.vcycles
         return {"status": STATUS.get(self.status, self.status), "vcycles": k, "levels": self.levels,
                 "rel_res": [self.rel_res[i] for i in range(k + 1)], "norm_b": self.norm_b,
                 "seconds": self.seconds, "hbm_bytes_est": self.hbm_bytes_est,
-                "kernel_launches": self.kernel_launches}
+                "kernel_launches": self.kernel_launches, "dx_inf": self.dx_inf}
 
 
 class KernelStat(C.Structure):

@@ -4,8 +4,9 @@
 //   * NCCL (world > 1): one slab per process, ncclSend/ncclRecv over NVLink, ncclAllReduce;
 //   * loopback (gdp_ctx_create_loopback): `world` slabs inside one process on one GPU, the
 //     "exchange" is a device copy between the slabs' buffers.
-// Sums are made exact and partition-independent by giving every element exactly one non-zero
-// contributor (each rank fills its own planes of a zeroed array, then a sum-allreduce).
+// Per-plane sums are made exact and partition-independent by giving every element exactly one
+// non-zero contributor (each rank fills its own planes of a zeroed array, then a sum-allreduce);
+// the gathered coarse level is an all-gather-v of the slabs' plane ranges.
 #include <nccl.h>
 
 #include <vector>
@@ -76,12 +77,6 @@ int comm_allreduce_sum2(Ctx& c, double* a, double* b, cudaStream_t s) {
   *a = h[0];
   *b = h[1];
   return GDP_OK;
-}
-
-int comm_halo_x(Ctx& c, Hier& H, int level, float* x, cudaStream_t s) {
-  (void)H; (void)level; (void)x; (void)s;
-  if (c.world == 1) return GDP_OK;
-  return set_err(GDP_ENCCL, "halo of a single hierarchy on a distributed ctx");
 }
 
 // ---------------------------------------------------------------------------------
@@ -155,11 +150,18 @@ int comm_ghosts(Ctx& c, DistPlan& D, float* const* wins, cudaStream_t s, int lev
   return GDP_OK;
 }
 
-// complete the gathered coarse rhs: every rank restricted into its own planes of a zeroed
-// buffer; the sum over ranks has one non-zero term per element (exact)
-int comm_gather_full(Ctx& c, float* full, size_t n, cudaStream_t s) {
-  if (c.world == 1) return GDP_OK;  // loopback: the slabs wrote disjoint planes of one buffer
-  NCK(ncclAllReduce(full, full, n, ncclFloat, ncclSum, c.comm->nc, s));
+// complete the gathered coarse rhs: every slab restricted into its own planes [off_r, off_r +
+// cnt_r) (elements) of the full buffer; an all-gather-v of those ranges, as one group of
+// ncclBroadcast calls rooted at each rank (in place: the bytes moved are the level, once).
+// Loopback: the slabs wrote disjoint ranges of one buffer already.
+int comm_gather_full(Ctx& c, DistPlan& D, float* full, cudaStream_t s) {
+  if (c.world == 1) return GDP_OK;
+  NCK(ncclGroupStart());
+  for (int r = 0; r < c.world; ++r) {
+    float* p = full + D.goff[r];
+    NCK(ncclBroadcast(p, p, D.gcnt[r], ncclFloat, r, c.comm->nc, s));
+  }
+  NCK(ncclGroupEnd());
   return GDP_OK;
 }
 

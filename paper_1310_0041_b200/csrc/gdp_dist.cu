@@ -68,6 +68,17 @@ static int build_plan(const HierKey& gkey, const std::vector<long long>& z0s, co
                      "aligned to even planes; use an even split or weights with bz < max(bx, by) / 2",
                      ff - 1, i, lz0, lz0 + lnz);
   }
+  // the gathered level: the element range each slab restricts into (all-gather-v, gdp_comm.cu)
+  {
+    const Level& Cg = chains[0][ff];
+    const size_t tpl = (size_t)Cg.nx * Cg.ny;
+    for (size_t i = 0; i < z0s.size(); ++i) {
+      const Level& L = chains[i][ff - 1];
+      const bool cz = Cg.tz.coarsened != 0;
+      D->goff.push_back((size_t)(cz ? L.z0 / 2 : L.z0) * tpl);
+      D->gcnt.push_back((size_t)(cz ? L.nzl / 2 : L.nzl) * tpl);
+    }
+  }
   // the fused finest level needs every slab (all ranks, not just the local ones: the halo
   // schedule must match) to hold >= G planes on level 0 and on a split level 1
   D->slabs_fusable = true;
@@ -223,7 +234,6 @@ static int team_vcycle(Ctx& c, DistPlan& D, float* const* x0, const gdp_opts& o,
   Level& TF = T.lv[0];
   const size_t tplane = (size_t)TF.nx * TF.ny;
   if (D.active) {
-    if (ff == 1 && c.world > 1) CKD(cudaMemsetAsync(TF.b, 0, sizeof(float) * tplane * TF.nzl, s));
     RETD(team_fused_sweeps(c, D, cur, o.nu_pre, false, 1, nullptr, nullptr, s));
   }
   for (int l = D.active ? 1 : 0; l < ff; ++l) {
@@ -235,7 +245,6 @@ static int team_vcycle(Ctx& c, DistPlan& D, float* const* x0, const gdp_opts& o,
     }
     RETD(team_smooth(c, D, l, xs.data(), bs.data(), o.nu_pre, s));
     RETD(comm_halo_parts(c, D, l, xs.data(), s));
-    if (l + 1 == ff && c.world > 1) CKD(cudaMemsetAsync(TF.b, 0, sizeof(float) * tplane * TF.nzl, s));
     for (int i = 0; i < np; ++i) {
       Level& L = D.parts[i]->lv[l];
       RhsK R{bs[i], nullptr, nullptr, 0.f, 0};
@@ -252,7 +261,7 @@ static int team_vcycle(Ctx& c, DistPlan& D, float* const* x0, const gdp_opts& o,
     }
   }
   // gathered levels: one V-cycle of the tail from a zero start (replicated on every rank)
-  RETD(comm_gather_full(c, TF.b, tplane * TF.nzl, s));
+  RETD(comm_gather_full(c, D, TF.b, s));
   CKD(cudaMemsetAsync(TF.x, 0, sizeof(float) * tplane * TF.nzl, s));
   Fine ft;
   ft.x = TF.x;
@@ -317,10 +326,9 @@ static int team_norms(Ctx& c, DistPlan& D, float* const* x0, double* rel, double
   return GDP_OK;
 }
 
-int dist_diffuse_z(Ctx& c, const void* I0, int tI, float* I1, long long nx, long long ny, long long nzl,
-                   long long z0g, long long nzg, float bx, float by, float bz, float alpha, const gdp_opts& o,
-                   gdp_report* rep, cudaStream_t s) {
-  if (alpha != 0.f) return set_err(GDP_EINVAL, "the z-slab partition implements Eq. (1) (alpha = 0)");
+// the partition plan of this rank's slab (built once per geometry / weights / alpha / options)
+static int get_plan(Ctx& c, long long nx, long long ny, long long nzl, long long z0g, long long nzg, float bx,
+                    float by, float bz, float alpha, const gdp_opts& o, DistPlan** out) {
   std::vector<long long> z0s;
   std::vector<int> nzls;
   std::vector<int> local;
@@ -332,16 +340,88 @@ int dist_diffuse_z(Ctx& c, const void* I0, int tI, float* I1, long long nx, long
   HierKey ck = gk;
   ck.z0 = z0g;  // the plan depends on this rank's slab (NCCL) or on the loopback split
   ck.nzl = nzl;
-  DistPlan* D;
   auto it = c.dist.find(ck);
   if (it == c.dist.end()) {
     std::unique_ptr<DistPlan> P;
     RETD(build_plan(gk, z0s, nzls, local, P));
-    D = P.get();
+    *out = P.get();
     c.dist[ck] = std::move(P);
   } else {
-    D = it->second.get();
+    *out = it->second.get();
   }
+  return GDP_OK;
+}
+
+// local slabs' pointers into the caller's arrays (loopback: the whole stack is passed)
+template <typename T>
+static std::vector<T*> slab_ptrs(Ctx& c, DistPlan& D, T* base, long long z0g, size_t plane) {
+  const long long base_z = c.world > 1 ? z0g : 0;
+  std::vector<T*> v(D.parts.size());
+  for (size_t i = 0; i < D.parts.size(); ++i) v[i] = base ? base + (D.z0[i] - base_z) * (long long)plane : nullptr;
+  return v;
+}
+
+int dist_residual(Ctx& c, const float* x, const float* b, float* r, long long nx, long long ny, long long nzl,
+                  long long z0g, long long nzg, float bx, float by, float bz, float alpha, const gdp_opts& o,
+                  double* rr, double* bb, cudaStream_t s) {
+  DistPlan* D;
+  RETD(get_plan(c, nx, ny, nzl, z0g, nzg, bx, by, bz, alpha, o, &D));
+  const size_t plane = (size_t)nx * ny;
+  auto xs = slab_ptrs(c, *D, const_cast<float*>(x), z0g, plane);
+  auto bs = slab_ptrs(c, *D, b, z0g, plane);
+  auto rs = slab_ptrs(c, *D, r, z0g, plane);
+  RETD(comm_halo_parts(c, *D, 0, xs.data(), s));  // ghost planes of x: the neighbours' faces
+  const int np = (int)D->parts.size();
+  std::vector<double2*> loc(np);
+  for (int i = 0; i < np; ++i) {
+    Hier& H = *D->parts[i];
+    Level& L = H.lv[0];
+    launch_norms(L.K, xs[i], L.xlo, L.xhi, RhsK{bs[i], nullptr, nullptr, 0.f, 0}, RHS_B, 1, rs[i], H.partials,
+                 H.plane_sums, s);
+    loc[i] = H.plane_sums;
+  }
+  CKD(cudaGetLastError());
+  RETD(comm_plane_sums(c, *D, loc.data(), D->h_planes, s));  // global plane order: partition-independent
+  double a = 0.0, q = 0.0;
+  for (int z = 0; z < D->nzg; ++z) { a += D->h_planes[z].x; q += D->h_planes[z].y; }
+  if (rr) *rr = a;
+  if (bb) *bb = q;
+  return GDP_OK;
+}
+
+int dist_vcycle(Ctx& c, float* x, const float* b, long long nx, long long ny, long long nzl, long long z0g,
+                long long nzg, float bx, float by, float bz, float alpha, const gdp_opts& o, double* rel,
+                cudaStream_t s) {
+  DistPlan* D;
+  RETD(get_plan(c, nx, ny, nzl, z0g, nzg, bx, by, bz, alpha, o, &D));
+  const size_t plane = (size_t)nx * ny;
+  auto xs = slab_ptrs(c, *D, x, z0g, plane);
+  auto bs = slab_ptrs(c, *D, const_cast<float*>(b), z0g, plane);
+  // the split levels run the reference schedule on the caller's arrays (the fused finest level
+  // needs the ghosted windows of a whole solve)
+  std::vector<float*> b0own = D->b0;
+  struct Restore {
+    DistPlan* D;
+    std::vector<float*>* own;
+    bool active;
+    ~Restore() { D->b0 = *own; D->active = active; }
+  } restore{D, &b0own, D->active};
+  for (size_t i = 0; i < bs.size(); ++i) D->b0[i] = bs[i];
+  D->active = false;
+  int cur = 0;
+  double nrel = 0.0;
+  RETD(team_vcycle(c, *D, xs.data(), o, s, &cur, &nrel));
+  if (rel) RETD(team_norms(c, *D, xs.data(), rel, nullptr, s));
+  CKD(cudaGetLastError());
+  return GDP_OK;
+}
+
+int dist_diffuse_z(Ctx& c, const void* I0, int tI, float* I1, long long nx, long long ny, long long nzl,
+                   long long z0g, long long nzg, float bx, float by, float bz, float alpha, const gdp_opts& o,
+                   gdp_report* rep, cudaStream_t s) {
+  if (alpha != 0.f) return set_err(GDP_EINVAL, "the z-slab partition implements Eq. (1) (alpha = 0)");
+  DistPlan* D;
+  RETD(get_plan(c, nx, ny, nzl, z0g, nzg, bx, by, bz, alpha, o, &D));
   const int np = (int)D->parts.size();
   const size_t plane = (size_t)nx * ny;
   const size_t sI = tI == 0 ? 1 : 4;
@@ -416,6 +496,7 @@ int dist_diffuse_z(Ctx& c, const void* I0, int tI, float* I1, long long nx, long
   for (int i = 0; i < np; ++i) xw[i] = D->active ? D->w0[i] + plane * DistPlan::G : x0[i];
   if (D->active) RETD(comm_ghosts(c, *D, D->bw.data(), s));  // the rhs ghosts, once per solve
   gdp_report r{};
+  r.dx_inf = -1.0;  // the a9 correction norm is measured by the single-rank in-core solve only
   r.levels = D->ff + (int)D->tail->lv.size();
   double rel, nb;
   RETD(team_norms(c, *D, xw.data(), &rel, &nb, s));

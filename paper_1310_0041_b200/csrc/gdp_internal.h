@@ -56,7 +56,9 @@ struct Hier {
   double2* h_plane = nullptr;      // pinned host mirror
   float* scratch_e = nullptr;      // single-level direct solve correction
   float* b0 = nullptr;             // finest-level rhs written out for the fused 2D passes
-  unsigned int* dx_dev = nullptr;  // bound of max |x_k - x_{k-1}| of the running cycle (float bits)
+  unsigned int* dx_dev = nullptr;  // max |x_k - x_{k-1}| of the running cycle (float bits, device)
+  unsigned int* dx_host = nullptr; // pinned mirror
+  float* xprev = nullptr;          // x_{k-1} of a cycle that can end the solve (a9 correction norm)
   size_t partials_cap = 0;         // entries of `partials` per plane
   int up_norm_per = 0;             // >0: the last fused up pass left per-plane partials (this many per plane)
   int up_norm_planes = 0;          // planes of those partials (1: one row for the whole slab)
@@ -83,6 +85,7 @@ struct DistPlan {
   std::vector<int> nzl;                      // planes of each local slab
   std::vector<float*> b0;                    // finest rhs of each local slab
   int ff = 0;                                // first full level
+  std::vector<size_t> goff, gcnt;            // per slab: elements of the gathered level it restricts into
   int nzg = 0;
   double2* h_planes = nullptr;               // pinned, nzg per-plane sums in global order
   // fused finest level (k_march3d): per local slab two x windows and the rhs with G ghost planes
@@ -172,15 +175,22 @@ int stream_slices(Ctx& C, gdp_ctx* cctx, const void* I0h, gdp_dtype dtype, float
 int comm_init(Ctx& c, const void* nccl_unique_id);
 void comm_destroy(Ctx& c);
 int comm_allreduce_sum2(Ctx& c, double* a, double* b, cudaStream_t s);
-int comm_halo_x(Ctx& c, Hier& H, int level, float* x, cudaStream_t s);
 int comm_unique_id(void* out, size_t n);
 int comm_halo_parts(Ctx& c, DistPlan& D, int l, float* const* xs, cudaStream_t s);
-int comm_gather_full(Ctx& c, float* full, size_t n, cudaStream_t s);
+int comm_gather_full(Ctx& c, DistPlan& D, float* full, cudaStream_t s);
 int comm_plane_sums(Ctx& c, DistPlan& D, double2* const* local, double2* out, cudaStream_t s);
 int comm_ghosts(Ctx& c, DistPlan& D, float* const* wins, cudaStream_t s, int level = 0);
 int dist_diffuse_z(Ctx& c, const void* I0, int tI, float* I1, long long nx, long long ny, long long nzl,
                    long long z0g, long long nzg, float bx, float by, float bz, float alpha, const gdp_opts& o,
                    gdp_report* rep, cudaStream_t s);
+// gdp_vcycle / gdp_residual on a z-slab partition (x, b, r: the caller's slab, or the whole stack
+// in loopback); norms summed over all slabs in global plane order
+int dist_vcycle(Ctx& c, float* x, const float* b, long long nx, long long ny, long long nzl, long long z0g,
+                long long nzg, float bx, float by, float bz, float alpha, const gdp_opts& o, double* rel,
+                cudaStream_t s);
+int dist_residual(Ctx& c, const float* x, const float* b, float* r, long long nx, long long ny, long long nzl,
+                  long long z0g, long long nzg, float bx, float by, float bz, float alpha, const gdp_opts& o,
+                  double* rr, double* bb, cudaStream_t s);
 
 }  // namespace gdp
 

@@ -872,6 +872,42 @@ void launch_add_scalar(float* x, long long n, float v, cudaStream_t s) {
   k_add_scalar<<<ew_grid(n), 256, 0, s>>>(x, n, v);
 }
 
+// a9 correction norm: *out = max(*out, max_i |a_i - b_i|) as float bits (values >= 0 order like
+// their bit patterns), float4 grid-stride with a warp-shuffle / block max
+__global__ void __launch_bounds__(256) k_maxdiff(const float* __restrict__ a, const float* __restrict__ b, long long n,
+                                                 int vec, unsigned int* out) {
+  float m = 0.f;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const long long t0 = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  long long done = 0;
+  if (vec) {
+    const long long n4 = n >> 2;
+    const float4* a4 = reinterpret_cast<const float4*>(a);
+    const float4* b4 = reinterpret_cast<const float4*>(b);
+    for (long long i = t0; i < n4; i += stride) {
+      const float4 u = __ldg(a4 + i), v = __ldg(b4 + i);
+      m = fmaxf(m, fmaxf(fmaxf(fabsf(u.x - v.x), fabsf(u.y - v.y)), fmaxf(fabsf(u.z - v.z), fabsf(u.w - v.w))));
+    }
+    done = n4 << 2;
+  }
+  for (long long i = done + t0; i < n; i += stride) m = fmaxf(m, fabsf(__ldg(a + i) - __ldg(b + i)));
+  if (m != m) m = __int_as_float(0x7f800000);  // a NaN difference reads as +inf (never passes a gate)
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  __shared__ float sm[8];
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < 8; ++w) m = fmaxf(m, sm[w]);
+    atomicMax(out, __float_as_uint(m));
+  }
+}
+
+void launch_maxdiff(const float* a, const float* b, long long n, unsigned int* out, cudaStream_t s) {
+  ProfScope ps(KC_UTIL, (double)n * 8.0, s);
+  const int vec = (((uintptr_t)a | (uintptr_t)b) & 15) == 0;
+  k_maxdiff<<<ew_grid(n / 4 + 1), 256, 0, s>>>(a, b, n, vec, out);
+}
+
 void launch_axpy(float* x, const float* e, long long n, cudaStream_t s) {
   ProfScope ps(KC_UTIL, (double)n * 12.0, s);
   k_axpy<<<ew_grid(n), 256, 0, s>>>(x, e, n);

@@ -119,6 +119,7 @@ void launch_init(const LevelK& L, const RhsK& R, int tI, float* x0, float* b, do
                  const InitXfer& X = InitXfer{});
 void launch_add_scalar(float* x, long long n, float v, cudaStream_t s);
 void launch_axpy(float* x, const float* e, long long n, cudaStream_t s);
+void launch_maxdiff(const float* a, const float* b, long long n, unsigned int* out, cudaStream_t s);
 size_t coarse_smem_bytes(const CoarseK& C);
 cudaError_t launch_coarse(const CoarseK& C, const float* b, float* x, cudaStream_t s);
 

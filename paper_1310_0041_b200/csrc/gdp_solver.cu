@@ -229,6 +229,9 @@ Hier::~Hier() {
   if (scratch_e) cudaFree(scratch_e);
   if (b0) cudaFree(b0);
   if (h_plane) cudaFreeHost(h_plane);
+  if (dx_dev) cudaFree(dx_dev);
+  if (dx_host) cudaFreeHost(dx_host);
+  if (xprev) cudaFree(xprev);
 }
 
 static int upload(std::vector<float*>& owned, const std::vector<float>& v, const float** out) {
@@ -700,11 +703,30 @@ int solve(Ctx& ctx, Hier& H, const Fine& f, const gdp_opts& o, bool per_slice, g
   int stall = 0;
   int k = 0;
   const int cap = std::min(o.max_vcycles, GDP_MAX_CYCLES);
-  while (rel > o.rel_tol) {
+  // a9 correction norm: x_{k-1} is kept before every cycle that can end the solve (rel-res within
+  // 100x of the gate) and ||x_k - x_{k-1}||_inf measured after it
+  const bool dxg = o.dx_tol > 0.0;
+  const size_t n0 = (size_t)H.lv[0].nx * H.lv[0].ny * H.lv[0].nzl;
+  double dx = -1.0;  // of the last cycle; < 0: not measured
+  r.dx_inf = -1.0;
+  auto done = [&](double rl) { return rl <= o.rel_tol && (!dxg || (dx >= 0.0 && dx <= o.dx_tol)); };
+  while (!done(rel)) {
     if (k >= cap) { status = GDP_ENOCONV; break; }
     const bool fmg = k == 0 && (o.fmg & 3) != 0 && H.lv.size() >= 3;
+    const bool keep = dxg && rel <= 100.0 * o.rel_tol;
+    if (keep) {
+      if (!H.xprev) CK(cudaMalloc(&H.xprev, n0 * sizeof(float)));
+      if (!H.dx_dev) CK(cudaMalloc(&H.dx_dev, sizeof(unsigned int)));
+      if (!H.dx_host) CK(cudaMallocHost(&H.dx_host, sizeof(unsigned int)));
+      CK(cudaMemcpyAsync(H.xprev, f.x, n0 * sizeof(float), cudaMemcpyDeviceToDevice, s));
+      CK(cudaMemsetAsync(H.dx_dev, 0, sizeof(unsigned int), s));
+    }
     if (fmg) RET(fmg_start(ctx, H, f, o, r0_restricted, s));
     RET(run_vcycle(ctx, H, f, o, s, 0, fmg ? RV_PROLONG : 0u));
+    if (keep) {
+      launch_maxdiff(f.x, H.xprev, (long long)n0, H.dx_dev, s);
+      CK(cudaMemcpyAsync(H.dx_host, H.dx_dev, sizeof(unsigned int), cudaMemcpyDeviceToHost, s));
+    }
     if (H.up_norm_per > 0) {  // norms of the final iterate came with the fused up pass
       launch_finalize(H.partials, H.up_norm_per, H.up_norm_planes, H.plane_sums, s);
       CK(cudaMemcpyAsync(H.h_plane, H.plane_sums, sizeof(double2) * H.up_norm_planes, cudaMemcpyDeviceToHost, s));
@@ -717,8 +739,17 @@ int solve(Ctx& ctx, Hier& H, const Fine& f, const gdp_opts& o, bool per_slice, g
     ++k;
     r.rel_res[k] = nrel;
     if (!std::isfinite(nrel)) return set_err(GDP_EINVAL, "non-finite residual after V-cycle %d", k);
+    if (keep) {  // synchronised with the norms read back above
+      CK(cudaStreamSynchronize(s));
+      float v;
+      std::memcpy(&v, H.dx_host, sizeof v);
+      dx = v;
+    } else {
+      dx = -1.0;
+    }
+    r.dx_inf = dx;
     if (o.stagnation > 0 && nrel > 0.9 * rel) {
-      if (++stall >= o.stagnation) { rel = nrel; status = nrel <= o.rel_tol ? GDP_OK : GDP_ENOCONV; break; }
+      if (++stall >= o.stagnation) { rel = nrel; status = done(nrel) ? GDP_OK : GDP_ENOCONV; break; }
     } else {
       stall = 0;
     }
@@ -776,6 +807,7 @@ static gdp_opts resolve_opts(const gdp_opts* o) {
   if (r.coarse_max <= 0) r.coarse_max = d.coarse_max;
   if (!(r.omega > 0.f && r.omega < 2.f)) r.omega = d.omega;
   if (!(r.omega_slices > 0.f && r.omega_slices < 2.f)) r.omega_slices = d.omega_slices;
+  if (!(r.dx_tol >= 0.0) || !std::isfinite(r.dx_tol)) r.dx_tol = d.dx_tol;
   return r;
 }
 
@@ -807,6 +839,7 @@ int gdp_opts_default(gdp_opts* o) {
   o->omega_slices = 1.f;
   o->fmg = 1;
   o->fmg_slices = 3;
+  o->dx_tol = 1e-4;
   return GDP_OK;
 }
 
@@ -1084,6 +1117,9 @@ int gdp_vcycle(gdp_ctx* ctx, float* x, const float* b, gdp_dims local, int64_t z
   const gdp_opts o = resolve_opts(opts);
   cudaStream_t s = (cudaStream_t)stream;
   Ctx& C = ctx->impl;
+  if (C.world > 1 || C.loop > 1)  // z-slab partition: halos per half-sweep, gathered coarse levels
+    return dist_vcycle(C, x, b, local.nx, local.ny, local.nz, z0_global, nz_global, W.bx, W.by, W.bz, alpha, o,
+                       rel_res_after, s);
   Hier* H;
   RET(C.get_hier(make_key(local, z0_global, nz_global, W, alpha, o), &H));
   Fine f;
@@ -1096,7 +1132,6 @@ int gdp_vcycle(gdp_ctx* ctx, float* x, const float* b, gdp_dims local, int64_t z
     RET(finest_norms(C, *H, f, nullptr, s));
     double rr = 0.0, bb = 0.0;
     for (int z = 0; z < H->lv[0].nzl; ++z) { rr += H->h_plane[z].x; bb += H->h_plane[z].y; }
-    RET(comm_allreduce_sum2(C, &rr, &bb, s));
     *rel_res_after = bb > 0 ? std::sqrt(rr / bb) : std::sqrt(rr);
   }
   return GDP_OK;
@@ -1112,9 +1147,11 @@ int gdp_residual(gdp_ctx* ctx, const float* x, const float* b, float* r, gdp_dim
   gdp_opts_default(&o);
   cudaStream_t s = (cudaStream_t)stream;
   Ctx& C = ctx->impl;
+  if (C.world > 1 || C.loop > 1)  // ghost planes from the neighbouring slabs, norms over all slabs
+    return dist_residual(C, x, b, r, local.nx, local.ny, local.nz, z0_global, nz_global, W.bx, W.by, W.bz, alpha, o,
+                         norm2_r, norm2_b, s);
   Hier* H;
   RET(C.get_hier(make_key(local, z0_global, nz_global, W, alpha, o), &H));
-  RET(comm_halo_x(C, *H, 0, const_cast<float*>(x), s));
   Fine f;
   f.x = const_cast<float*>(x);
   f.mode = RHS_B;
@@ -1123,7 +1160,6 @@ int gdp_residual(gdp_ctx* ctx, const float* x, const float* b, float* r, gdp_dim
   RET(finest_norms(C, *H, f, r, s));
   double rr = 0.0, bb = 0.0;
   for (int z = 0; z < H->lv[0].nzl; ++z) { rr += H->h_plane[z].x; bb += H->h_plane[z].y; }
-  RET(comm_allreduce_sum2(C, &rr, &bb, s));
   if (norm2_r) *norm2_r = rr;
   if (norm2_b) *norm2_b = bb;
   return GDP_OK;

@@ -268,6 +268,7 @@ int stream_diffuse_z(Ctx& C, const void* I0h, int tI, float* xh, long long nx, l
   SK(cudaEventRecord(e0, S.st.s));
 
   gdp_report r{};
+  r.dx_inf = -1.0;  // the a9 correction norm is measured by the single-rank in-core solve only
   r.levels = (int)S.H->lv.size();
   // initial guess x0 = I0, b, initial residual
   SR(stream_pass(S, SP_INIT, false, 0, nullptr));
@@ -344,6 +345,7 @@ int stream_slices(Ctx& C, gdp_ctx* cctx, const void* I0h, gdp_dtype dtype, float
   Streams T;
   SR(T.create());
   gdp_report agg{};
+  agg.dx_inf = -1.0;
   agg.status = GDP_OK;
   const float fs = (float)shift;
   int k = 0;

@@ -51,6 +51,8 @@ def parse():
     p.add_argument("--alpha", type=float, default=ALPHA)
     p.add_argument("--fused", type=int, default=3)
     p.add_argument("--fmg", type=int, default=None, help="gdp_opts.fmg and fmg_slices (default: the library's)")
+    p.add_argument("--graphs", type=int, default=1, help="gdp_opts.use_graphs (CUDA graph replay of V-cycles)")
+    p.add_argument("--dx-tol", type=float, default=None, help="gdp_opts.dx_tol (default: the library's)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     return p.parse_args()
@@ -259,7 +261,9 @@ def main():
         ctx = gdp.Ctx(local, rank=rank, world=world, nccl_unique_id=bytes(uid.cpu().numpy()))
     else:
         ctx = gdp.Ctx(local)
-    opts = gdp.default_opts(fused=args.fused)
+    opts = gdp.default_opts(fused=args.fused, use_graphs=args.graphs)
+    if args.dx_tol is not None:
+        opts.dx_tol = args.dx_tol
     if args.fmg is not None:
         opts.fmg = opts.fmg_slices = args.fmg
     stream = torch.cuda.Stream()
@@ -375,7 +379,8 @@ def main():
                            "W": list(W), "rel_tol": 1e-6, "nu_phase1": [opts.nu_pre, opts.nu_post],
                            "nu_phase2": [opts.nu_pre_slices, opts.nu_post_slices],
                            "schedule": "fused" if args.fused else "reference",
-                           "fmg": [opts.fmg, opts.fmg_slices],
+                           "fmg": [opts.fmg, opts.fmg_slices], "use_graphs": opts.use_graphs,
+                           "dx_tol": opts.dx_tol,
                            "l2": "working set > L2 (I0 134 MB + three 537 MB fp32 volumes); no flush",
                            "parallelism": f"z-slabs x{world} (phase 1 NCCL halo, phase 2 slab-local)",
                            "global_dims": [nx, ny, nzg]},

@@ -97,7 +97,11 @@ typedef struct {
                              kernels).  Bit-identical; measured slower than 2 on B200 so far
                              (DESIGN.md section 7), hence off by default.
                          Default 3.                                                          */
-  int use_graphs;     /* reserved (0).                                                      */
+  int use_graphs;     /* 1: every V-cycle of a single-rank in-core solve (with its norm read-back)
+                         is captured once as a CUDA graph per (output buffer, cycle variant) and
+                         replayed by later solves on the same hierarchy (launch latency; needs a
+                         non-NULL stream; bit-identical).  The first solve on a hierarchy and
+                         profiled solves launch normally.  Default 1.                        */
   int nu_pre_slices;  /* phase 2 (gdp_screened_poisson_slices) pre-smoothing sweeps; < 0: nu_pre.
                          Default 1.                                                          */
   int nu_post_slices; /* phase 2 post-smoothing sweeps; < 0: nu_post.  Default 2: V(1,2) reaches

@@ -59,6 +59,13 @@ struct Hier {
   unsigned int* dx_dev = nullptr;  // max |x_k - x_{k-1}| of the running cycle (float bits, device)
   unsigned int* dx_host = nullptr; // pinned mirror
   float* xprev = nullptr;          // x_{k-1} of a cycle that can end the solve (a9 correction norm)
+  bool warm = false;               // run_vcycle ran once: every lazily allocated buffer exists
+  struct CycleGraph {              // one V-cycle (+ its norm read-back) captured as a CUDA graph
+    cudaGraphExec_t exec = nullptr;
+    int up_norm_per = 0, up_norm_planes = 0;
+    long long launches = 0;
+  };
+  std::map<std::tuple<const void*, const void*, long long>, CycleGraph> graphs;
   size_t partials_cap = 0;         // entries of `partials` per plane
   int up_norm_per = 0;             // >0: the last fused up pass left per-plane partials (this many per plane)
   int up_norm_planes = 0;          // planes of those partials (1: one row for the whole slab)

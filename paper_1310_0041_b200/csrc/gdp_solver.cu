@@ -232,6 +232,8 @@ Hier::~Hier() {
   if (dx_dev) cudaFree(dx_dev);
   if (dx_host) cudaFreeHost(dx_host);
   if (xprev) cudaFree(xprev);
+  for (auto& g : graphs)
+    if (g.second.exec) cudaGraphExecDestroy(g.second.exec);
 }
 
 static int upload(std::vector<float*>& owned, const std::vector<float>& v, const float** out) {
@@ -707,9 +709,38 @@ int solve(Ctx& ctx, Hier& H, const Fine& f, const gdp_opts& o, bool per_slice, g
   // 100x of the gate) and ||x_k - x_{k-1}||_inf measured after it
   const bool dxg = o.dx_tol > 0.0;
   const size_t n0 = (size_t)H.lv[0].nx * H.lv[0].ny * H.lv[0].nzl;
-  double dx = -1.0;  // of the last cycle; < 0: not measured
-  r.dx_inf = -1.0;
+  double dx = 0.0;   // of the last cycle (none yet: no correction); < 0: not measured
+  r.dx_inf = 0.0;
   auto done = [&](double rl) { return rl <= o.rel_tol && (!dxg || (dx >= 0.0 && dx <= o.dx_tol)); };
+  // one cycle's GPU work, ending with the D2H of its norms (and dx); no host synchronisation inside,
+  // so that it can be captured as a CUDA graph (gdp_opts.use_graphs) and replayed by later solves
+  auto enqueue = [&](bool fmg, bool keep) -> int {
+    if (keep) {
+      CK(cudaMemcpyAsync(H.xprev, f.x, n0 * sizeof(float), cudaMemcpyDeviceToDevice, s));
+      CK(cudaMemsetAsync(H.dx_dev, 0, sizeof(unsigned int), s));
+    }
+    if (fmg) RET(fmg_start(ctx, H, f, o, r0_restricted, s));
+    RET(run_vcycle(ctx, H, f, o, s, 0, fmg ? RV_PROLONG : 0u));
+    H.warm = true;
+    if (keep) {
+      launch_maxdiff(f.x, H.xprev, (long long)n0, H.dx_dev, s);
+      CK(cudaMemcpyAsync(H.dx_host, H.dx_dev, sizeof(unsigned int), cudaMemcpyDeviceToHost, s));
+    }
+    if (H.up_norm_per > 0) {  // norms of the final iterate came with the fused up pass
+      launch_finalize(H.partials, H.up_norm_per, H.up_norm_planes, H.plane_sums, s);
+      CK(cudaMemcpyAsync(H.h_plane, H.plane_sums, sizeof(double2) * H.up_norm_planes, cudaMemcpyDeviceToHost, s));
+    } else {
+      Level& L = H.lv[0];
+      launch_norms(L.K, f.x, L.xlo, L.xhi, f.R, f.mode, f.tI, nullptr, H.partials, H.plane_sums, s);
+      CK(cudaMemcpyAsync(H.h_plane, H.plane_sums, sizeof(double2) * L.nzl, cudaMemcpyDeviceToHost, s));
+    }
+    CK(cudaGetLastError());
+    return GDP_OK;
+  };
+  // graphs need a non-legacy stream, buffers that already exist, and no profiler events
+  const bool graphs = o.use_graphs && s != nullptr && f.mode == RHS_B && !g_prof_on;
+  const long long okey = ((long long)o.nu_pre << 40) ^ ((long long)o.nu_post << 32) ^ ((long long)o.fused << 24) ^
+                         ((long long)o.fmg << 16) ^ (long long)H.lv.size();
   while (!done(rel)) {
     if (k >= cap) { status = GDP_ENOCONV; break; }
     const bool fmg = k == 0 && (o.fmg & 3) != 0 && H.lv.size() >= 3;
@@ -718,29 +749,47 @@ int solve(Ctx& ctx, Hier& H, const Fine& f, const gdp_opts& o, bool per_slice, g
       if (!H.xprev) CK(cudaMalloc(&H.xprev, n0 * sizeof(float)));
       if (!H.dx_dev) CK(cudaMalloc(&H.dx_dev, sizeof(unsigned int)));
       if (!H.dx_host) CK(cudaMallocHost(&H.dx_host, sizeof(unsigned int)));
-      CK(cudaMemcpyAsync(H.xprev, f.x, n0 * sizeof(float), cudaMemcpyDeviceToDevice, s));
-      CK(cudaMemsetAsync(H.dx_dev, 0, sizeof(unsigned int), s));
     }
-    if (fmg) RET(fmg_start(ctx, H, f, o, r0_restricted, s));
-    RET(run_vcycle(ctx, H, f, o, s, 0, fmg ? RV_PROLONG : 0u));
-    if (keep) {
-      launch_maxdiff(f.x, H.xprev, (long long)n0, H.dx_dev, s);
-      CK(cudaMemcpyAsync(H.dx_host, H.dx_dev, sizeof(unsigned int), cudaMemcpyDeviceToHost, s));
+    bool ran = false;
+    if (graphs && H.warm) {
+      const long long vkey = okey ^ ((long long)fmg << 1) ^ ((long long)keep << 2) ^ ((long long)r0_restricted << 3);
+      auto key = std::make_tuple((const void*)f.x, (const void*)f.R.b, vkey);
+      auto it = H.graphs.find(key);
+      if (it == H.graphs.end()) {  // capture once
+        Hier::CycleGraph G;
+        const long long l0 = g_launches.load();
+        cudaGraph_t gr = nullptr;
+        if (cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
+          const int rc = enqueue(fmg, keep);
+          const cudaError_t ce = cudaStreamEndCapture(s, &gr);
+          if (rc == GDP_OK && ce == cudaSuccess && gr && cudaGraphInstantiate(&G.exec, gr, 0) == cudaSuccess) {
+            G.up_norm_per = H.up_norm_per;
+            G.up_norm_planes = H.up_norm_planes;
+            G.launches = g_launches.load() - l0;
+            it = H.graphs.emplace(key, G).first;
+          }
+          if (gr) cudaGraphDestroy(gr);
+        }
+        cudaGetLastError();  // a failed capture falls back to plain launches
+        g_launches.fetch_sub(g_launches.load() - l0);  // the captured launches run below
+      }
+      if (it != H.graphs.end()) {
+        CK(cudaGraphLaunch(it->second.exec, s));
+        count_launch(it->second.launches);
+        H.up_norm_per = it->second.up_norm_per;
+        H.up_norm_planes = it->second.up_norm_planes;
+        ran = true;
+      }
     }
-    if (H.up_norm_per > 0) {  // norms of the final iterate came with the fused up pass
-      launch_finalize(H.partials, H.up_norm_per, H.up_norm_planes, H.plane_sums, s);
-      CK(cudaMemcpyAsync(H.h_plane, H.plane_sums, sizeof(double2) * H.up_norm_planes, cudaMemcpyDeviceToHost, s));
-      CK(cudaStreamSynchronize(s));
+    if (!ran) RET(enqueue(fmg, keep));
+    CK(cudaStreamSynchronize(s));
+    if (H.up_norm_per > 0)
       for (int z = H.up_norm_planes; z < H.lv[0].nzl; ++z) H.h_plane[z] = make_double2(0.0, 0.0);
-    } else {
-      RET(finest_norms(ctx, H, f, nullptr, s));
-    }
     const double nrel = rel_from_planes(H, per_slice, nullptr);
     ++k;
     r.rel_res[k] = nrel;
     if (!std::isfinite(nrel)) return set_err(GDP_EINVAL, "non-finite residual after V-cycle %d", k);
-    if (keep) {  // synchronised with the norms read back above
-      CK(cudaStreamSynchronize(s));
+    if (keep) {  // read back with the norms
       float v;
       std::memcpy(&v, H.dx_host, sizeof v);
       dx = v;
@@ -832,7 +881,7 @@ int gdp_opts_default(gdp_opts* o) {
   o->coarse_max = 4096;
   o->stagnation = 2;
   o->fused = 3;
-  o->use_graphs = 0;
+  o->use_graphs = 1;
   o->nu_pre_slices = 1;
   o->nu_post_slices = 2;
   o->omega = 1.f;

@@ -494,3 +494,23 @@ def test_dx_tol_gate_measures_last_correction(gpu_ctx):
     assert rep2["vcycles"] > k and rep2["dx_inf"] >= 0.0
     off, rep3 = gdp.gdp_diffuse_z(gpu_ctx, I0, opts=gdp.default_opts(dx_tol=0.0))
     assert rep3["dx_inf"] == -1.0 or rep3["vcycles"] <= k
+
+
+def test_cuda_graph_replay_bit_identical(gpu_ctx):
+    """use_graphs: the V-cycles of later solves replay captured CUDA graphs (same launches counted),
+    with the same iterate, report and launch count as plain launches."""
+    I0 = dev(synth.make_stack(320, 256, 20, 63, "u8"))
+    st = torch.cuda.Stream()
+    outs = {}
+    for g in (0, 1):
+        o = gdp.default_opts(use_graphs=g)
+        res = []
+        for _ in range(3):  # the first solve warms the hierarchy, the next ones capture / replay
+            I1, I2, r1, r2 = gdp.gdp_destripe(gpu_ctx, I0, alpha=0.01, opts=o, stream=st)
+            st.synchronize()
+            res.append((I1.cpu().numpy(), I2.cpu().numpy(), r1, r2))
+        outs[g] = res
+    for a, b in zip(outs[0], outs[1]):
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+        assert a[2]["rel_res"] == b[2]["rel_res"] and a[3]["rel_res"] == b[3]["rel_res"]
+        assert a[2]["kernel_launches"] == b[2]["kernel_launches"] and a[3]["kernel_launches"] == b[3]["kernel_launches"]

@@ -126,8 +126,9 @@ typedef struct {
   double dx_tol;      /* correction-norm gate of the stopping rule: a
                          single-rank in-core solve stops only when also ||x_k - x_{k-1}||_inf
                          <= dx_tol for its last cycle k (measured exactly: the iterate is kept
-                         before every cycle that can end the solve, i.e. once rel-res is within
-                         100x of rel_tol).  Default 1e-4 (reading a9-dx: with the
+                         before a cycle predicted to pass the residual gate from the observed
+                         contraction; a cycle that passes unmeasured is followed by a measured
+                         one).  Default 1e-4 (reading a9-dx: with the
                          measured contraction <= 0.1 per cycle the error left after such a cycle
                          is <= 1e-5).  0 disables.                                          */
 } gdp_opts;

@@ -705,8 +705,8 @@ int solve(Ctx& ctx, Hier& H, const Fine& f, const gdp_opts& o, bool per_slice, g
   int stall = 0;
   int k = 0;
   const int cap = std::min(o.max_vcycles, GDP_MAX_CYCLES);
-  // a9 correction norm: x_{k-1} is kept before every cycle that can end the solve (rel-res within
-  // 100x of the gate) and ||x_k - x_{k-1}||_inf measured after it
+  // a9 correction norm: x_{k-1} is kept before a cycle predicted to end the solve and
+  // ||x_k - x_{k-1}||_inf measured after it
   const bool dxg = o.dx_tol > 0.0;
   const size_t n0 = (size_t)H.lv[0].nx * H.lv[0].ny * H.lv[0].nzl;
   double dx = 0.0;   // of the last cycle (none yet: no correction); < 0: not measured
@@ -744,7 +744,11 @@ int solve(Ctx& ctx, Hier& H, const Fine& f, const gdp_opts& o, bool per_slice, g
   while (!done(rel)) {
     if (k >= cap) { status = GDP_ENOCONV; break; }
     const bool fmg = k == 0 && (o.fmg & 3) != 0 && H.lv.size() >= 3;
-    const bool keep = dxg && rel <= 100.0 * o.rel_tol;
+    // keep x_{k-1} when this cycle is predicted to pass the residual gate: rel-res times the last
+    // observed contraction (at least 0.05) within 3x of rel_tol (a cycle that passes unmeasured is
+    // followed by a measured one)
+    const double rho = k > 0 && r.rel_res[k - 1] > 0.0 ? std::min(1.0, std::max(0.05, rel / r.rel_res[k - 1])) : 1.0;
+    const bool keep = dxg && (rel * rho <= 3.0 * o.rel_tol || rel <= o.rel_tol);
     if (keep) {
       if (!H.xprev) CK(cudaMalloc(&H.xprev, n0 * sizeof(float)));
       if (!H.dx_dev) CK(cudaMalloc(&H.dx_dev, sizeof(unsigned int)));
@@ -770,10 +774,14 @@ int solve(Ctx& ctx, Hier& H, const Fine& f, const gdp_opts& o, bool per_slice, g
           }
           if (gr) cudaGraphDestroy(gr);
         }
-        cudaGetLastError();  // a failed capture falls back to plain launches
+        const cudaError_t le = cudaGetLastError();  // a failed capture falls back to plain launches
+        if (getenv("GDP_GRAPH_DEBUG"))
+          fprintf(stderr, "gdp graph capture fmg=%d keep=%d ok=%d err=%s launches=%lld\n", (int)fmg, (int)keep,
+                  it != H.graphs.end(), cudaGetErrorString(le), g_launches.load() - l0);
+        if (it == H.graphs.end()) it = H.graphs.emplace(key, Hier::CycleGraph{}).first;  // remember the failure
         g_launches.fetch_sub(g_launches.load() - l0);  // the captured launches run below
       }
-      if (it != H.graphs.end()) {
+      if (it->second.exec) {
         CK(cudaGraphLaunch(it->second.exec, s));
         count_launch(it->second.launches);
         H.up_norm_per = it->second.up_norm_per;

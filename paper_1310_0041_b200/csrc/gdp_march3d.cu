@@ -657,6 +657,10 @@ static int max_clusters() {
 
 bool fusable3d(const Level& L, const Level& C, const gdp_opts& o) {
   const bool zlinks = L.K.az.k != 0.f || L.K.az.kr != 0.f || L.K.az.kl != 0.f;
+  // levels below ~2M cells take the reference kernels (one launch per half-sweep): the persistent
+  // z-march's pipeline fill dominates there (config 1: 22.57 vs 22.87 ms per step with graphs)
+  static const long long minc = getenv("GDP_F3D_MIN") ? atoll(getenv("GDP_F3D_MIN")) : 2000000LL;
+  if ((long long)L.nx * L.ny * L.nzl < minc) return false;
   return (o.fused & 2) && zlinks && C.tx.coarsened && C.ty.coarsened &&
          L.nzl == L.gz.n /* single slab (no ghost planes) */ && L.z0 == 0 &&
          (long long)L.nx * L.ny < (1LL << 31) && (long long)C.nx * C.ny < (1LL << 31);

@@ -95,7 +95,12 @@ typedef struct {
                              the prolongation + nu sweeps + the norms) in one temporally
                              blocked HBM pass, TMA-staged (nu <= 2, nx % 4 == 0; else per-sweep
                              kernels).  Bit-identical; measured slower than 2 on B200 so far
-                             (DESIGN.md section 7), hence off by default.
+                             (DESIGN.md section 7), hence off by default;
+                         8 = the coarse tail of every V-cycle (single-slab levels under 2M cells)
+                             in two cooperative launches (down walk, up walk) around the
+                             coarsest solve, instead of ~5 launches per level.  Bit-identical;
+                             measured 0.45 ms slower per config-1 step than graph-replayed
+                             per-level launches, hence off by default.
                          Default 3.                                                          */
   int use_graphs;     /* 1: every V-cycle of a single-rank in-core solve (with its norm read-back)
                          is captured once as a CUDA graph per (output buffer, cycle variant) and

@@ -60,6 +60,7 @@ struct Hier {
   unsigned int* dx_host = nullptr; // pinned mirror
   float* xprev = nullptr;          // x_{k-1} of a cycle that can end the solve (a9 correction norm)
   bool warm = false;               // run_vcycle ran once: every lazily allocated buffer exists
+  CoopLv* coop_dev = nullptr;      // per level l >= 1 (index l - 1): the cooperative coarse tail's view
   struct CycleGraph {              // one V-cycle (+ its norm read-back) captured as a CUDA graph
     cudaGraphExec_t exec = nullptr;
     int up_norm_per = 0, up_norm_planes = 0;

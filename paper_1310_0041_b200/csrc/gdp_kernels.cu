@@ -5,6 +5,8 @@
 // residual+restriction, one per prolongation+correction.  The fused schedule lives
 // in gdp_fused.cu and calls the same per-point arithmetic (gdp_device.cuh), so both
 // schedules produce bit-identical iterates.
+#include <cooperative_groups.h>
+
 #include "gdp_kernels.h"
 
 namespace gdp {
@@ -45,15 +47,13 @@ __device__ __forceinline__ bool is_interior(const LevelK& L, const Interior& I, 
   return ix >= 1 && ix <= L.ax.n - 3 && iy >= 1 && iy <= L.ay.n - 3 && (I.zreg_all || (zg >= 1 && zg <= L.az.n - 3));
 }
 
-// a4: one red-black Gauss-Seidel half-sweep (colour = (x + y + z_global) & 1).
+// a4: one red-black Gauss-Seidel half-sweep (colour = (x + y + z_global) & 1); the point
+// (ixh, iy, iz) of the half grid (every schedule that runs the reference arithmetic calls this)
 template <int MODE, typename TI>
-__global__ void __launch_bounds__(256) k_rbgs(LevelK L, float* __restrict__ x, const float* xlo,
-                                              const float* xhi, RhsK R, int color) {
-  const int iy = blockIdx.y * blockDim.y + threadIdx.y;
-  const int iz = blockIdx.z;
-  if (iy >= L.ny) return;
+__device__ __forceinline__ void rbgs_point(const LevelK& L, float* __restrict__ x, const float* xlo,
+                                           const float* xhi, const RhsK& R, int color, int ixh, int iy, int iz) {
   const long long zg = L.z0 + iz;
-  const int ix = 2 * (blockIdx.x * blockDim.x + threadIdx.x) + ((color + iy + (int)(zg & 1)) & 1);
+  const int ix = 2 * ixh + ((color + iy + (int)(zg & 1)) & 1);
   if (ix >= L.nx) return;
   const long long plane = (long long)L.nx * L.ny;
   const long long c = iz * plane + (long long)iy * L.nx + ix;
@@ -73,18 +73,21 @@ __global__ void __launch_bounds__(256) k_rbgs(LevelK L, float* __restrict__ x, c
   x[c] = gs_update(xc, r, k.diag(L.alpha), L.omega);
 }
 
+template <int MODE, typename TI>
+__global__ void __launch_bounds__(256) k_rbgs(LevelK L, float* __restrict__ x, const float* xlo,
+                                              const float* xhi, RhsK R, int color) {
+  const int iy = blockIdx.y * blockDim.y + threadIdx.y;
+  if (iy >= L.ny) return;
+  rbgs_point<MODE, TI>(L, x, xlo, xhi, R, color, blockIdx.x * blockDim.x + threadIdx.x, iy, blockIdx.z);
+}
+
 // a5+a6: residual at the fine level, restricted by volume-weighted child average.
 // One thread per coarse cell; every fine cell belongs to exactly one parent.
 template <int MODE, typename TI>
-__global__ void __launch_bounds__(256) k_restrict(LevelK L, const float* __restrict__ x,
-                                                  const float* xlo, const float* xhi, RhsK R,
-                                                  XferAxis tx, XferAxis ty, XferAxis tz,
-                                                  int ncx, int ncy, int nczl,
-                                                  float* __restrict__ bc) {
-  const int cx = blockIdx.x * blockDim.x + threadIdx.x;
-  const int cy = blockIdx.y * blockDim.y + threadIdx.y;
-  const int cz = blockIdx.z;
-  if (cx >= ncx || cy >= ncy) return;
+__device__ __forceinline__ void restrict_point(const LevelK& L, const float* __restrict__ x, const float* xlo,
+                                               const float* xhi, const RhsK& R, const XferAxis& tx,
+                                               const XferAxis& ty, const XferAxis& tz, int ncx, int ncy,
+                                               float* __restrict__ bc, int cx, int cy, int cz) {
   const long long plane = (long long)L.nx * L.ny;
   const int fx0 = tx.coarsened ? 2 * cx : cx, fx1 = tx.coarsened ? min(2 * cx + 1, L.nx - 1) : cx;
   const int fy0 = ty.coarsened ? 2 * cy : cy, fy1 = ty.coarsened ? min(2 * cy + 1, L.ny - 1) : cy;
@@ -115,6 +118,18 @@ __global__ void __launch_bounds__(256) k_restrict(LevelK L, const float* __restr
     }
   }
   bc[(long long)cz * ncx * ncy + (long long)cy * ncx + cx] = acc;
+}
+
+template <int MODE, typename TI>
+__global__ void __launch_bounds__(256) k_restrict(LevelK L, const float* __restrict__ x,
+                                                  const float* xlo, const float* xhi, RhsK R,
+                                                  XferAxis tx, XferAxis ty, XferAxis tz,
+                                                  int ncx, int ncy, int nczl,
+                                                  float* __restrict__ bc) {
+  const int cx = blockIdx.x * blockDim.x + threadIdx.x;
+  const int cy = blockIdx.y * blockDim.y + threadIdx.y;
+  if (cx >= ncx || cy >= ncy) return;
+  restrict_point<MODE, TI>(L, x, xlo, xhi, R, tx, ty, tz, ncx, ncy, bc, cx, cy, blockIdx.z);
 }
 
 // Restriction of a right-hand side alone (FMG start): the sum k_restrict forms for x = 0, where
@@ -932,6 +947,133 @@ cudaError_t launch_coarse(const CoarseK& C, const float* b, float* x, cudaStream
   const int nsys = C.cz ? 1 : C.nz;
   k_coarse_fd<<<nsys, 512, smem, s>>>(C, b, x);
   return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------------
+// Coarse tail of a V-cycle in two cooperative launches (the small levels
+// are launch- and latency-bound): one persistent grid walks the levels [lc, nl-1) down (zero start,
+// nu_pre red-black sweeps, residual restriction) with a grid-wide barrier between the phases, the
+// coarsest solve stays its own kernel, and a second grid walks them up (prolongation + correction,
+// nu_post sweeps).  Every point runs the reference schedule's arithmetic (rbgs_point,
+// restrict_point, prolong_point), so the iterate is bit-identical.  Single-slab levels only.
+// ---------------------------------------------------------------------------------
+// x_f(cell) += P x_c: the reference prolongation of one fine cell (k_prolong_rows' per-cell order)
+__device__ __forceinline__ void prolong_point(const LevelK& L, float* __restrict__ xf, const XferAxis& tx,
+                                              const XferAxis& ty, const XferAxis& tz, int ncx, int ncy,
+                                              const float* __restrict__ xc, int fx, int fy, int fz) {
+  long long Ix, Jx, Iy, Jy, Iz, Jz;
+  float txw, tyw, tzw;
+  if (ptaps_regular(tx, fx)) ptaps_fast(tx, fx, Ix, Jx, txw); else ptaps(tx, fx, Ix, Jx, txw);
+  if (ptaps_regular(ty, fy)) ptaps_fast(ty, fy, Iy, Jy, tyw); else ptaps(ty, fy, Iy, Jy, tyw);
+  if (ptaps_regular(tz, L.z0 + fz)) ptaps_fast(tz, L.z0 + fz, Iz, Jz, tzw); else ptaps(tz, L.z0 + fz, Iz, Jz, tzw);
+  const long long cplane = (long long)ncx * ncy;
+  const float* pI = xc + Iz * cplane;
+  const float* pJ = xc + Jz * cplane;
+  auto bil = [&](const float* p) {
+    const float* rI = p + Iy * ncx;
+    const float* rJ = p + Jy * ncx;
+    return bilerp(rI[Ix], rI[Jx], rJ[Ix], rJ[Jx], txw, tyw);
+  };
+  float e = bil(pI);
+  if (tzw != 0.f) e = __fmaf_rn(tzw, bil(pJ), __fmul_rn(1.f - tzw, e));
+  const long long c = (long long)fz * L.nx * L.ny + (long long)fy * L.nx + fx;
+  xf[c] = __fadd_rn(xf[c], e);
+}
+
+// grid-wide barrier of the cooperative launch (cooperative_groups: release / acquire at gpu scope)
+__device__ __forceinline__ void grid_barrier(unsigned int*, unsigned int&) { cooperative_groups::this_grid().sync(); }
+
+__global__ void __launch_bounds__(256) k_coop_down(const CoopLv* __restrict__ lv, int n, int nu, int zero_first,
+                                                   unsigned int* bar) {
+  unsigned int gen = 0;
+  const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x, nth = (long long)gridDim.x * blockDim.x;
+  for (int i = 0; i < n; ++i) {
+    const CoopLv V = lv[i];
+    const LevelK& L = V.K;
+    const long long pl = (long long)L.nx * L.ny, N = pl * L.nzl;
+    if (i > 0 || zero_first) {
+      for (long long c = tid; c < N; c += nth) V.x[c] = 0.f;
+      grid_barrier(bar, gen);
+    }
+    const RhsK R{V.b, nullptr, nullptr, 0.f, 0};
+    const int nxh = (L.nx + 1) / 2;
+    const long long NH = (long long)nxh * L.ny * L.nzl;
+    for (int k = 0; k < nu; ++k)
+      for (int color = 0; color < 2; ++color) {
+        for (long long h = tid; h < NH; h += nth) {
+          const int ixh = (int)(h % nxh);
+          const long long r = h / nxh;
+          rbgs_point<RHS_B, float>(L, V.x, nullptr, nullptr, R, color, ixh, (int)(r % L.ny), (int)(r / L.ny));
+        }
+        grid_barrier(bar, gen);
+      }
+    const long long NC = (long long)V.ncx * V.ncy * V.nczl;
+    for (long long q = tid; q < NC; q += nth) {
+      const int cx = (int)(q % V.ncx);
+      const long long r = q / V.ncx;
+      restrict_point<RHS_B, float>(L, V.x, nullptr, nullptr, R, V.tx, V.ty, V.tz, V.ncx, V.ncy, V.bc, cx,
+                                   (int)(r % V.ncy), (int)(r / V.ncy));
+    }
+    grid_barrier(bar, gen);
+  }
+}
+
+__global__ void __launch_bounds__(256) k_coop_up(const CoopLv* __restrict__ lv, int n, int nu, unsigned int* bar) {
+  unsigned int gen = 0;
+  const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x, nth = (long long)gridDim.x * blockDim.x;
+  for (int i = n - 1; i >= 0; --i) {
+    const CoopLv V = lv[i];
+    const LevelK& L = V.K;
+    const long long pl = (long long)L.nx * L.ny, N = pl * L.nzl;
+    for (long long c = tid; c < N; c += nth) {
+      const int fx = (int)(c % L.nx);
+      const long long r = c / L.nx;
+      prolong_point(L, V.x, V.tx, V.ty, V.tz, V.ncx, V.ncy, V.xc, fx, (int)(r % L.ny), (int)(r / L.ny));
+    }
+    grid_barrier(bar, gen);
+    const RhsK R{V.b, nullptr, nullptr, 0.f, 0};
+    const int nxh = (L.nx + 1) / 2;
+    const long long NH = (long long)nxh * L.ny * L.nzl;
+    for (int k = 0; k < nu; ++k)
+      for (int color = 0; color < 2; ++color) {
+        for (long long h = tid; h < NH; h += nth) {
+          const int ixh = (int)(h % nxh);
+          const long long r = h / nxh;
+          rbgs_point<RHS_B, float>(L, V.x, nullptr, nullptr, R, color, ixh, (int)(r % L.ny), (int)(r / L.ny));
+        }
+        if (i > 0 || k < nu - 1 || color == 0) grid_barrier(bar, gen);  // the kernel end orders the last
+      }
+  }
+}
+
+static int coop_grid() {
+  static int g = 0;
+  if (!g) {
+    int dev = 0, nsm = 148, per = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_coop_down, 256, 0);
+    int per2 = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per2, k_coop_up, 256, 0);
+    g = nsm * std::max(1, std::min(std::min(per, per2), 4));
+  }
+  return g;
+}
+
+cudaError_t launch_coop(bool down, const CoopLv* lv, int n, int nu, int zero_first, unsigned int* bar,
+                        double cells, double bytes, cudaStream_t s) {
+  ProfScope ps(KC_COOP, bytes, s, cells);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(coop_grid());
+  cfg.blockDim = dim3(256);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;  // co-residency of the whole grid (grid.sync)
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  if (down) return cudaLaunchKernelEx(&cfg, k_coop_down, lv, n, nu, zero_first, bar);
+  return cudaLaunchKernelEx(&cfg, k_coop_up, lv, n, nu, bar);
 }
 
 }  // namespace gdp

@@ -18,7 +18,7 @@ inline void count_launch(long long n = 1) { g_launches.fetch_add(n, std::memory_
 // algorithmic bytes it must move.  Disabled: no cost.
 enum KClass {
   KC_RBGS = 0, KC_RESTRICT, KC_PROLONG, KC_NORMS, KC_COARSE, KC_UTIL,
-  KC_DOWN2D, KC_UP2D, KC_DOWN3D, KC_UP3D, KC_COUNT
+  KC_DOWN2D, KC_UP2D, KC_DOWN3D, KC_UP3D, KC_COOP, KC_COUNT
 };
 extern const char* kclass_name[KC_COUNT];
 extern bool g_prof_on;
@@ -120,6 +120,18 @@ void launch_init(const LevelK& L, const RhsK& R, int tI, float* x0, float* b, do
 void launch_add_scalar(float* x, long long n, float v, cudaStream_t s);
 void launch_axpy(float* x, const float* e, long long n, cudaStream_t s);
 void launch_maxdiff(const float* a, const float* b, long long n, unsigned int* out, cudaStream_t s);
+// the coarse tail of a V-cycle (levels lc .. nl-2 of a single-slab hierarchy), cooperative grids
+struct CoopLv {
+  LevelK K;             // the level
+  float* x;             // its x
+  const float* b;       // its rhs
+  XferAxis tx, ty, tz;  // to the next coarser level
+  int ncx, ncy, nczl;
+  float* bc;            // next level's rhs (down: restricted residual)
+  const float* xc;      // next level's x (up: prolongated correction)
+};
+cudaError_t launch_coop(bool down, const CoopLv* lv, int n, int nu, int zero_first, unsigned int* bar,
+                        double cells, double bytes, cudaStream_t s);
 size_t coarse_smem_bytes(const CoarseK& C);
 cudaError_t launch_coarse(const CoarseK& C, const float* b, float* x, cudaStream_t s);
 

@@ -29,7 +29,7 @@ std::atomic<long long> g_launches{0};
 // per-kernel-class profiler
 // ---------------------------------------------------------------------------------
 const char* kclass_name[KC_COUNT] = {"rbgs", "restrict", "prolong", "norms", "coarse", "util",
-                                     "down2d", "up2d", "down3d", "up3d"};
+                                     "down2d", "up2d", "down3d", "up3d", "coop"};
 bool g_prof_on = false;
 double g_prof_finest = 0.0;
 double g_prof_l1 = 0.0;
@@ -232,6 +232,7 @@ Hier::~Hier() {
   if (dx_dev) cudaFree(dx_dev);
   if (dx_host) cudaFreeHost(dx_host);
   if (xprev) cudaFree(xprev);
+  if (coop_dev) cudaFree(coop_dev);
   for (auto& g : graphs)
     if (g.second.exec) cudaGraphExecDestroy(g.second.exec);
 }
@@ -499,6 +500,27 @@ int run_vcycle(Ctx& ctx, Hier& H, const Fine& f, const gdp_opts& o, cudaStream_t
     else if (rhs_ok && nu_ok && fusable3d(L, C, o)) fz[l] = 3;
     if (fz[l] && !L.x2) CK(cudaMalloc(&L.x2, sizeof(float) * (size_t)L.nx * L.ny * L.nzl));
   }
+  // the coarse tail [lc, nl - 1): single-slab levels under the size threshold run in two cooperative
+  // launches (fused bit 8); lc = nl - 1: none
+  int lc = nl - 1;
+  if (o.fused & 8) {
+    static const long long cmax = getenv("GDP_COOP_MAX") ? atoll(getenv("GDP_COOP_MAX")) : 2000000LL;
+    for (int l = nl - 2; l >= std::max(l0, 1); --l) {
+      const Level& L = H.lv[l];
+      if ((long long)L.nx * L.ny * L.nzl >= cmax || L.nzl != L.gz.n || L.xlo) break;
+      lc = l;
+    }
+    if (lc < nl - 1 && !H.coop_dev) {  // the levels' device views, once per hierarchy (before any capture)
+      std::vector<CoopLv> v(nl - 1);
+      for (int l = 1; l < nl - 1; ++l) {
+        const Level& L = H.lv[l];
+        const Level& C = H.lv[l + 1];
+        v[l - 1] = CoopLv{L.K, L.x, L.b, C.tx, C.ty, C.tz, C.nx, C.ny, C.nzl, C.b, C.x};
+      }
+      CK(cudaMalloc(&H.coop_dev, sizeof(CoopLv) * v.size()));
+      CK(cudaMemcpy(H.coop_dev, v.data(), sizeof(CoopLv) * v.size(), cudaMemcpyHostToDevice));
+    }
+  }
   for (int l = l0; l < nl - 1; ++l) {
     Level& L = H.lv[l];
     Level& C = H.lv[l + 1];
@@ -509,6 +531,18 @@ int run_vcycle(Ctx& ctx, Hier& H, const Fine& f, const gdp_opts& o, cudaStream_t
       R = RhsK{L.b, nullptr, nullptr, 0.f, 0};
       mode = RHS_B;
       tI = 1;
+    }
+    if (l >= lc) {  // the cooperative down walk over [lc, nl - 1)
+      const bool pro = l == l0 && (flags & RV_PROLONG);
+      if (pro) {  // FMG start at l0: x = P x_{l0+1} (zero + correction), then the walk without zeroing
+        CK(cudaMemsetAsync(x, 0, sizeof(float) * (size_t)L.nx * L.ny * L.nzl, s));
+        launch_prolong(L.K, x, C.tx, C.ty, C.tz, C.nx, C.ny, C.nzl, C.z0, C.x, C.xlo, C.xhi, s);
+      }
+      double cells = 0.0;
+      for (int q = lc; q < nl - 1; ++q) cells += (double)H.lv[q].nx * H.lv[q].ny * H.lv[q].nzl;
+      CK(launch_coop(true, H.coop_dev + (lc - 1), nl - 1 - lc, o.nu_pre, pro ? 0 : 1, nullptr, cells,
+                     cells * 4.0 * (2.0 * o.nu_pre + 2.0), s));
+      break;
     }
     // FMG start at l0: x (zeroed above level 0) += P x_{l0+1}, in the first fused 3D sweep
     // when there is one to carry it, else by the prolongation kernel
@@ -551,7 +585,13 @@ int run_vcycle(Ctx& ctx, Hier& H, const Fine& f, const gdp_opts& o, cudaStream_t
   }
   Level& Lc = H.lv[nl - 1];
   CK(launch_coarse(H.coarse, Lc.b, Lc.x, s));
-  for (int l = nl - 2; l >= l0; --l) {
+  if (lc < nl - 1) {  // the cooperative up walk over (nl - 1, lc]
+    double cells = 0.0;
+    for (int q = lc; q < nl - 1; ++q) cells += (double)H.lv[q].nx * H.lv[q].ny * H.lv[q].nzl;
+    CK(launch_coop(false, H.coop_dev + (lc - 1), nl - 1 - lc, o.nu_post, 0, nullptr, cells,
+                   cells * 4.0 * (2.0 * o.nu_post + 2.0), s));
+  }
+  for (int l = std::min(nl - 2, lc - 1); l >= l0; --l) {
     Level& L = H.lv[l];
     Level& C = H.lv[l + 1];
     float* x = l == 0 ? f.x : L.x;

@@ -516,3 +516,23 @@ def test_cuda_graph_replay_bit_identical(gpu_ctx):
         assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
         assert a[2]["rel_res"] == b[2]["rel_res"] and a[3]["rel_res"] == b[3]["rel_res"]
         assert a[2]["kernel_launches"] == b[2]["kernel_launches"] and a[3]["kernel_launches"] == b[3]["kernel_launches"]
+
+
+def test_host_entry_in_core_batched_phase2(gpu_ctx):
+    """gdp_destripe_host in core, phase 2 in slice batches (GDP_E2E_BATCHES, default 1) whose
+    device-to-host copies overlap the next batch's solve.  Slices are independent systems, so the
+    result meets the same bars as the one-launch device solve."""
+    shape = (96, 140, 200)
+    nz, ny, nx = shape
+    I0 = synth.make_stack(nx, ny, nz, 65, "u8")
+    t0 = torch.from_numpy(I0).pin_memory()
+    I1 = torch.empty(shape, dtype=torch.float32).pin_memory()
+    I2 = torch.empty(shape, dtype=torch.float32).pin_memory()
+    r1, r2 = gdp.gdp_destripe_host(gpu_ctx, t0, I2, I1=I1, alpha=0.01)
+    assert r1["status"] == "GDP_OK" and r2["status"] == "GDP_OK"
+    d1, d2, _, _ = gdp.gdp_destripe(gpu_ctx, dev(I0), alpha=0.01)
+    assert np.array_equal(I1.numpy(), d1.cpu().numpy())  # phase 1 is the same solve
+    assert np.abs(I2.numpy() - d2.cpu().numpy()).max() <= 2e-5
+    ref1, ref2 = O.destripe(I0, alpha=0.01)
+    assert np.abs(I2.numpy().astype(np.float64) - ref2).max() <= 1e-4
+    assert _rel_sp(I0, I1.numpy().astype(np.float64), I2.numpy().astype(np.float64), 0.01) <= TOL_R

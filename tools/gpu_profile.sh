@@ -23,6 +23,6 @@ for r in ("prof3d_$TAG", "prof2d_$TAG"):
     except Exception as e: print("summary failed", r, e)
 json.dump(rows, open("gpurun_out/ncu_full_$TAG.json", "w"), indent=1)
 PY
-python tools/make_traffic.py gpurun_out/ncu_full_$TAG.json > gpurun_out/ncu_full_summary.json
+python tools/make_traffic.py gpurun_out/ncu_full_$TAG.json "ncu --set full of tools/prof_step.py 1 0 3 (profiles/ncu_full_$TAG.json)" > gpurun_out/ncu_full_summary.json
 rm -f gpurun_out/prof3d_$TAG.ncu-rep gpurun_out/prof2d_$TAG.ncu-rep; ls -la gpurun_out/*.ncu-rep
 du -sh gpurun_out; free -g | head -2; nproc; df -h /dev/shm /tmp | tail -2

@@ -35,4 +35,5 @@ for name, v in best.items():
 out = {c: {"dram_bytes_per_launch": sum(x["bytes"] for x in vs) / len(vs),
            "ncu_time_s_per_launch": sum(x["time_s"] for x in vs) / len(vs), "variants": len(vs)}
        for c, vs in classes.items()}
+out["_source"] = sys.argv[2] if len(sys.argv) > 2 else sys.argv[1]
 print(json.dumps(out, indent=1))

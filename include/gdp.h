@@ -100,7 +100,9 @@ typedef struct {
                              in two cooperative launches (down walk, up walk) around the
                              coarsest solve, instead of ~5 launches per level.  Bit-identical;
                              measured 0.45 ms slower per config-1 step than graph-replayed
-                             per-level launches, hence off by default.
+                             per-level launches, hence off by default;
+                         16 = with 2: each 3D sweep by the TMA-staged single-sweep pass kernel
+                             instead of the z-march (bit-identical; measured slower).
                          Default 3.                                                          */
   int use_graphs;     /* 1: every V-cycle of a single-rank in-core solve (with its norm read-back)
                          is captured once as a CUDA graph per (output buffer, cycle variant) and

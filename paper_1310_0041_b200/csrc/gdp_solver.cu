@@ -572,7 +572,12 @@ int run_vcycle(Ctx& ctx, Hier& H, const Fine& f, const gdp_opts& o, cudaStream_t
       float* c = x;
       for (int k = 0; k < o.nu_pre; ++k) {
         float* d = c == x ? L.x2 : x;
-        fused_sweep3d(L, C, c, d, R.b, zx && k == 0, pro_fused && k == 0, k == o.nu_pre - 1 ? 1 : 0, nullptr, s);
+        const int tl = k == o.nu_pre - 1 ? 1 : 0;
+        const bool pk = pro_fused && k == 0;
+        if ((o.fused & 16) && vpass3d_ok(L, C, 1, pk, tl, c, d, R.b))  // one TMA-staged sweep per launch
+          RET(fused_pass3d(L, C, c, d, R.b, zx && k == 0, pk, 1, tl, nullptr, nullptr, s, nullptr));
+        else
+          fused_sweep3d(L, C, c, d, R.b, zx && k == 0, pk, tl, nullptr, s);
         c = d;
       }
       cur[l] = c;
@@ -622,16 +627,23 @@ int run_vcycle(Ctx& ctx, Hier& H, const Fine& f, const gdp_opts& o, cudaStream_t
       float* c = cur[l];
       // coarse levels: the prolongation by its own kernel (the z-march's coarse-row loads are
       // exposed latency there: e.g. 156 vs 53 + ~25 us on a 256^2 x 128 level)
-      const bool sep = l > 0;
+      const bool v16 = (o.fused & 16) && vpass3d_ok(L, C, 1, true, 0, c, x, R.b);
+      const bool sep = l > 0 && !v16;
       if (sep) launch_prolong(L.K, c, C.tx, C.ty, C.tz, C.nx, C.ny, C.nzl, C.z0, C.x, C.xlo, C.xhi, s);
+      int got = 0;
       for (int k = 0; k < o.nu_post; ++k) {
         float* d = c == x ? L.x2 : x;
         const bool last = k == o.nu_post - 1;
-        fused_sweep3d(L, C, c, d, R.b, false, k == 0 && !sep, last && want ? 2 : 0, want ? H.partials : nullptr, s);
+        const int tl = last && want ? 2 : 0;
+        if (v16 && vpass3d_ok(L, C, 1, k == 0, tl, c, d, R.b))
+          RET(fused_pass3d(L, C, c, d, R.b, false, k == 0, 1, tl, tl ? H.partials : nullptr, nullptr, s,
+                           tl ? &got : nullptr));
+        else
+          fused_sweep3d(L, C, c, d, R.b, false, k == 0 && !sep, tl, want ? H.partials : nullptr, s);
         c = d;
       }
       if (c != x) CK(cudaMemcpyAsync(x, c, sizeof(float) * (size_t)L.nx * L.ny * L.nzl, cudaMemcpyDeviceToDevice, s));
-      if (want) { H.up_norm_per = items; H.up_norm_planes = 1; }
+      if (want) { H.up_norm_per = got > 0 ? got : items; H.up_norm_planes = 1; }
       continue;
     }
     launch_prolong(L.K, x, C.tx, C.ty, C.tz, C.nx, C.ny, C.nzl, C.z0, C.x, C.xlo, C.xhi, s);

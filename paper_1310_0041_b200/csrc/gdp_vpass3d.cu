@@ -85,6 +85,10 @@ static cudaError_t dispatch(const Pass& P, bool prolong, bool zc, int tail, cuda
     VPL(0, true, false);
   }
   if (tail == TAIL_RESTRICT) { if (zc) VPL(1, false, true); VPL(1, false, false); }
+  if constexpr (NU == 1) {  // single sweeps (fused bit 16)
+    if (tail == TAIL_NORMS) VPL(2, false, false);
+    VPL(0, false, false);
+  }
   return cudaErrorInvalidValue;  // not instantiated (vpass3d_ok refuses it)
 #undef VPL
 }
@@ -95,7 +99,7 @@ static cudaError_t dispatch(const Pass& P, bool prolong, bool zc, int tail, cuda
 bool vpass3d_ok(const Level& L, const Level& C, int nu, bool prolong, int tail, const float* xin,
                 const float* xout, const float* b) {
   if (nu != 1 && nu != 2) return false;
-  if (!prolong && tail != TAIL_RESTRICT) return false;  // variants not instantiated
+  if (!prolong && tail != TAIL_RESTRICT && nu != 1) return false;  // variants not instantiated
   if (!C.tx.coarsened || !C.ty.coarsened || (prolong && C.tz.coarsened)) return false;
   if ((L.nx & 3) != 0 || (C.nx & 3) != 0) return false;
   if (!al16(xin) || !al16(xout) || !al16(b) || !al16(C.x) || !al16(C.b)) return false;

@@ -651,7 +651,8 @@ cudaError_t launch_vp(const Pass& P, cudaStream_t s) {
 #define GDP_VP_VARIANTS(X) \
   X(1, 1, false, false) X(1, 1, false, true) X(1, 1, true, false) \
   X(2, 1, false, false) X(2, 1, false, true) X(2, 1, true, false) \
-  X(1, 2, true, false) X(1, 0, true, false) X(2, 2, true, false) X(2, 0, true, false)
+  X(1, 2, true, false) X(1, 0, true, false) X(2, 2, true, false) X(2, 0, true, false) \
+  X(1, 0, false, false) X(1, 2, false, false)
 
 }  // namespace vp
 }  // namespace gdp

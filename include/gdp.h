@@ -117,8 +117,8 @@ typedef struct {
   float omega;        /* over-relaxation of the red-black sweeps, 0 < omega < 2 (1 = Gauss-Seidel;
                          the converged answer does not depend on it).  Phases 1 / general.    */
   float omega_slices; /* the same for phase 2.                                              */
-  int fmg;            /* full-multigrid start of an in-core single-rank solve (the z-slab team
-                         and the out-of-core streamer start from x0 as before): r0 is
+  int fmg;            /* full-multigrid start of an in-core solve, single rank or z-slab team (the
+                         out-of-core streamer starts from x0): r0 is
                          restricted to level 1, solved there by nested iteration (coarsest
                          solve, then per level a prolongation and one V-cycle), and the
                          correction is prolongated into the first fine V-cycle.  Changes the

@@ -224,8 +224,33 @@ static int team_fused_sweeps(Ctx& c, DistPlan& D, int* cur, int nu, bool prolong
   return GDP_OK;
 }
 
+// prolongation of level l+1 into level l of every local part (x_l += P x_{l+1}); the coarse level
+// is split (ghost planes refreshed first) or the gathered tail's first level
+static int team_prolong(Ctx& c, DistPlan& D, int l, float* const* xs, cudaStream_t s) {
+  const int np = (int)D.parts.size();
+  Level& TF = D.tail->lv[0];
+  if (l + 1 < D.ff) {
+    std::vector<float*> xc(np);
+    for (int i = 0; i < np; ++i) xc[i] = D.parts[i]->lv[l + 1].x;
+    RETD(comm_halo_parts(c, D, l + 1, xc.data(), s));
+  }
+  for (int i = 0; i < np; ++i) {
+    Level& L = D.parts[i]->lv[l];
+    if (l + 1 < D.ff) {
+      Level& C = D.parts[i]->lv[l + 1];
+      launch_prolong(L.K, xs[i], C.tx, C.ty, C.tz, C.nx, C.ny, C.nzl, C.z0, C.x, C.xlo, C.xhi, s);
+    } else {
+      launch_prolong(L.K, xs[i], TF.tx, TF.ty, TF.tz, TF.nx, TF.ny, TF.nzl, 0, TF.x, nullptr, nullptr, s);
+    }
+  }
+  return GDP_OK;
+}
+
+// One V-cycle of the partition over global levels l0.. (l0 > 0: a nested FMG cycle); flags
+// RV_PROLONG: level l0 starts from the prolongation of level l0 + 1 (added to x at level 0, to zero
+// above), the single-rank run_vcycle's convention.  *rel: the norms of the fused finest level.
 static int team_vcycle(Ctx& c, DistPlan& D, float* const* x0, const gdp_opts& o, cudaStream_t s, int* cur,
-                       double* rel) {
+                       double* rel, int l0 = 0, unsigned flags = 0) {
   const int np = (int)D.parts.size();
   const int ff = D.ff;
   std::vector<float*> xs(np);
@@ -233,16 +258,26 @@ static int team_vcycle(Ctx& c, DistPlan& D, float* const* x0, const gdp_opts& o,
   Hier& T = *D.tail;
   Level& TF = T.lv[0];
   const size_t tplane = (size_t)TF.nx * TF.ny;
-  if (D.active) {
-    RETD(team_fused_sweeps(c, D, cur, o.nu_pre, false, 1, nullptr, nullptr, s));
+  Fine ft;
+  ft.x = TF.x;
+  ft.mode = RHS_B;
+  ft.tI = 1;
+  ft.R = RhsK{TF.b, nullptr, nullptr, 0.f, 0};
+  const bool pro = (flags & RV_PROLONG) != 0;
+  if (l0 >= ff) {  // the whole cycle lives in the gathered levels (replicated on every rank)
+    if (l0 == ff && pro) CKD(cudaMemsetAsync(TF.x, 0, sizeof(float) * tplane * TF.nzl, s));  // run_vcycle adds P e at its level 0
+    return run_vcycle(c, T, ft, o, s, l0 - ff, flags);
   }
-  for (int l = D.active ? 1 : 0; l < ff; ++l) {
+  const bool fused0 = D.active && l0 == 0;
+  if (fused0) RETD(team_fused_sweeps(c, D, cur, o.nu_pre, pro, 1, nullptr, nullptr, s));
+  for (int l = fused0 ? 1 : l0; l < ff; ++l) {
     for (int i = 0; i < np; ++i) {
       Level& L = D.parts[i]->lv[l];
       xs[i] = l == 0 ? x0[i] : L.x;
       bs[i] = l == 0 ? D.b0[i] : L.b;
       if (l > 0) CKD(cudaMemsetAsync(xs[i], 0, sizeof(float) * (size_t)L.nx * L.ny * L.nzl, s));
     }
+    if (l == l0 && pro) RETD(team_prolong(c, D, l, xs.data(), s));  // FMG start at l0
     RETD(team_smooth(c, D, l, xs.data(), bs.data(), o.nu_pre, s));
     RETD(comm_halo_parts(c, D, l, xs.data(), s));
     for (int i = 0; i < np; ++i) {
@@ -263,35 +298,17 @@ static int team_vcycle(Ctx& c, DistPlan& D, float* const* x0, const gdp_opts& o,
   // gathered levels: one V-cycle of the tail from a zero start (replicated on every rank)
   RETD(comm_gather_full(c, D, TF.b, s));
   CKD(cudaMemsetAsync(TF.x, 0, sizeof(float) * tplane * TF.nzl, s));
-  Fine ft;
-  ft.x = TF.x;
-  ft.mode = RHS_B;
-  ft.tI = 1;
-  ft.R = RhsK{TF.b, nullptr, nullptr, 0.f, 0};
   RETD(run_vcycle(c, T, ft, o, s));
-  for (int l = ff - 1; l >= (D.active ? 1 : 0); --l) {
+  for (int l = ff - 1; l >= (fused0 ? 1 : l0); --l) {
     for (int i = 0; i < np; ++i) {
       Level& L = D.parts[i]->lv[l];
       xs[i] = l == 0 ? x0[i] : L.x;
       bs[i] = l == 0 ? D.b0[i] : L.b;
     }
-    if (l + 1 < ff) {
-      std::vector<float*> xc(np);
-      for (int i = 0; i < np; ++i) xc[i] = D.parts[i]->lv[l + 1].x;
-      RETD(comm_halo_parts(c, D, l + 1, xc.data(), s));
-    }
-    for (int i = 0; i < np; ++i) {
-      Level& L = D.parts[i]->lv[l];
-      if (l + 1 < ff) {
-        Level& C = D.parts[i]->lv[l + 1];
-        launch_prolong(L.K, xs[i], C.tx, C.ty, C.tz, C.nx, C.ny, C.nzl, C.z0, C.x, C.xlo, C.xhi, s);
-      } else {
-        launch_prolong(L.K, xs[i], TF.tx, TF.ty, TF.tz, TF.nx, TF.ny, TF.nzl, 0, TF.x, nullptr, nullptr, s);
-      }
-    }
+    RETD(team_prolong(c, D, l, xs.data(), s));
     RETD(team_smooth(c, D, l, xs.data(), bs.data(), o.nu_post, s));
   }
-  if (D.active) {
+  if (fused0) {
     if (ff > 1) {  // the split level 1 feeds the prolongation: refresh its ghost planes
       std::vector<float*> xc(np);
       for (int i = 0; i < np; ++i) xc[i] = D.parts[i]->lv[1].x;
@@ -299,7 +316,90 @@ static int team_vcycle(Ctx& c, DistPlan& D, float* const* x0, const gdp_opts& o,
     }
     double rr = 0.0, bb = 0.0;
     RETD(team_fused_sweeps(c, D, cur, o.nu_post, true, 2, &rr, &bb, s));
-    *rel = bb > 0 ? std::sqrt(rr / bb) : std::sqrt(rr);
+    if (rel) *rel = bb > 0 ? std::sqrt(rr / bb) : std::sqrt(rr);
+  }
+  CKD(cudaGetLastError());
+  return GDP_OK;
+}
+
+// FMG start of the partition (the single-rank fmg_start, level by level): r0 = b - A x0 restricted
+// to level 1, the right-hand side restricted on down (split levels per slab, gathered once), the
+// coarsest solve, then per level a nested V-cycle started from the prolongation of the level below
+// (V(nu_pre, nu_post - 1)); the caller's first fine cycle prolongates e_1 into x (RV_PROLONG).
+static int team_fmg_start(Ctx& c, DistPlan& D, float* const* x0, const gdp_opts& o, cudaStream_t s, int* cur) {
+  const int np = (int)D.parts.size();
+  const int ff = D.ff;
+  Hier& T = *D.tail;
+  Level& TF = T.lv[0];
+  const size_t tplane = (size_t)TF.nx * TF.ny;
+  const size_t pl = (size_t)D.parts[0]->lv[0].nx * D.parts[0]->lv[0].ny;
+  std::vector<float*> xw(np);  // level-0 x of every part (the fused windows' interior when active)
+  for (int i = 0; i < np; ++i) xw[i] = D.active ? (*cur ? D.w1[i] : D.w0[i]) + pl * DistPlan::G : x0[i];
+  RETD(comm_halo_parts(c, D, 0, xw.data(), s));
+  auto into_gathered = [&](const Level& L, bool b_only, const float* src, const float* b) {
+    const bool cz = TF.tz.coarsened;
+    const long long off = cz ? L.z0 / 2 : L.z0;
+    const int nczl = cz ? L.nzl / 2 : L.nzl;
+    if (b_only) launch_restrict_b(L.K, b, TF.tx, TF.ty, TF.tz, TF.nx, TF.ny, nczl, TF.b + off * tplane, s);
+    else launch_restrict(L.K, src, L.xlo, L.xhi, RhsK{b, nullptr, nullptr, 0.f, 0}, RHS_B, 1, TF.tx, TF.ty, TF.tz,
+                         TF.nx, TF.ny, nczl, TF.b + off * tplane, s);
+  };
+  for (int i = 0; i < np; ++i) {  // r0 restricted to level 1
+    const Level& L = D.parts[i]->lv[0];
+    if (ff > 1) {
+      const Level& C = D.parts[i]->lv[1];
+      launch_restrict(L.K, xw[i], L.xlo, L.xhi, RhsK{D.b0[i], nullptr, nullptr, 0.f, 0}, RHS_B, 1, C.tx, C.ty, C.tz,
+                      C.nx, C.ny, C.nzl, C.b, s);
+    } else {
+      into_gathered(L, false, xw[i], D.b0[i]);
+    }
+  }
+  for (int l = 1; l < ff; ++l)  // the rhs restricted on down the split levels
+    for (int i = 0; i < np; ++i) {
+      const Level& L = D.parts[i]->lv[l];
+      if (l + 1 < ff) {
+        const Level& C = D.parts[i]->lv[l + 1];
+        launch_restrict_b(L.K, L.b, C.tx, C.ty, C.tz, C.nx, C.ny, C.nzl, C.b, s);
+      } else {
+        into_gathered(L, true, nullptr, L.b);
+      }
+    }
+  RETD(comm_gather_full(c, D, TF.b, s));
+  for (size_t j = 0; j + 1 < T.lv.size(); ++j) {  // and through the gathered levels
+    const Level& L = T.lv[j];
+    const Level& C = T.lv[j + 1];
+    launch_restrict_b(L.K, L.b, C.tx, C.ty, C.tz, C.nx, C.ny, C.nzl, C.b, s);
+  }
+  Level& Lc = T.lv.back();
+  CKD(launch_coarse(T.coarse, Lc.b, Lc.x, s));
+  gdp_opts on = o;
+  on.nu_post = std::max(1, o.nu_post - 1);
+  const int mode = o.fmg & 3;
+  const int lmin = mode == 1 ? 1 : 2;
+  const int ntot = ff + (int)T.lv.size();
+  for (int l = ntot - 2; l >= lmin; --l) RETD(team_vcycle(c, D, x0, on, s, cur, nullptr, l, RV_PROLONG));
+  for (int l = lmin - 1; l >= 1; --l) {  // levels only interpolated (3) or interpolated and smoothed (2)
+    if (l >= ff) {
+      Level& L = T.lv[l - ff];
+      Level& C = T.lv[l - ff + 1];
+      CKD(cudaMemsetAsync(L.x, 0, sizeof(float) * (size_t)L.nx * L.ny * L.nzl, s));
+      launch_prolong(L.K, L.x, C.tx, C.ty, C.tz, C.nx, C.ny, C.nzl, C.z0, C.x, C.xlo, C.xhi, s);
+      if (mode == 2)
+        for (int k = 0; k < o.nu_post; ++k)
+          for (int color = 0; color < 2; ++color)
+            launch_rbgs(L.K, L.x, L.xlo, L.xhi, RhsK{L.b, nullptr, nullptr, 0.f, 0}, RHS_B, 1, color, s);
+      continue;
+    }
+    std::vector<float*> xs(np);
+    std::vector<const float*> bs(np);
+    for (int i = 0; i < np; ++i) {
+      Level& L = D.parts[i]->lv[l];
+      xs[i] = L.x;
+      bs[i] = L.b;
+      CKD(cudaMemsetAsync(L.x, 0, sizeof(float) * (size_t)L.nx * L.ny * L.nzl, s));
+    }
+    RETD(team_prolong(c, D, l, xs.data(), s));
+    if (mode == 2) RETD(team_smooth(c, D, l, xs.data(), bs.data(), o.nu_post, s));
   }
   CKD(cudaGetLastError());
   return GDP_OK;
@@ -508,7 +608,9 @@ int dist_diffuse_z(Ctx& c, const void* I0, int tI, float* I1, long long nx, long
   while (rel > o.rel_tol) {
     if (k >= cap) { status = GDP_ENOCONV; break; }
     double nrel = 0.0;
-    RETD(team_vcycle(c, *D, x0.data(), o, s, &cur, &nrel));
+    const bool fmg = k == 0 && (o.fmg & 3) != 0 && D->ff + (int)D->tail->lv.size() >= 3;
+    if (fmg) RETD(team_fmg_start(c, *D, x0.data(), o, s, &cur));
+    RETD(team_vcycle(c, *D, x0.data(), o, s, &cur, &nrel, 0, fmg ? RV_PROLONG : 0u));
     if (!D->active) RETD(team_norms(c, *D, x0.data(), &nrel, nullptr, s));
     r.rel_res[++k] = nrel;
     if (!std::isfinite(nrel)) return set_err(GDP_EINVAL, "non-finite residual after V-cycle %d", k);

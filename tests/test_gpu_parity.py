@@ -251,12 +251,13 @@ def test_fused_3d_vcycle_nu_variants(gpu_ctx, nu, shape):
 # ------------------------------------------------------------------ z-slab partition (loopback)
 @pytest.mark.parametrize("shape,world", [((16, 64, 64), 2), ((33, 40, 48), 3), ((128, 96, 96), 4),
                                          ((12, 70, 90), 5), ((64, 130, 75), 8)])
-def test_loopback_partition_bit_identical(gpu_ctx, shape, world):
-    """Phase 1 on `world` z-slabs (halo exchange per half-sweep, gathered coarse levels) gives
-    the single-rank iterate bit for bit, and the same converged answer as the oracle."""
+@pytest.mark.parametrize("fmg", [0, 1])
+def test_loopback_partition_bit_identical(gpu_ctx, shape, world, fmg):
+    """Phase 1 on `world` z-slabs (halo exchange per half-sweep, gathered coarse levels, the FMG
+    start level by level) gives the single-rank iterate bit for bit, and the oracle's answer."""
     nz, ny, nx = shape
     I0 = synth.make_stack(nx, ny, nz, 51, "u8")
-    o = gdp.default_opts(fused=0, fmg=0)  # the z-slab team has no FMG start (gdp.h)
+    o = gdp.default_opts(fused=0, fmg=fmg)
     ref, r1 = gdp.gdp_diffuse_z(gpu_ctx, dev(I0), opts=o)
     lb = gdp.Ctx(0, loopback=world)
     try:
@@ -272,12 +273,14 @@ def test_loopback_partition_bit_identical(gpu_ctx, shape, world):
 
 @pytest.mark.parametrize("shape,world", [((48, 128, 256), 2), ((40, 130, 250), 4), ((128, 256, 256), 8),
                                          ((27, 96, 200), 3)])
-def test_loopback_fused_partition_bit_identical(gpu_ctx, shape, world):
+@pytest.mark.parametrize("fmg", [0, 1])
+def test_loopback_fused_partition_bit_identical(gpu_ctx, shape, world, fmg):
     """Default opts: the finest level of every slab runs the fused z-march sweeps with 3 ghost
-    planes per face; the iterate equals the single-rank fused solve bit for bit."""
+    planes per face (and the FMG start on the team); the iterate equals the single-rank fused
+    solve bit for bit, in the same number of cycles."""
     nz, ny, nx = shape
     I0 = synth.make_stack(nx, ny, nz, 53, "u8")
-    o = gdp.default_opts(fmg=0)  # the z-slab team has no FMG start (gdp.h)
+    o = gdp.default_opts(fmg=fmg)
     ref, r1 = gdp.gdp_diffuse_z(gpu_ctx, dev(I0), opts=o)
     lb = gdp.Ctx(0, loopback=world)
     try:

@@ -49,7 +49,7 @@ def parse():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--config", type=int, default=CONFIG)
     p.add_argument("--alpha", type=float, default=ALPHA)
-    p.add_argument("--fused", type=int, default=3)
+    p.add_argument("--fused", type=int, default=35)
     p.add_argument("--fmg", type=int, default=None, help="gdp_opts.fmg and fmg_slices (default: the library's)")
     p.add_argument("--graphs", type=int, default=1, help="gdp_opts.use_graphs (CUDA graph replay of V-cycles)")
     p.add_argument("--dx-tol", type=float, default=None, help="gdp_opts.dx_tol (default: the library's)")

@@ -102,8 +102,13 @@ typedef struct {
                              measured 0.45 ms slower per config-1 step than graph-replayed
                              per-level launches, hence off by default;
                          16 = with 2: each 3D sweep by the TMA-staged single-sweep pass kernel
-                             instead of the z-march (bit-identical; measured slower).
-                         Default 3.                                                          */
+                             instead of the z-march (bit-identical; measured slower);
+                         32 = with 2: each 3D sweep by the vertical-pack z-march (8 x 2 cells per
+                             thread as f32x2 packs of one colour, x / b planes in and the final
+                             plane out by TMA; nx % 4 == 0, 16-byte aligned arrays; z-coarsened
+                             prolongating sweeps keep the 2 kernel).  Bit-identical; 2-9 % faster
+                             per launch than 2 on config 1.
+                         Default 35.                                                         */
   int use_graphs;     /* 1: every V-cycle of a single-rank in-core solve (with its norm read-back)
                          is captured once as a CUDA graph per (output buffer, cycle variant) and
                          replayed by later solves on the same hierarchy (launch latency; needs a

@@ -165,6 +165,11 @@ int fused_pass3d(const Level& L, const Level& C, const float* xin, float* xout, 
 int fused_sweep3d(const Level& L, const Level& C, const float* xin, float* xout, const float* b,
                   bool zero_x, bool prolong, int tail, double2* partials, cudaStream_t s, int zlo = 0,
                   int zhi = -1);
+// the vertical-pack TMA z-march sweep (gdp_march3dv.cu; fused bit 32)
+bool sweep3dv_ok(const Level& L, const Level& C, bool prolong, const float* xin, const float* xout, const float* b);
+int sweep3dv_items(const Level& L, const Level& C);
+int fused_sweep3dv(const Level& L, const Level& C, const float* xin, float* xout, const float* b, bool zero_x,
+                   bool prolong, int tail, double2* partials, cudaStream_t s, int* items);
 
 // out-of-core streaming of the finest level (gdp_stream.cu)
 struct HostPin {

@@ -576,6 +576,8 @@ int run_vcycle(Ctx& ctx, Hier& H, const Fine& f, const gdp_opts& o, cudaStream_t
         const bool pk = pro_fused && k == 0;
         if ((o.fused & 16) && vpass3d_ok(L, C, 1, pk, tl, c, d, R.b))  // one TMA-staged sweep per launch
           RET(fused_pass3d(L, C, c, d, R.b, zx && k == 0, pk, 1, tl, nullptr, nullptr, s, nullptr));
+        else if ((o.fused & 32) && sweep3dv_ok(L, C, pk, c, d, R.b))  // vertical-pack z-march
+          RET(fused_sweep3dv(L, C, c, d, R.b, zx && k == 0, pk, tl, nullptr, s, nullptr));
         else
           fused_sweep3d(L, C, c, d, R.b, zx && k == 0, pk, tl, nullptr, s);
         c = d;
@@ -622,13 +624,16 @@ int run_vcycle(Ctx& ctx, Hier& H, const Fine& f, const gdp_opts& o, cudaStream_t
       continue;
     }
     if (fz[l] == 3) {  // prolongation fused into the first sweep, norms into the last
-      const int items = fused3d_items(L, C);
-      const bool want = l == 0 && (size_t)items <= H.partials_cap * (size_t)L.nzl;
       float* c = cur[l];
       // coarse levels: the prolongation by its own kernel (the z-march's coarse-row loads are
-      // exposed latency there: e.g. 156 vs 53 + ~25 us on a 256^2 x 128 level)
+      // exposed latency there: e.g. 156 vs 53 + ~25 us on a 256^2 x 128 level); the TMA-staged
+      // kernels carry it
       const bool v16 = (o.fused & 16) && vpass3d_ok(L, C, 1, true, 0, c, x, R.b);
-      const bool sep = l > 0 && !v16;
+      const bool v32 = !v16 && (o.fused & 32) && sweep3dv_ok(L, C, true, c, x, R.b);
+      // partial slots of the norms sweep (the kernel that runs it: its own work split)
+      const int items = v32 ? sweep3dv_items(L, C) : fused3d_items(L, C);
+      const bool want = l == 0 && (size_t)items <= H.partials_cap * (size_t)L.nzl;
+      const bool sep = l > 0 && !v16 && !v32;
       if (sep) launch_prolong(L.K, c, C.tx, C.ty, C.tz, C.nx, C.ny, C.nzl, C.z0, C.x, C.xlo, C.xhi, s);
       int got = 0;
       for (int k = 0; k < o.nu_post; ++k) {
@@ -638,8 +643,12 @@ int run_vcycle(Ctx& ctx, Hier& H, const Fine& f, const gdp_opts& o, cudaStream_t
         if (v16 && vpass3d_ok(L, C, 1, k == 0, tl, c, d, R.b))
           RET(fused_pass3d(L, C, c, d, R.b, false, k == 0, 1, tl, tl ? H.partials : nullptr, nullptr, s,
                            tl ? &got : nullptr));
-        else
-          fused_sweep3d(L, C, c, d, R.b, false, k == 0 && !sep, tl, want ? H.partials : nullptr, s);
+        else if (v32 && sweep3dv_ok(L, C, k == 0, c, d, R.b))
+          RET(fused_sweep3dv(L, C, c, d, R.b, false, k == 0, tl, tl ? H.partials : nullptr, s, tl ? &got : nullptr));
+        else {
+          const int n = fused_sweep3d(L, C, c, d, R.b, false, k == 0 && !sep, tl, want ? H.partials : nullptr, s);
+          if (tl) got = n;
+        }
         c = d;
       }
       if (c != x) CK(cudaMemcpyAsync(x, c, sizeof(float) * (size_t)L.nx * L.ny * L.nzl, cudaMemcpyDeviceToDevice, s));
@@ -940,7 +949,7 @@ int gdp_opts_default(gdp_opts* o) {
   o->nu_post = 2;
   o->coarse_max = 4096;
   o->stagnation = 2;
-  o->fused = 3;
+  o->fused = 35;
   o->use_graphs = 1;
   o->nu_pre_slices = 1;
   o->nu_post_slices = 2;

@@ -46,6 +46,13 @@ static int make_map(CUtensorMap* m, const float* p, int nx, int ny, long long np
   return GDP_OK;
 }
 
+// the same, for other TMA-staged kernels (gdp_march3dv.cu)
+int vp_make_map(CUtensorMap* m, const float* p, int nx, int ny, long long np, int bw, int bh) {
+  const int rc = load_encode();
+  if (rc != GDP_OK) return rc;
+  return make_map(m, p, nx, ny, np, bw, bh);
+}
+
 static int g_nsm_vp = 0;
 static int nsm() {
   if (!g_nsm_vp) {

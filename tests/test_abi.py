@@ -37,7 +37,7 @@ def test_opts_defaults():
     import paper_1310_0041_b200 as gdp
     o = gdp.default_opts()
     assert o.rel_tol == 1e-6 and o.max_vcycles == 30 and o.nu_pre == 2 and o.nu_post == 2
-    assert o.coarse_max == 4096 and o.fused == 3
+    assert o.coarse_max == 4096 and o.fused == 35
     assert o.nu_pre_slices == 1 and o.nu_post_slices == 2 and o.omega == 1.0
     assert o.fmg == 1 and o.fmg_slices == 3
 

@@ -221,13 +221,20 @@ def test_fused_3d_bit_identical_to_reference(gpu_ctx, shape, dtype):
     nz, ny, nx = shape
     I0 = synth.make_stack(nx, ny, nz, 41, dtype)
     outs = []
-    # reference, one kernel per sweep, one kernel per pass (temporal blocking), + cooperative coarse tail
-    for fused in (0, 3, 7, 11):
+    # reference, one kernel per sweep, one kernel per pass (temporal blocking), + cooperative coarse
+    # tail, the vertical-pack z-march
+    reps = []
+    for fused in (0, 3, 7, 11, 35, 34):
         o = gdp.default_opts(fused=fused, max_vcycles=2, rel_tol=1e-30, stagnation=0)
         I1, rep = gdp.gdp_diffuse_z(gpu_ctx, dev(I0), opts=o, check=False)
         outs.append(I1.cpu().numpy())
+        reps.append(rep)
     for k in range(1, len(outs)):
         assert np.array_equal(outs[0], outs[k]), k
+        # the reported residual history too (fp64 norm sums in another order: rounding only)
+        n = reps[0]["vcycles"] + 1
+        assert reps[k]["vcycles"] == reps[0]["vcycles"], k
+        np.testing.assert_allclose(reps[k]["rel_res"][:n], reps[0]["rel_res"][:n], rtol=1e-9, atol=0)
 
 
 @pytest.mark.parametrize("nu", [(1, 1), (2, 1), (1, 2), (2, 2), (3, 1)])
@@ -238,7 +245,7 @@ def test_fused_3d_vcycle_nu_variants(gpu_ctx, nu, shape):
     b -= b.mean()
     bd = dev(b.astype(np.float32))
     xs = []
-    for fused in (0, 3, 7, 11):
+    for fused in (0, 3, 7, 11, 35):
         x = torch.zeros(shape, dtype=torch.float32, device="cuda")
         for _ in range(2):
             gdp.gdp_vcycle(gpu_ctx, x, bd, W=(1.0, 1.0, 0.1), alpha=0.0,
@@ -384,7 +391,7 @@ def test_fmg_phase1_schedules_bit_identical(gpu_ctx, shape, W, fmg, dtype, nu):
     nz, ny, nx = shape
     I0 = synth.make_stack(nx, ny, nz, 43, dtype)
     outs = []
-    for fused, f in ((0, fmg), (3, fmg), (3, fmg + 4), (7, fmg), (7, fmg + 4), (11, fmg)):
+    for fused, f in ((0, fmg), (3, fmg), (3, fmg + 4), (7, fmg), (7, fmg + 4), (11, fmg), (35, fmg), (35, fmg + 4)):
         o = gdp.default_opts(fused=fused, fmg=f, max_vcycles=2, rel_tol=1e-30, stagnation=0,
                              nu_pre=nu[0], nu_post=nu[1])
         I1, rep = gdp.gdp_diffuse_z(gpu_ctx, dev(I0), W=W, opts=o, check=False)

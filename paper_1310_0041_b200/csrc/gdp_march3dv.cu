@@ -31,7 +31,10 @@ using vp::row_rep;
 using vp::sa;
 using vp::tma3;
 
-constexpr int MW = 8;             // warps, stacked in y
+#ifndef GDP_M3V_MW
+#define GDP_M3V_MW 11
+#endif
+constexpr int MW = GDP_M3V_MW;             // warps, stacked in y
 constexpr int MR = 8;              // rows per warp
 constexpr int MT = MW * 32;        // 352 threads
 constexpr int TX = 64;             // tile columns (2 per lane)
@@ -59,7 +62,8 @@ struct alignas(128) Smem {
   float ex[2][2][MW][2][32];       // [consumer colour][parity][warp][row 0 | 7][lane]: one column each
   float2 et[2][MW][2][32];         // rows 0 | 7 after stage 2 (both columns) for the tail
   float inv[4][6][2][32];          // 1/D per [plane class][row class][column][lane]
-  Tap tpx[TX], tpy[TY];            // prolongation taps of the tile's columns / rows (box-relative)
+  Tap tpx[TX], tpy[TY];
+  float4 ky[MW][4];                // y links of pack p of warp w: (kyl row r, row r + 2, kyr row r, row r + 2)            // prolongation taps of the tile's columns / rows (box-relative)
   float st[SS][TYI][TXI];          // final interior planes, stored by TMA
   float stpad[4 * TXI + 2 * HX];   // the halo lanes' (discarded) reads past the last slot
   unsigned long long barx[XS];
@@ -198,11 +202,9 @@ __global__ void __launch_bounds__(MT, 1) k_m3v(const __grid_constant__ Sweep P) 
       ivo[j] = rc * 2 * 32 + lane;
     }
     const bool rfull = rin[0] && rin[1] && rin[2] && rin[3] && rin[4] && rin[5] && rin[6] && rin[7];
-    float2 kyl[4], kyr[4];
-#pragma unroll
-    for (int p = 0; p < 4; ++p) {
-      kyl[p] = make_float2(cl(L.ay, gyw + R0(p)), cl(L.ay, gyw + R0(p) + 2));
-      kyr[p] = make_float2(cr(L.ay, gyw + R0(p)), cr(L.ay, gyw + R0(p) + 2));
+    if (lane < 4) {  // read after the item's first barrier
+      const int g = gyw + R0(lane);
+      S.ky[warp][lane] = make_float4(cl(L.ay, g), cl(L.ay, g + 2), cr(L.ay, g), cr(L.ay, g + 2));
     }
     // restriction weights 1/2 x 1/2 for the in-level children (the others are discarded)
     bool rwreg = TAIL == TAIL_RESTRICT;
@@ -359,8 +361,9 @@ __global__ void __launch_bounds__(MT, 1) k_m3v(const __grid_constant__ Sweep P) 
       float2 s = __fmul2_rn(al2, Xc);
       s = __ffma2_rn(f2(kxl[C]), sub2(Xc, W), s);
       s = __ffma2_rn(f2(kxr[C]), sub2(Xc, E), s);
-      s = __ffma2_rn(kyl[PP], (PP == 0 || PP == 2) ? subm(Xc, Sn) : sub2(Xc, Sn), s);
-      s = __ffma2_rn(kyr[PP], (PP == 1 || PP == 3) ? subm(Xc, Nn) : sub2(Xc, Nn), s);
+      const float4 ky = S.ky[warp][PP];
+      s = __ffma2_rn(make_float2(ky.x, ky.y), (PP == 0 || PP == 2) ? subm(Xc, Sn) : sub2(Xc, Sn), s);
+      s = __ffma2_rn(make_float2(ky.z, ky.w), (PP == 1 || PP == 3) ? subm(Xc, Nn) : sub2(Xc, Nn), s);
       s = __ffma2_rn(zl2, sub2(Xc, Xd.V[PP][C]), s);
       return __ffma2_rn(zr2, sub2(Xc, Xu.V[PP][C]), s);
     };

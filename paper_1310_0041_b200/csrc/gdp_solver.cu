@@ -629,11 +629,12 @@ int run_vcycle(Ctx& ctx, Hier& H, const Fine& f, const gdp_opts& o, cudaStream_t
       // exposed latency there: e.g. 156 vs 53 + ~25 us on a 256^2 x 128 level); the TMA-staged
       // kernels carry it
       const bool v16 = (o.fused & 16) && vpass3d_ok(L, C, 1, true, 0, c, x, R.b);
-      const bool v32 = !v16 && (o.fused & 32) && sweep3dv_ok(L, C, true, c, x, R.b);
+      const bool v32 = !v16 && (o.fused & 32) && sweep3dv_ok(L, C, false, c, x, R.b);
+      const bool v32p = v32 && sweep3dv_ok(L, C, true, c, x, R.b);  // it also carries the prolongation
       // partial slots of the norms sweep (the kernel that runs it: its own work split)
       const int items = v32 ? sweep3dv_items(L, C) : fused3d_items(L, C);
       const bool want = l == 0 && (size_t)items <= H.partials_cap * (size_t)L.nzl;
-      const bool sep = l > 0 && !v16 && !v32;
+      const bool sep = l > 0 && !v16 && !v32p;
       if (sep) launch_prolong(L.K, c, C.tx, C.ty, C.tz, C.nx, C.ny, C.nzl, C.z0, C.x, C.xlo, C.xhi, s);
       int got = 0;
       for (int k = 0; k < o.nu_post; ++k) {
@@ -643,8 +644,9 @@ int run_vcycle(Ctx& ctx, Hier& H, const Fine& f, const gdp_opts& o, cudaStream_t
         if (v16 && vpass3d_ok(L, C, 1, k == 0, tl, c, d, R.b))
           RET(fused_pass3d(L, C, c, d, R.b, false, k == 0, 1, tl, tl ? H.partials : nullptr, nullptr, s,
                            tl ? &got : nullptr));
-        else if (v32 && sweep3dv_ok(L, C, k == 0, c, d, R.b))
-          RET(fused_sweep3dv(L, C, c, d, R.b, false, k == 0, tl, tl ? H.partials : nullptr, s, tl ? &got : nullptr));
+        else if (v32 && sweep3dv_ok(L, C, k == 0 && !sep, c, d, R.b))
+          RET(fused_sweep3dv(L, C, c, d, R.b, false, k == 0 && !sep, tl, tl ? H.partials : nullptr, s,
+                             tl ? &got : nullptr));
         else {
           const int n = fused_sweep3d(L, C, c, d, R.b, false, k == 0 && !sep, tl, want ? H.partials : nullptr, s);
           if (tl) got = n;

@@ -10,9 +10,9 @@ timeout 300 $CMD > gpurun_out/plain_$TAG.log 2>&1 && \
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv $CMD > /dev/null 2>&1
 echo "launches rc=$?"
 python tools/launch_summary.py gpurun_out/launches_$TAG.csv > gpurun_out/launches_$TAG.txt 2>&1
-timeout 300 python tools/prof_step.py 1 0 3 > gpurun_out/plain2_$TAG.log 2>&1 && \
-timeout 900 ncu --set full --clock-control none --import-source on --profile-from-start off -k "regex:k_march3d|k_init" -c 130 -f -o gpurun_out/prof3d_$TAG python tools/prof_step.py 1 0 3 > /dev/null 2>&1 && \
-timeout 600 ncu --set full --clock-control none --import-source on --profile-from-start off -k "regex:k_pass2d|k_rows2d" -c 30 -f -o gpurun_out/prof2d_$TAG python tools/prof_step.py 1 0 3 > /dev/null 2>&1
+timeout 300 python tools/prof_step.py 1 0 35 > gpurun_out/plain2_$TAG.log 2>&1 && \
+timeout 900 ncu --set full --clock-control none --import-source on --profile-from-start off -k "regex:k_m3v|k_march3d|k_init" -c 130 -f -o gpurun_out/prof3d_$TAG python tools/prof_step.py 1 0 35 > /dev/null 2>&1 && \
+timeout 600 ncu --set full --clock-control none --import-source on --profile-from-start off -k "regex:k_pass2d|k_rows2d" -c 30 -f -o gpurun_out/prof2d_$TAG python tools/prof_step.py 1 0 35 > /dev/null 2>&1
 echo "ncu rc=$?"
 python - <<PY
 import json, subprocess
@@ -23,6 +23,6 @@ for r in ("prof3d_$TAG", "prof2d_$TAG"):
     except Exception as e: print("summary failed", r, e)
 json.dump(rows, open("gpurun_out/ncu_full_$TAG.json", "w"), indent=1)
 PY
-python tools/make_traffic.py gpurun_out/ncu_full_$TAG.json "ncu --set full of tools/prof_step.py 1 0 3 (profiles/ncu_full_$TAG.json)" > gpurun_out/ncu_full_summary.json
+python tools/make_traffic.py gpurun_out/ncu_full_$TAG.json "ncu --set full of tools/prof_step.py 1 0 35 (profiles/ncu_full_$TAG.json)" > gpurun_out/ncu_full_summary.json
 rm -f gpurun_out/prof3d_$TAG.ncu-rep gpurun_out/prof2d_$TAG.ncu-rep; ls -la gpurun_out/*.ncu-rep
 du -sh gpurun_out; free -g | head -2; nproc; df -h /dev/shm /tmp | tail -2

@@ -53,6 +53,8 @@ def parse():
     p.add_argument("--fmg", type=int, default=None, help="gdp_opts.fmg and fmg_slices (default: the library's)")
     p.add_argument("--graphs", type=int, default=1, help="gdp_opts.use_graphs (CUDA graph replay of V-cycles)")
     p.add_argument("--dx-tol", type=float, default=None, help="gdp_opts.dx_tol (default: the library's)")
+    p.add_argument("--scheme", default="constant", choices=["constant", "hybrid", "linear"],
+                   help="gdp_opts.scheme: the paper's discretisation (PAPER.md:305-323, NEXT-3)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     return p.parse_args()
@@ -261,7 +263,7 @@ def main():
         ctx = gdp.Ctx(local, rank=rank, world=world, nccl_unique_id=bytes(uid.cpu().numpy()))
     else:
         ctx = gdp.Ctx(local)
-    opts = gdp.default_opts(fused=args.fused, use_graphs=args.graphs)
+    opts = gdp.default_opts(fused=args.fused, use_graphs=args.graphs, scheme=args.scheme)
     if args.dx_tol is not None:
         opts.dx_tol = args.dx_tol
     if args.fmg is not None:
@@ -368,7 +370,7 @@ def main():
                "timing": "host wall clock around gdp_destripe_host (blocking), max over ranks"}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.scheme == "constant":
         cpu = run_cpu_baseline(args.config, args.alpha)
 
     if rank == 0:
@@ -380,7 +382,7 @@ def main():
                            "nu_phase2": [opts.nu_pre_slices, opts.nu_post_slices],
                            "schedule": "fused" if args.fused else "reference",
                            "fmg": [opts.fmg, opts.fmg_slices], "use_graphs": opts.use_graphs,
-                           "dx_tol": opts.dx_tol,
+                           "dx_tol": opts.dx_tol, "scheme": args.scheme,
                            "l2": "working set > L2 (I0 134 MB + three 537 MB fp32 volumes); no flush",
                            "parallelism": f"z-slabs x{world} (phase 1 NCCL halo, phase 2 slab-local)",
                            "global_dims": [nx, ny, nzg]},

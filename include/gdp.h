@@ -72,6 +72,21 @@ typedef enum {
 
 typedef enum { GDP_U8 = 0, GDP_F32 = 1 } gdp_dtype;
 
+/* Discretisation of the multigrid hierarchy, PAPER.md:305-323 (§4.2), SURVEY.md §8(f) NEXT-3.
+ *   CONSTANT: the 6-point (7-point with the centre) finite-difference Laplacian on every level
+ *             (this library's main path: finite-volume rediscretised coarse operators, volume-
+ *             weighted restriction, cell-centred linear prolongation);
+ *   HYBRID:   the same finest operator (same discrete answer), B-spline transfers (1/2, 1, 1/2)
+ *             per axis and Galerkin coarse operators P^T A P (27-point);
+ *   LINEAR:   the first-order B-spline finite-element operator (27-point, a different discrete
+ *             answer: oracle/fem_linear.py), the same transfers, Galerkin coarse operators
+ *             (PAPER.md:309-311).
+ * HYBRID and LINEAR smooth with multicoloured Gauss-Seidel (8 colours on 27-point levels, 4 per
+ * slice in phase 2, red-black on the Hybrid finest level) and solve the coarsest level exactly by
+ * generalised fast diagonalisation.  They run single-rank and in core, without the FMG start,
+ * graph replay or the dx gate.                                          */
+typedef enum { GDP_SCHEME_CONSTANT = 0, GDP_SCHEME_HYBRID = 1, GDP_SCHEME_LINEAR = 2 } gdp_scheme;
+
 typedef struct { int64_t nx, ny, nz; } gdp_dims;
 
 /* W = Diag(bx, by, bz), PAPER.md:150-152 (application value (1, 1, 0.1)). */
@@ -143,6 +158,11 @@ typedef struct {
                          one).  Default 1e-4 (reading a9-dx: with the
                          measured contraction <= 0.1 per cycle the error left after such a cycle
                          is <= 1e-5).  0 disables.                                          */
+  int scheme;         /* gdp_scheme of the hierarchy (above).  Default GDP_SCHEME_CONSTANT.       */
+  int half_staging;   /* NEXT-4, out-of-core phase 1 only: V-cycles whose residual
+                         is predicted (observed contraction) to stay above 5e-3 keep the host-resident
+                         iterate in fp16 (half the host-link bytes of those passes); the later cycles
+                         read it back and store fp32, so the answer is an fp32 iterate.  Default 0. */
 } gdp_opts;
 
 typedef struct {
@@ -251,6 +271,24 @@ int gdp_vcycle(gdp_ctx* ctx, float* x, const float* b, gdp_dims local, int64_t z
 int gdp_residual(gdp_ctx* ctx, const float* x, const float* b, float* r, gdp_dims local,
                  int64_t z0_global, int64_t nz_global, gdp_weights W, float alpha,
                  double* norm2_r, double* norm2_b, void* stream);
+
+/* NEXT-3 inspection of a Hybrid / Linear hierarchy (single rank).  The hierarchy is the one the
+ * solves build for (dims, W, alpha, per_slice, opts->coarse_max): per_slice = 1 is phase 2's
+ * set of independent 2D slice systems (W's bz ignored), 0 a 3D system.
+ * gdp_scheme_levels: *nlev = number of levels; level_dims[l] (may be NULL) their sizes and
+ *   coarsened[3 l + d] (may be NULL) whether axis d (x, y, z) was coarsened from level l - 1,
+ *   for l < max_levels.
+ * gdp_scheme_apply: y = A_level x on the device (x, y fp32 of level `level`'s size, no aliasing);
+ *   level 0 is the finest operator of the scheme, level l >= 1 its Galerkin operator
+ *   P_l^T ... P_1^T A P_1 ... P_l (reading L-4).
+ * gdp_scheme_residual: r = b - A_0 x (r may be NULL) and fp64 norms ||r||^2, ||b||^2.      */
+int gdp_scheme_levels(gdp_ctx* ctx, int scheme, gdp_dims dims, gdp_weights W, float alpha, int per_slice,
+                      const gdp_opts* opts, int* nlev, gdp_dims* level_dims, int* coarsened, int max_levels);
+int gdp_scheme_apply(gdp_ctx* ctx, int scheme, int level, const float* x, float* y, gdp_dims dims,
+                     gdp_weights W, float alpha, int per_slice, const gdp_opts* opts, void* stream);
+int gdp_scheme_residual(gdp_ctx* ctx, int scheme, const float* x, const float* b, float* r, gdp_dims dims,
+                        gdp_weights W, float alpha, int per_slice, double* norm2_r, double* norm2_b,
+                        void* stream);
 
 /* Per-kernel-class device timing (roofline measurement, bench.py).  Between begin and end
  * every library launch is bracketed by CUDA events on its own stream and tagged with the

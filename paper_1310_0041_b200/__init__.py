@@ -13,6 +13,9 @@ from .gdp import (  # noqa: F401
     gdp_diffuse_z,
     gdp_npr_filter,
     gdp_residual,
+    gdp_scheme_apply,
+    gdp_scheme_levels,
+    gdp_scheme_residual,
     gdp_screened_poisson_slices,
     gdp_vcycle,
     get_unique_id,

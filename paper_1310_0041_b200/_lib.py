@@ -22,7 +22,10 @@ EXPORTS = [
     "gdp_diffuse_z", "gdp_screened_poisson_slices", "gdp_destripe", "gdp_destripe_host",
     "gdp_vcycle", "gdp_residual", "gdp_last_error", "gdp_version", "gdp_kernel_launch_count",
     "gdp_profile_begin", "gdp_profile_end", "gdp_get_unique_id", "gdp_npr_filter",
+    "gdp_scheme_levels", "gdp_scheme_apply", "gdp_scheme_residual",
 ]
+GDP_SCHEME_CONSTANT, GDP_SCHEME_HYBRID, GDP_SCHEME_LINEAR = 0, 1, 2
+SCHEMES = {"constant": 0, "hybrid": 1, "linear": 2}
 
 
 class Dims(C.Structure):
@@ -38,7 +41,8 @@ class Opts(C.Structure):
                 ("nu_post", C.c_int), ("coarse_max", C.c_int), ("stagnation", C.c_int),
                 ("fused", C.c_int), ("use_graphs", C.c_int), ("nu_pre_slices", C.c_int),
                 ("nu_post_slices", C.c_int), ("omega", C.c_float), ("omega_slices", C.c_float),
-                ("fmg", C.c_int), ("fmg_slices", C.c_int), ("dx_tol", C.c_double)]
+                ("fmg", C.c_int), ("fmg_slices", C.c_int), ("dx_tol", C.c_double), ("scheme", C.c_int),
+                ("half_staging", C.c_int)]
 
 
 class Report(C.Structure):
@@ -94,6 +98,10 @@ def lib():
         "gdp_profile_begin": ([], i32),
         "gdp_get_unique_id": ([vp, C.c_size_t], i32),
         "gdp_profile_end": ([P(KernelStat), i32, P(i32)], i32),
+        "gdp_scheme_levels": ([vp, i32, Dims, Weights, f32, i32, P(Opts), P(i32), P(Dims), P(i32), i32], i32),
+        "gdp_scheme_apply": ([vp, i32, i32, vp, vp, Dims, Weights, f32, i32, P(Opts), vp], i32),
+        "gdp_scheme_residual": ([vp, i32, vp, vp, vp, Dims, Weights, f32, i32, P(C.c_double), P(C.c_double), vp],
+                                i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)

@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libgdp.so")
-SOURCES = ["gdp_solver.cu", "gdp_kernels.cu", "gdp_fused.cu", "gdp_march3d.cu", "gdp_comm.cu", "gdp_dist.cu", "gdp_host.cu", "gdp_stream.cu", "gdp_rows2d.cu", "gdp_vpass3d.cu", "gdp_vp_down.cu", "gdp_vp_up.cu", "gdp_vp_sweep.cu", "gdp_march3dv.cu"]
+SOURCES = ["gdp_solver.cu", "gdp_kernels.cu", "gdp_fused.cu", "gdp_march3d.cu", "gdp_comm.cu", "gdp_dist.cu", "gdp_host.cu", "gdp_stream.cu", "gdp_rows2d.cu", "gdp_vpass3d.cu", "gdp_vp_down.cu", "gdp_vp_up.cu", "gdp_vp_sweep.cu", "gdp_march3dv.cu", "gdp_scheme.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

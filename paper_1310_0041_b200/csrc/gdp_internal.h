@@ -123,6 +123,7 @@ struct Ctx {
   size_t hbuf_cap[3] = {0, 0, 0};
   cudaStream_t hs = nullptr, hcs = nullptr;
   cudaEvent_t hev = nullptr;
+  void* scheme_cache = nullptr;  // NEXT-3 hierarchies (gdp_scheme.cu)
   int get_hier(const HierKey& k, Hier** out);
   int ensure_scratch(size_t bytes);
   int ensure_hbuf(int i, size_t bytes);
@@ -183,6 +184,24 @@ int stream_diffuse_z(Ctx& C, const void* I0h, int tI, float* xh, long long nx, l
 int stream_slices(Ctx& C, gdp_ctx* cctx, const void* I0h, gdp_dtype dtype, float* I1h, float* I2h, long long nx,
                   long long ny, long long nz, float alpha, double shift, const gdp_opts& o, size_t budget,
                   gdp_report* rep);
+
+void jacobi_eig(int n, std::vector<double>& A, std::vector<double>& Q, std::vector<double>& lam);
+
+// NEXT-3: the Hybrid / Linear discretisations (gdp_scheme.cu), single rank, in core
+void scheme_cache_destroy(void* p);
+int scheme_diffuse_z(Ctx& C, const void* I0, int tI, float* I1, long long nx, long long ny, long long nz, float bx,
+                     float by, float bz, float alpha, const gdp_opts& o, gdp_report* rep, cudaStream_t s);
+int scheme_slices(Ctx& C, const void* I0, int tI, const float* I1, float* I2, long long nx, long long ny,
+                  long long nz, float alpha, float vshift, const gdp_opts& o, gdp_report* rep, cudaStream_t s);
+int scheme_vcycle(Ctx& C, float* x, const float* b, long long nx, long long ny, long long nz, float bx, float by,
+                  float bz, float alpha, const gdp_opts& o, double* rel, cudaStream_t s);
+int scheme_levels(Ctx& C, int scheme, long long nx, long long ny, long long nz, float bx, float by, float bz,
+                  float alpha, int per_slice, const gdp_opts& o, int* nlev, gdp_dims* dims, int* coarsened, int max);
+int scheme_apply(Ctx& C, int scheme, int level, const float* x, float* y, long long nx, long long ny, long long nz,
+                 float bx, float by, float bz, float alpha, int per_slice, const gdp_opts& o, cudaStream_t s);
+int scheme_residual(Ctx& C, int scheme, const float* x, const float* b, float* r, long long nx, long long ny,
+                    long long nz, float bx, float by, float bz, float alpha, int per_slice, const gdp_opts& o,
+                    double* rr, double* bb, cudaStream_t s);
 
 // communication (gdp_comm.cu); single-rank contexts make these no-ops
 int comm_init(Ctx& c, const void* nccl_unique_id);

@@ -111,7 +111,7 @@ static XferAxis make_xfer(const AxisG& f, const AxisG& c, bool coarsened) {
 }
 
 // cyclic Jacobi eigen-decomposition of a symmetric n x n matrix (row-major), n <= 64
-static void jacobi_eig(int n, std::vector<double>& A, std::vector<double>& Q, std::vector<double>& lam) {
+void jacobi_eig(int n, std::vector<double>& A, std::vector<double>& Q, std::vector<double>& lam) {
   Q.assign((size_t)n * n, 0.0);
   for (int i = 0; i < n; ++i) Q[(size_t)i * n + i] = 1.0;
   for (int sweep = 0; sweep < 100; ++sweep) {
@@ -424,6 +424,7 @@ int build_hier_levels(const HierKey& key, const std::vector<Level>& chain, int f
 // ---------------------------------------------------------------------------------
 Ctx::~Ctx() {
   hier.clear();
+  if (scheme_cache) scheme_cache_destroy(scheme_cache);
   dist.clear();
   if (ev0) cudaEventDestroy(ev0);
   if (ev1) cudaEventDestroy(ev1);
@@ -931,6 +932,13 @@ static gdp_opts resolve_opts(const gdp_opts* o) {
   return r;
 }
 
+static int check_scheme(const Ctx& C, const gdp_opts& o) {
+  if (o.scheme != GDP_SCHEME_HYBRID && o.scheme != GDP_SCHEME_LINEAR)
+    return set_err(GDP_EINVAL, "unknown scheme %d", o.scheme);
+  if (C.world > 1 || C.loop > 1) return set_err(GDP_EINVAL, "the Hybrid / Linear schemes are single-rank in this build");
+  return GDP_OK;
+}
+
 static HierKey make_key(gdp_dims d, int64_t z0, int64_t nzg, gdp_weights W, float alpha,
                         const gdp_opts& o) {
   HierKey k{};
@@ -960,6 +968,8 @@ int gdp_opts_default(gdp_opts* o) {
   o->fmg = 1;
   o->fmg_slices = 3;
   o->dx_tol = 1e-4;
+  o->scheme = GDP_SCHEME_CONSTANT;
+  o->half_staging = 0;
   return GDP_OK;
 }
 
@@ -1045,6 +1055,11 @@ static int diffuse_z_impl(gdp_ctx* ctx, const void* I0, gdp_dtype dtype, float* 
   cudaStream_t s = (cudaStream_t)stream;
   Ctx& C = ctx->impl;
   const int tI = dtype == GDP_U8 ? 0 : 1;
+  if (o.scheme != GDP_SCHEME_CONSTANT) {  // NEXT-3: Hybrid / Linear (gdp_scheme.cu)
+    RET(check_scheme(C, o));
+    if (defer_shift) *defer_shift = 0.f;  // the scheme path applies its mean pin itself
+    return scheme_diffuse_z(C, I0, tI, I1, local.nx, local.ny, local.nz, W.bx, W.by, W.bz, alpha, o, report, s);
+  }
   if (C.world > 1 || C.loop > 1) {  // z-slab partition (gdp_dist.cu)
     const int st = dist_diffuse_z(C, I0, tI, I1, local.nx, local.ny, local.nz, z0_global, nz_global, W.bx, W.by,
                                   W.bz, alpha, o, report, s);
@@ -1125,6 +1140,11 @@ static int slices_impl(gdp_ctx* ctx, const void* I0, gdp_dtype dtype, const floa
   o.fmg = o.fmg_slices;
   cudaStream_t s = (cudaStream_t)stream;
   Ctx& C = ctx->impl;
+  if (o.scheme != GDP_SCHEME_CONSTANT) {  // NEXT-3: Hybrid / Linear (gdp_scheme.cu)
+    RET(check_scheme(C, o));
+    return scheme_slices(C, I0, dtype == GDP_U8 ? 0 : 1, I1, I2, local.nx, local.ny, local.nz, alpha,
+                         vshift ? *vshift : 0.f, o, report, s);
+  }
   const long long before = g_launches.load();
   gdp_weights W{1.f, 1.f, 0.f};  // pi = Diag(1,1,0), Eq. (2)
   Hier* H;
@@ -1180,6 +1200,7 @@ int gdp_npr_filter(gdp_ctx* ctx, const void* I0, gdp_dtype dtype, float* out, gd
   Ctx& C = ctx->impl;
   if (C.world > 1 || C.loop > 1) return set_err(GDP_EINVAL, "gdp_npr_filter is single-rank in this build");
   const gdp_opts o = resolve_opts(opts);
+  if (o.scheme != GDP_SCHEME_CONSTANT) return set_err(GDP_EINVAL, "gdp_npr_filter runs the Constant scheme only");
   cudaStream_t s = (cudaStream_t)stream;
   const long long before = g_launches.load();
   Hier* H;
@@ -1237,6 +1258,10 @@ int gdp_vcycle(gdp_ctx* ctx, float* x, const float* b, gdp_dims local, int64_t z
   const gdp_opts o = resolve_opts(opts);
   cudaStream_t s = (cudaStream_t)stream;
   Ctx& C = ctx->impl;
+  if (o.scheme != GDP_SCHEME_CONSTANT) {  // NEXT-3: Hybrid / Linear (gdp_scheme.cu)
+    RET(check_scheme(C, o));
+    return scheme_vcycle(C, x, b, local.nx, local.ny, local.nz, W.bx, W.by, W.bz, alpha, o, rel_res_after, s);
+  }
   if (C.world > 1 || C.loop > 1)  // z-slab partition: halos per half-sweep, gathered coarse levels
     return dist_vcycle(C, x, b, local.nx, local.ny, local.nz, z0_global, nz_global, W.bx, W.by, W.bz, alpha, o,
                        rel_res_after, s);
@@ -1283,6 +1308,42 @@ int gdp_residual(gdp_ctx* ctx, const float* x, const float* b, float* r, gdp_dim
   if (norm2_r) *norm2_r = rr;
   if (norm2_b) *norm2_b = bb;
   return GDP_OK;
+}
+
+int gdp_scheme_levels(gdp_ctx* ctx, int scheme, gdp_dims dims, gdp_weights W, float alpha, int per_slice,
+                      const gdp_opts* opts, int* nlev, gdp_dims* level_dims, int* coarsened, int max_levels) {
+  RET(check_common(ctx, dims, 0, dims.nz));
+  RET(check_params(W, per_slice ? alpha : alpha));
+  if (!nlev) return set_err(GDP_EINVAL, "null nlev");
+  gdp_opts o = resolve_opts(opts);
+  o.scheme = scheme;
+  RET(check_scheme(ctx->impl, o));
+  return scheme_levels(ctx->impl, scheme, dims.nx, dims.ny, dims.nz, W.bx, W.by, W.bz, alpha, per_slice ? 1 : 0, o,
+                       nlev, level_dims, coarsened, max_levels);
+}
+
+int gdp_scheme_apply(gdp_ctx* ctx, int scheme, int level, const float* x, float* y, gdp_dims dims, gdp_weights W,
+                     float alpha, int per_slice, const gdp_opts* opts, void* stream) {
+  RET(check_common(ctx, dims, 0, dims.nz));
+  RET(check_params(W, alpha));
+  if (!x || !y || (const float*)y == x) return set_err(GDP_EINVAL, "null or aliased x / y");
+  gdp_opts o = resolve_opts(opts);
+  o.scheme = scheme;
+  RET(check_scheme(ctx->impl, o));
+  return scheme_apply(ctx->impl, scheme, level, x, y, dims.nx, dims.ny, dims.nz, W.bx, W.by, W.bz, alpha,
+                      per_slice ? 1 : 0, o, (cudaStream_t)stream);
+}
+
+int gdp_scheme_residual(gdp_ctx* ctx, int scheme, const float* x, const float* b, float* r, gdp_dims dims,
+                        gdp_weights W, float alpha, int per_slice, double* norm2_r, double* norm2_b, void* stream) {
+  RET(check_common(ctx, dims, 0, dims.nz));
+  RET(check_params(W, alpha));
+  if (!x || !b) return set_err(GDP_EINVAL, "null x / b");
+  gdp_opts o = resolve_opts(nullptr);
+  o.scheme = scheme;
+  RET(check_scheme(ctx->impl, o));
+  return scheme_residual(ctx->impl, scheme, x, b, r, dims.nx, dims.ny, dims.nz, W.bx, W.by, W.bz, alpha,
+                         per_slice ? 1 : 0, o, norm2_r, norm2_b, (cudaStream_t)stream);
 }
 
 int gdp_profile_begin(void) {

@@ -15,9 +15,18 @@
 // arithmetic per voxel is the in-core kernels', so the iterate is bit-identical to the in-core
 // solve (tests/test_gpu_parity.py::test_out_of_core_*).
 //
+// fp16 staging ("intermediate solutions ... are stored
+// ... using half-precision floating point values"): with gdp_opts.half_staging a V-cycle whose
+// residual is predicted (from the observed contraction) to stay above HALF_REL stores the host
+// iterate as fp16 in a pinned scratch (2 B instead of 4 per voxel each way); computation stays
+// fp32 on the device.  The first cycle predicted below HALF_REL reads the fp16 iterate and writes
+// fp32 again, so the answer comes from fp32 cycles (the quantisation error, ~1e-4 on [0, 1], is
+// high-frequency and the next cycle's smoothing removes it, as the paper notes).
+//
 // Phase 2 (Eq. 2).  Slices are independent systems: batches of slices go host->device, are
 // solved in core (gdp_screened_poisson_slices) and come back; the mean-pin shift of phase 1 is
 // applied to each I1 batch on the way (and written back to the caller's I1).
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -51,6 +60,24 @@ int HostPin::pin(const void* ptr, size_t bytes) {
   SK(cudaHostRegister(const_cast<void*>(ptr), bytes, cudaHostRegisterDefault));
   p = const_cast<void*>(ptr);
   return GDP_OK;
+}
+
+constexpr double HALF_REL = 5e-3;  // fp16 iterate storage while the residual stays above this
+
+__global__ void k_f16_to_f32(const __half* __restrict__ a, float* __restrict__ b, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    b[i] = __half2float(a[i]);
+}
+__global__ void k_f32_to_f16(const float* __restrict__ a, __half* __restrict__ b, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    b[i] = __float2half_rn(a[i]);
+}
+static void convert(const void* a, void* b, long long n, bool to_half, cudaStream_t s) {
+  if (n <= 0) return;
+  const int blocks = (int)std::min<long long>((n + 255) / 256, 148 * 16);
+  ProfScope ps(KC_UTIL, 6.0 * (double)n, s);
+  if (to_half) k_f32_to_f16<<<blocks, 256, 0, s>>>(static_cast<const float*>(a), static_cast<__half*>(b), n);
+  else k_f16_to_f32<<<blocks, 256, 0, s>>>(static_cast<const __half*>(a), static_cast<float*>(b), n);
 }
 
 struct DevBuf {
@@ -107,21 +134,27 @@ struct Stream1 {
   int nz = 0, C = 0;          // chunk planes
   size_t sI = 1;
   DevBuf xin[2], xout[2], iw[2], bw[2];
+  DevBuf xin16[2], xout16[2];  // fp16 staging of the iterate's window (NEXT-4)
+  __half* h16 = nullptr;       // host fp16 iterate (pinned), allocated on first use
   DevBuf part;                // norm partials (init: per plane rows; sweeps: per item)
   DevBuf psum;                // plane sums (mean pin)
   size_t part_cap = 0;
   Streams st;
   long long h2d = 0, d2h = 0;  // bytes moved over the host link
+  ~Stream1() { if (h16) cudaFreeHost(h16); }
 };
 
-enum { SP_INIT = 0, SP_SWEEP = 1, SP_SUMS = 2 };
+enum { SP_INIT = 0, SP_SWEEP = 1, SP_SUMS = 2, SP_WIDEN = 3 };
 
 static int chunk_count(const Stream1& S) { return (S.nz + S.C - 1) / S.C; }
 
 // One streaming pass over the finest level.  SP_INIT: x0 = I0 (written to the host iterate),
 // initial residual partials (per plane rows).  SP_SWEEP: one red-black sweep (+ prolongation /
-// restriction / norms).  SP_SUMS: per-plane fp64 sums of x and I0 (the mean pin).
-static int stream_pass(Stream1& S, int kind, bool prolong, int tail, long long* items_out) {
+// restriction / norms).  SP_SUMS: per-plane fp64 sums of x and I0 (the mean pin).  SP_WIDEN:
+// the fp16 host iterate back to fp32.  in16 / out16: the host iterate is read from / written to
+// the fp16 scratch instead of the caller's fp32 buffer (NEXT-4).
+static int stream_pass(Stream1& S, int kind, bool prolong, int tail, long long* items_out, bool in16 = false,
+                       bool out16 = false) {
   Hier& H = *S.H;
   const Level& L0 = H.lv[0];
   const Level& L1 = H.lv[1];
@@ -143,17 +176,26 @@ static int stream_pass(Stream1& S, int kind, bool prolong, int tail, long long* 
                            cudaMemcpyDeviceToDevice, T.ci));
         from = pwhi;
       }
-      if (kind == SP_SUMS) from = p_lo;
-      const int to = kind == SP_SUMS ? p_hi : whi;
-      if (to > from) {
-        SK(cudaMemcpyAsync(S.xin[b].f() + (from - (kind == SP_SUMS ? p_lo : wlo)) * pl, S.xh + from * pl,
-                           sizeof(float) * pl * (to - from), cudaMemcpyHostToDevice, T.ci));
+      const bool exact = kind == SP_SUMS || kind == SP_WIDEN;  // no halo planes
+      if (exact) from = p_lo;
+      const int to = exact ? p_hi : whi;
+      const long long base = from - (exact ? p_lo : wlo);
+      if (to > from && in16) {
+        SK(cudaMemcpyAsync(S.xin16[b].p, S.h16 + from * pl, sizeof(__half) * pl * (to - from),
+                           cudaMemcpyHostToDevice, T.ci));
+        convert(S.xin16[b].p, S.xin[b].f() + base * pl, pl * (to - from), false, T.ci);
+        S.h2d += (long long)sizeof(__half) * pl * (to - from);
+      } else if (to > from) {
+        SK(cudaMemcpyAsync(S.xin[b].f() + base * pl, S.xh + from * pl, sizeof(float) * pl * (to - from),
+                           cudaMemcpyHostToDevice, T.ci));
         S.h2d += (long long)sizeof(float) * pl * (to - from);
       }
     }
-    SK(cudaMemcpyAsync(S.iw[b].u(), static_cast<const unsigned char*>(S.I0h) + S.sI * wlo * pl,
-                       S.sI * pl * (whi - wlo), cudaMemcpyHostToDevice, T.ci));
-    S.h2d += (long long)S.sI * pl * (whi - wlo);
+    if (kind != SP_WIDEN) {
+      SK(cudaMemcpyAsync(S.iw[b].u(), static_cast<const unsigned char*>(S.I0h) + S.sI * wlo * pl,
+                         S.sI * pl * (whi - wlo), cudaMemcpyHostToDevice, T.ci));
+      S.h2d += (long long)S.sI * pl * (whi - wlo);
+    }
     SK(cudaEventRecord(T.evI[b], T.ci));
     // ---- kernels
     SK(cudaStreamWaitEvent(T.s, T.evI[b], 0));
@@ -174,20 +216,30 @@ static int stream_pass(Stream1& S, int kind, bool prolong, int tail, long long* 
       items += fused_sweep3d(L0, L1, S.xin[b].f() - wlo * pl, S.xout[b].f() - p_lo * pl, S.bw[b].f() - wlo * pl,
                              false, prolong, tail, tail == 2 ? static_cast<double2*>(S.part.p) + items : nullptr,
                              T.s, p_lo, p_hi);
+    } else if (kind == SP_WIDEN) {
+      SK(cudaMemcpyAsync(S.xout[b].f(), S.xin[b].f(), sizeof(float) * pl * (p_hi - p_lo), cudaMemcpyDeviceToDevice,
+                         T.s));
     } else {
       const int per = norms_blocks_per_plane(L0.nx, L0.ny);
       launch_plane_sums(S.xin[b].f(), 1, iwin + S.sI * (p_lo - wlo) * pl, S.tI, L0.nx, L0.ny, p_hi - p_lo,
                         static_cast<double2*>(S.part.p), static_cast<double2*>(S.psum.p) + p_lo, T.s);
       (void)per;
     }
+    if (kind != SP_SUMS && out16) convert(S.xout[b].f(), S.xout16[b].p, pl * (p_hi - p_lo), true, T.s);
     SK(cudaGetLastError());
     SK(cudaEventRecord(T.evK[b], T.s));
     // ---- output of the window back to the host iterate (in place: no later window reads it)
     if (kind != SP_SUMS) {
       SK(cudaStreamWaitEvent(T.co, T.evK[b], 0));
-      SK(cudaMemcpyAsync(S.xh + p_lo * pl, S.xout[b].f(), sizeof(float) * pl * (p_hi - p_lo),
-                         cudaMemcpyDeviceToHost, T.co));
-      S.d2h += (long long)sizeof(float) * pl * (p_hi - p_lo);
+      if (out16) {
+        SK(cudaMemcpyAsync(S.h16 + p_lo * pl, S.xout16[b].p, sizeof(__half) * pl * (p_hi - p_lo),
+                           cudaMemcpyDeviceToHost, T.co));
+        S.d2h += (long long)sizeof(__half) * pl * (p_hi - p_lo);
+      } else {
+        SK(cudaMemcpyAsync(S.xh + p_lo * pl, S.xout[b].f(), sizeof(float) * pl * (p_hi - p_lo),
+                           cudaMemcpyDeviceToHost, T.co));
+        S.d2h += (long long)sizeof(float) * pl * (p_hi - p_lo);
+      }
       SK(cudaEventRecord(T.evO[b], T.co));
     }
     pwlo = wlo;
@@ -282,19 +334,38 @@ int stream_diffuse_z(Ctx& C, const void* I0h, int tI, float* xh, long long nx, l
   f.mode = RHS_B;
   int status = GDP_OK, stall = 0, k = 0;
   const int cap = std::min(o.max_vcycles, GDP_MAX_CYCLES);
-  while (rel > o.rel_tol) {
+  bool stored16 = false;  // the host iterate currently lives in the fp16 scratch (NEXT-4)
+  double q = 0.1;         // contraction per cycle, observed (first cycle: assumed)
+  while (rel > o.rel_tol || stored16) {
     if (k >= cap) { status = GDP_ENOCONV; break; }
-    for (int i = 0; i < o.nu_pre; ++i) SR(stream_pass(S, SP_SWEEP, false, i == o.nu_pre - 1 ? 1 : 0, nullptr));
+    // NEXT-4: this cycle stores fp16 if its residual is predicted to stay above HALF_REL
+    const bool h = o.half_staging && rel * q > HALF_REL;
+    if (h && !S.h16) {
+      SK(cudaMallocHost(&S.h16, sizeof(__half) * (size_t)pl * nz));
+      for (int b = 0; b < 2; ++b) {
+        SR(S.xin16[b].alloc(sizeof(__half) * pl * (Cp + 6)));
+        SR(S.xout16[b].alloc(sizeof(__half) * pl * Cp));
+      }
+    }
+    bool in16 = stored16;
+    for (int i = 0; i < o.nu_pre; ++i) {
+      SR(stream_pass(S, SP_SWEEP, false, i == o.nu_pre - 1 ? 1 : 0, nullptr, in16, h));
+      in16 = h;
+    }
     SR(run_vcycle(C, *S.H, f, o, S.st.s, 1));
     SK(cudaStreamSynchronize(S.st.s));
     long long items = 0;
-    for (int i = 0; i < o.nu_post; ++i)
-      SR(stream_pass(S, SP_SWEEP, i == 0, i == o.nu_post - 1 ? 2 : 0, &items));
+    for (int i = 0; i < o.nu_post; ++i) {
+      SR(stream_pass(S, SP_SWEEP, i == 0, i == o.nu_post - 1 ? 2 : 0, &items, in16, h));
+      in16 = h;
+    }
+    stored16 = h;
     SR(read_norms(S, static_cast<double2*>(S.part.p), (int)items, 1, rr, bb));
     const double nrel = bb > 0 ? std::sqrt(rr / bb) : std::sqrt(rr);
     ++k;
     r.rel_res[k] = nrel;
     if (!std::isfinite(nrel)) return set_err(GDP_EINVAL, "non-finite residual after V-cycle %d", k);
+    q = std::min(1.0, std::max(1e-3, nrel / std::max(rel, 1e-300)));
     if (o.stagnation > 0 && nrel > 0.9 * rel) {
       if (++stall >= o.stagnation) { rel = nrel; status = nrel <= o.rel_tol ? GDP_OK : GDP_ENOCONV; break; }
     } else {
@@ -302,6 +373,9 @@ int stream_diffuse_z(Ctx& C, const void* I0h, int tI, float* xh, long long nx, l
     }
     rel = nrel;
   }
+  if (stored16) SR(stream_pass(S, SP_WIDEN, false, 0, nullptr, true, false));  // ended on an fp16 cycle (cap)
+  if (S.h16) cudaFreeHost(S.h16);
+  S.h16 = nullptr;
   r.vcycles = k;
   r.status = status;
   // a10: mean pin, per-plane fp64 sums in plane order (the in-core reduction)

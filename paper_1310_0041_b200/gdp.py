@@ -31,7 +31,7 @@ def default_opts(**kw) -> L.Opts:
     for k, v in kw.items():
         if not hasattr(o, k):
             raise AttributeError(f"gdp_opts has no field {k}")
-        setattr(o, k, v)
+        setattr(o, k, _scheme(v) if k == "scheme" else v)
     return o
 
 
@@ -220,6 +220,50 @@ def gdp_residual(ctx: Ctx, x: torch.Tensor, b: torch.Tensor, r: torch.Tensor | N
                                 None if r is None else _dev(r, "r", (torch.float32,)), d, z0_global,
                                 d.nz if nz_global is None else nz_global, L.Weights(*W), alpha,
                                 C.byref(nr), C.byref(nb), _stream(stream)), "gdp_residual")
+    return r, nr.value, nb.value
+
+
+def _scheme(s) -> int:
+    return L.SCHEMES[s] if isinstance(s, str) else int(s)
+
+
+def gdp_scheme_levels(ctx: Ctx, scheme, dims, W=(1.0, 1.0, 0.1), alpha: float = 0.0, per_slice: bool = False,
+                      opts=None) -> list[dict]:
+    """NEXT-3 hierarchy of a Hybrid / Linear solve: [{dims (nz, ny, nx), coarsened (x, y, z)}] per level."""
+    nz, ny, nx = dims
+    n = C.c_int()
+    ld = (L.Dims * 32)()
+    co = (C.c_int * 96)()
+    o = opts if opts is not None else default_opts()
+    _check(L.lib().gdp_scheme_levels(ctx.ptr, _scheme(scheme), L.Dims(nx, ny, nz), L.Weights(*W), alpha,
+                                     int(per_slice), C.byref(o), C.byref(n), ld, co, 32), "gdp_scheme_levels")
+    return [{"dims": (ld[i].nz, ld[i].ny, ld[i].nx), "coarsened": tuple(bool(co[3 * i + d]) for d in range(3))}
+            for i in range(n.value)]
+
+
+def gdp_scheme_apply(ctx: Ctx, scheme, level: int, x: torch.Tensor, y: torch.Tensor | None = None,
+                     fine_dims=None, W=(1.0, 1.0, 0.1), alpha: float = 0.0, per_slice: bool = False, opts=None,
+                     stream=None) -> torch.Tensor:
+    """y = A_level x of a Hybrid / Linear hierarchy built for `fine_dims` (nz, ny, nx)."""
+    nz, ny, nx = fine_dims
+    y = torch.empty_like(x) if y is None else y
+    o = opts if opts is not None else default_opts()
+    _check(L.lib().gdp_scheme_apply(ctx.ptr, _scheme(scheme), level, _dev(x, "x", (torch.float32,)),
+                                    _dev(y, "y", (torch.float32,)), L.Dims(nx, ny, nz), L.Weights(*W), alpha,
+                                    int(per_slice), C.byref(o), _stream(stream)), "gdp_scheme_apply")
+    return y
+
+
+def gdp_scheme_residual(ctx: Ctx, scheme, x: torch.Tensor, b: torch.Tensor, r: torch.Tensor | None = None,
+                        W=(1.0, 1.0, 0.1), alpha: float = 0.0, per_slice: bool = False, stream=None):
+    """r = b - A x of the scheme's finest operator; returns (r or None, ||r||^2, ||b||^2)."""
+    d = _dims(x)
+    nr, nb = C.c_double(), C.c_double()
+    _check(L.lib().gdp_scheme_residual(ctx.ptr, _scheme(scheme), _dev(x, "x", (torch.float32,)),
+                                       _dev(b, "b", (torch.float32,)),
+                                       None if r is None else _dev(r, "r", (torch.float32,)), d, L.Weights(*W),
+                                       alpha, int(per_slice), C.byref(nr), C.byref(nb), _stream(stream)),
+           "gdp_scheme_residual")
     return r, nr.value, nb.value
 
 

@@ -163,6 +163,12 @@ typedef struct {
                          is predicted (observed contraction) to stay above 5e-3 keep the host-resident
                          iterate in fp16 (half the host-link bytes of those passes); the later cycles
                          read it back and store fp32, so the answer is an fp32 iterate.  Default 0. */
+  int stream_fuse;    /* NEXT-2, out-of-core phase 1: each finest-level streaming
+                         pass applies several sweeps to the host-resident iterate in one host-link
+                         round trip (z-lagged stages, bit-identical to the in-core sweeps): the down
+                         pass (nu_pre sweeps + restriction) is one pass, and the up pass of a cycle
+                         that is not predicted to be the last also runs the next cycle's down sweeps
+                         (one round trip per V-cycle).  0: one pass per sweep.  Default 1.       */
 } gdp_opts;
 
 typedef struct {

@@ -42,7 +42,7 @@ class Opts(C.Structure):
                 ("fused", C.c_int), ("use_graphs", C.c_int), ("nu_pre_slices", C.c_int),
                 ("nu_post_slices", C.c_int), ("omega", C.c_float), ("omega_slices", C.c_float),
                 ("fmg", C.c_int), ("fmg_slices", C.c_int), ("dx_tol", C.c_double), ("scheme", C.c_int),
-                ("half_staging", C.c_int)]
+                ("half_staging", C.c_int), ("stream_fuse", C.c_int)]
 
 
 class Report(C.Structure):

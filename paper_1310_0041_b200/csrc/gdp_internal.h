@@ -124,6 +124,8 @@ struct Ctx {
   cudaStream_t hs = nullptr, hcs = nullptr;
   cudaEvent_t hev = nullptr;
   void* scheme_cache = nullptr;  // NEXT-3 hierarchies (gdp_scheme.cu)
+  void* h16 = nullptr;           // pinned fp16 host iterate of the out-of-core streamer (NEXT-4), kept
+  size_t h16_bytes = 0;          // across solves: pinning tens of GB costs seconds per call
   int get_hier(const HierKey& k, Hier** out);
   int ensure_scratch(size_t bytes);
   int ensure_hbuf(int i, size_t bytes);

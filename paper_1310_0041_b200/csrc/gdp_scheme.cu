@@ -772,7 +772,11 @@ static int ts_solve(TsHier& H, float* x, const float* b, const gdp_opts& o, int 
   if (rep) { rep->rel_res[0] = rel; rep->norm_b = nb; rep->levels = (int)H.lv.size(); rep->dx_inf = -1.0; }
   if (!std::isfinite(rel)) return set_err(GDP_ECUDA, "scheme: non-finite initial residual");
   int k = 0, stall = 0, st = GDP_OK;
-  while (rel > o.rel_tol) {
+  // the gate is taken on this path's fp32 residual with a 10 % margin, so that the fp64 residual of
+  // the fp32 iterate (the oracle's measure) also meets rel_tol (reading c-12: the 1e-6 gate is
+  // within a few ulps of the fp32 floor on small systems)
+  const double gate = 0.9 * o.rel_tol;
+  while (rel > gate) {
     if (k >= o.max_vcycles) { st = GDP_ENOCONV; break; }
     RETS(ts_cycle(H, x, b, nu_pre, nu_post, omega, s));
     double r2 = 0.0;
@@ -782,7 +786,7 @@ static int ts_solve(TsHier& H, float* x, const float* b, const gdp_opts& o, int 
     if (!std::isfinite(r2)) return set_err(GDP_ECUDA, "scheme: non-finite residual after cycle %d", k);
     stall = (r2 > 0.9 * rel) ? stall + 1 : 0;
     rel = r2;
-    if (o.stagnation > 0 && stall >= o.stagnation && rel > o.rel_tol) { st = GDP_ENOCONV; break; }
+    if (o.stagnation > 0 && stall >= o.stagnation && rel > gate) { st = rel <= o.rel_tol ? GDP_OK : GDP_ENOCONV; break; }
   }
   if (rep) { rep->vcycles = k; rep->status = st; }
   return st;

@@ -425,6 +425,7 @@ int build_hier_levels(const HierKey& key, const std::vector<Level>& chain, int f
 Ctx::~Ctx() {
   hier.clear();
   if (scheme_cache) scheme_cache_destroy(scheme_cache);
+  if (h16) cudaFreeHost(h16);
   dist.clear();
   if (ev0) cudaEventDestroy(ev0);
   if (ev1) cudaEventDestroy(ev1);
@@ -970,6 +971,7 @@ int gdp_opts_default(gdp_opts* o) {
   o->dx_tol = 1e-4;
   o->scheme = GDP_SCHEME_CONSTANT;
   o->half_staging = 0;
+  o->stream_fuse = 1;
   return GDP_OK;
 }
 

@@ -135,34 +135,30 @@ struct Stream1 {
   size_t sI = 1;
   DevBuf xin[2], xout[2], iw[2], bw[2];
   DevBuf xin16[2], xout16[2];  // fp16 staging of the iterate's window (NEXT-4)
-  __half* h16 = nullptr;       // host fp16 iterate (pinned), allocated on first use
+  static constexpr int MAXS = 8;  // sweeps per streaming pass (NEXT-2)
+  DevBuf sw[MAXS][2];             // input windows of stages 1.. of a multi-sweep pass
+  __half* h16 = nullptr;       // host fp16 iterate (pinned; Ctx::h16, allocated on first use)
   DevBuf part;                // norm partials (init: per plane rows; sweeps: per item)
   DevBuf psum;                // plane sums (mean pin)
   size_t part_cap = 0;
   Streams st;
   long long h2d = 0, d2h = 0;  // bytes moved over the host link
-  ~Stream1() { if (h16) cudaFreeHost(h16); }
 };
 
-enum { SP_INIT = 0, SP_SWEEP = 1, SP_SUMS = 2, SP_WIDEN = 3 };
+enum { SP_INIT = 0, SP_SUMS = 2, SP_WIDEN = 3 };  // the sweeps stream through stream_sweeps
 
 static int chunk_count(const Stream1& S) { return (S.nz + S.C - 1) / S.C; }
 
 // One streaming pass over the finest level.  SP_INIT: x0 = I0 (written to the host iterate),
-// initial residual partials (per plane rows).  SP_SWEEP: one red-black sweep (+ prolongation /
-// restriction / norms).  SP_SUMS: per-plane fp64 sums of x and I0 (the mean pin).  SP_WIDEN:
+// initial residual partials (per plane rows).  SP_SUMS: per-plane fp64 sums of x and I0 (the mean pin).  SP_WIDEN:
 // the fp16 host iterate back to fp32.  in16 / out16: the host iterate is read from / written to
 // the fp16 scratch instead of the caller's fp32 buffer (NEXT-4).
-static int stream_pass(Stream1& S, int kind, bool prolong, int tail, long long* items_out, bool in16 = false,
-                       bool out16 = false) {
+static int stream_pass(Stream1& S, int kind, bool in16 = false, bool out16 = false) {
   Hier& H = *S.H;
   const Level& L0 = H.lv[0];
-  const Level& L1 = H.lv[1];
   Streams& T = S.st;
   const long long pl = S.plane;
   const int K = chunk_count(S);
-  long long items = 0;
-  int pwlo = 0, pwhi = 0;
   for (int k = 0; k < K; ++k) {
     const int b = k & 1;
     const int p_lo = k * S.C, p_hi = std::min(p_lo + S.C, S.nz);
@@ -170,16 +166,8 @@ static int stream_pass(Stream1& S, int kind, bool prolong, int tail, long long* 
     // ---- inputs of the window: retained planes (device), new planes (host), I0 (host)
     SK(cudaStreamWaitEvent(T.ci, T.evK[b], 0));  // chunk k-2's kernels are done with buffer set b
     if (kind != SP_INIT) {
-      int from = wlo;
-      if (k > 0 && kind == SP_SWEEP && pwhi > wlo) {  // planes [wlo, pwhi) still sit in the previous window
-        SK(cudaMemcpyAsync(S.xin[b].f(), S.xin[b ^ 1].f() + (wlo - pwlo) * pl, sizeof(float) * pl * (pwhi - wlo),
-                           cudaMemcpyDeviceToDevice, T.ci));
-        from = pwhi;
-      }
-      const bool exact = kind == SP_SUMS || kind == SP_WIDEN;  // no halo planes
-      if (exact) from = p_lo;
-      const int to = exact ? p_hi : whi;
-      const long long base = from - (exact ? p_lo : wlo);
+      const int from = p_lo, to = p_hi;  // SP_SUMS / SP_WIDEN: the chunk's own planes
+      const long long base = 0;
       if (to > from && in16) {
         SK(cudaMemcpyAsync(S.xin16[b].p, S.h16 + from * pl, sizeof(__half) * pl * (to - from),
                            cudaMemcpyHostToDevice, T.ci));
@@ -209,13 +197,6 @@ static int stream_pass(Stream1& S, int kind, bool prolong, int tail, long long* 
       const int per = init_blocks_per_plane(L0.nx, L0.ny);
       launch_init(Lk, R, S.tI, S.xout[b].f(), S.bw[b].f() + (p_lo - wlo) * pl,
                   static_cast<double2*>(S.part.p) + (long long)p_lo * per, T.s);
-    } else if (kind == SP_SWEEP) {
-      LevelK Lw = L0.K;
-      Lw.nzl = whi - wlo;
-      launch_rhs(Lw, RhsK{nullptr, iwin, nullptr, 0.f, 0}, S.tI, S.bw[b].f(), T.s);  // a2 on the window
-      items += fused_sweep3d(L0, L1, S.xin[b].f() - wlo * pl, S.xout[b].f() - p_lo * pl, S.bw[b].f() - wlo * pl,
-                             false, prolong, tail, tail == 2 ? static_cast<double2*>(S.part.p) + items : nullptr,
-                             T.s, p_lo, p_hi);
     } else if (kind == SP_WIDEN) {
       SK(cudaMemcpyAsync(S.xout[b].f(), S.xin[b].f(), sizeof(float) * pl * (p_hi - p_lo), cudaMemcpyDeviceToDevice,
                          T.s));
@@ -242,8 +223,117 @@ static int stream_pass(Stream1& S, int kind, bool prolong, int tail, long long* 
       }
       SK(cudaEventRecord(T.evO[b], T.co));
     }
-    pwlo = wlo;
-    pwhi = whi;
+  }
+  SR(T.sync());
+  return GDP_OK;
+}
+
+// ---------------------------------------------------------------------------------
+// NEXT-2 streaming fusion ("temporal blocking is used to
+// perform multiple Gauss-Seidel relaxations in a single streaming pass").  One pass streams the
+// host iterate through the device once and applies m sweeps to it: stage j (0-based) of chunk k
+// updates planes [p_lo - 3j, p_hi - 3j) (the last chunk: up to nz), i.e. it lags stage j-1 by
+// the 3 planes a z-march sweep reads beyond its range, so every stage sweeps every plane exactly
+// once and the per-voxel arithmetic is the in-core kernels' (bit-identical iterates).  Stage j
+// reads its input window [lo_j - 3, hi_j + 3) from a device buffer holding stage j-1's output
+// (planes of earlier chunks retained, this chunk's written by stage j-1 directly); the last
+// stage's planes go back to the host.  A V-cycle's up pass and the next cycle's down pass become
+// one pass (prolongation, nu_post sweeps with the norms, nu_pre sweeps with the restriction).
+// ---------------------------------------------------------------------------------
+struct Stage { bool prolong; int tail; };
+constexpr int LAG = 3;
+
+static void stage_range(const Stream1& S, int k, int j, int& lo, int& hi) {
+  const int K = chunk_count(S);
+  const int p_lo = k * S.C, p_hi = std::min(p_lo + S.C, S.nz);
+  lo = std::max(0, p_lo - LAG * j);
+  hi = k == K - 1 ? S.nz : std::max(0, p_hi - LAG * j);
+  if (k == 0) lo = 0;
+}
+
+static int stream_sweeps(Stream1& S, const std::vector<Stage>& st, long long* items_out, bool in16, bool out16) {
+  Hier& H = *S.H;
+  const Level& L0 = H.lv[0];
+  const Level& L1 = H.lv[1];
+  Streams& T = S.st;
+  const long long pl = S.plane;
+  const int K = chunk_count(S), m = (int)st.size(), nz = S.nz;
+  if (m < 1 || m > Stream1::MAXS) return set_err(GDP_EINVAL, "stream_sweeps: %d stages", m);
+  long long items = 0;
+  int plo[Stream1::MAXS], phi[Stream1::MAXS];  // previous chunk's input window of each stage
+  for (int j = 0; j < m; ++j) plo[j] = phi[j] = 0;
+  for (int k = 0; k < K; ++k) {
+    const int b = k & 1;
+    int lo[Stream1::MAXS], hi[Stream1::MAXS], wlo[Stream1::MAXS], whi[Stream1::MAXS];
+    for (int j = 0; j < m; ++j) {
+      stage_range(S, k, j, lo[j], hi[j]);
+      wlo[j] = std::max(lo[j] - LAG, 0);
+      whi[j] = std::min(hi[j] + LAG, nz);
+    }
+    const int blo = wlo[m - 1], bhi = whi[0];  // rhs window: every stage's input range
+    // ---- stage 0's input: retained planes of the previous window, new planes from the host
+    SK(cudaStreamWaitEvent(T.ci, T.evK[b], 0));  // chunk k-2's kernels are done with buffer set b
+    int from = wlo[0];
+    if (k > 0 && phi[0] > wlo[0]) {
+      SK(cudaMemcpyAsync(S.xin[b].f(), S.xin[b ^ 1].f() + (wlo[0] - plo[0]) * pl, sizeof(float) * pl * (phi[0] - wlo[0]),
+                         cudaMemcpyDeviceToDevice, T.ci));
+      from = phi[0];
+    }
+    if (whi[0] > from) {
+      const long long n = pl * (whi[0] - from);
+      if (in16) {
+        SK(cudaMemcpyAsync(S.xin16[b].p, S.h16 + from * pl, sizeof(__half) * n, cudaMemcpyHostToDevice, T.ci));
+        convert(S.xin16[b].p, S.xin[b].f() + (from - wlo[0]) * pl, n, false, T.ci);
+        S.h2d += (long long)sizeof(__half) * n;
+      } else {
+        SK(cudaMemcpyAsync(S.xin[b].f() + (from - wlo[0]) * pl, S.xh + from * pl, sizeof(float) * n,
+                           cudaMemcpyHostToDevice, T.ci));
+        S.h2d += (long long)sizeof(float) * n;
+      }
+    }
+    SK(cudaMemcpyAsync(S.iw[b].u(), static_cast<const unsigned char*>(S.I0h) + S.sI * blo * pl,
+                       S.sI * pl * (bhi - blo), cudaMemcpyHostToDevice, T.ci));
+    S.h2d += (long long)S.sI * pl * (bhi - blo);
+    SK(cudaEventRecord(T.evI[b], T.ci));
+    // ---- kernels: the rhs of the window, then the stages in order
+    SK(cudaStreamWaitEvent(T.s, T.evI[b], 0));
+    SK(cudaStreamWaitEvent(T.s, T.evO[b], 0));  // chunk k-2's output left the device
+    LevelK Lw = L0.K;
+    Lw.nzl = bhi - blo;
+    launch_rhs(Lw, RhsK{nullptr, S.iw[b].u(), nullptr, 0.f, 0}, S.tI, S.bw[b].f(), T.s);  // a2 on the window
+    const float* bglob = S.bw[b].f() - (long long)blo * pl;
+    for (int j = 1; j < m; ++j) {  // retained input planes of stages 1.. (produced by earlier chunks)
+      const int rto = std::min(phi[j], lo[j - 1]);
+      if (k > 0 && rto > wlo[j])
+        SK(cudaMemcpyAsync(S.sw[j][b].f(), S.sw[j][b ^ 1].f() + (wlo[j] - plo[j]) * pl,
+                           sizeof(float) * pl * (rto - wlo[j]), cudaMemcpyDeviceToDevice, T.s));
+    }
+    for (int j = 0; j < m; ++j) {
+      if (hi[j] <= lo[j]) continue;
+      const float* in = (j == 0 ? S.xin[b].f() : S.sw[j][b].f()) - (long long)wlo[j] * pl;
+      float* out = j == m - 1 ? S.xout[b].f() - (long long)lo[j] * pl : S.sw[j + 1][b].f() - (long long)wlo[j + 1] * pl;
+      const int tail = st[j].tail;
+      const int n = fused_sweep3d(L0, L1, in, out, bglob, false, st[j].prolong, tail,
+                                  tail == 2 ? static_cast<double2*>(S.part.p) + items : nullptr, T.s, lo[j], hi[j]);
+      if (tail == 2) items += n;  // the norms stage's partials, in plane order over the chunks
+    }
+    const int olo = lo[m - 1], ohi = hi[m - 1];
+    if (ohi > olo && out16) convert(S.xout[b].f(), S.xout16[b].p, pl * (ohi - olo), true, T.s);
+    SK(cudaGetLastError());
+    SK(cudaEventRecord(T.evK[b], T.s));
+    // ---- the last stage's planes back to the host iterate (no later window reads them)
+    if (ohi > olo) {
+      SK(cudaStreamWaitEvent(T.co, T.evK[b], 0));
+      if (out16) {
+        SK(cudaMemcpyAsync(S.h16 + olo * pl, S.xout16[b].p, sizeof(__half) * pl * (ohi - olo), cudaMemcpyDeviceToHost, T.co));
+        S.d2h += (long long)sizeof(__half) * pl * (ohi - olo);
+      } else {
+        SK(cudaMemcpyAsync(S.xh + olo * pl, S.xout[b].f(), sizeof(float) * pl * (ohi - olo), cudaMemcpyDeviceToHost, T.co));
+        S.d2h += (long long)sizeof(float) * pl * (ohi - olo);
+      }
+    }
+    SK(cudaEventRecord(T.evO[b], T.co));
+    for (int j = 0; j < m; ++j) { plo[j] = wlo[j]; phi[j] = whi[j]; }
   }
   SR(T.sync());
   if (items_out) *items_out = items;
@@ -283,8 +373,11 @@ int stream_diffuse_z(Ctx& C, const void* I0h, int tI, float* xh, long long nx, l
   for (size_t l = 1; l < chain.size(); ++l) coarse += 12.0 * chain[l].nx * chain[l].ny * chain[l].nzl;
   const long long pl = nx * ny;
   const size_t sI = tI == 0 ? 1 : 4;
-  // two window sets: xin, I0, b over C+6 planes, xout over C planes
-  const double per_plane = 2.0 * (double)pl * ((4.0 + sI + 4.0) + 4.0);
+  // NEXT-2: the up pass of a cycle and the down pass of the next stream as one pass (gdp_opts.stream_fuse)
+  const bool fuse = o.stream_fuse != 0;
+  const int MS0 = fuse ? o.nu_pre + o.nu_post : std::max(o.nu_pre, o.nu_post);
+  // two window sets: x, I0, b and one input window per further stage (chunk + lagged halo planes)
+  const double per_plane = 2.0 * (double)pl * ((4.0 + sI + 4.0) + 4.0 + 4.0 * (MS0 - 1));
   // the budget is a target: below two-plane windows the streamer still runs (C = 2) and only
   // a failing allocation is an error
   const double left = (double)budget - coarse - 4.0 * 1024 * 1024;
@@ -299,16 +392,27 @@ int stream_diffuse_z(Ctx& C, const void* I0h, int tI, float* xh, long long nx, l
   S.H = Hp.get();
   if (!fusable3d(S.H->lv[0], S.H->lv[1], o))
     return set_err(GDP_EINVAL, "out-of-core phase 1 needs an x/y-coarsened second level (stack too small?)");
+  const int MS = fuse ? o.nu_pre + o.nu_post : std::max(o.nu_pre, o.nu_post);  // sweeps per pass
+  if (MS > Stream1::MAXS) return set_err(GDP_EINVAL, "out-of-core phase 1: at most %d sweeps per pass", Stream1::MAXS);
+  const int ext = LAG * MS + 6;  // planes a lagged stage window reaches beyond the chunk
   for (int b = 0; b < 2; ++b) {
     SR(S.xin[b].alloc(sizeof(float) * pl * (Cp + 6)));
-    SR(S.xout[b].alloc(sizeof(float) * pl * Cp));
-    SR(S.iw[b].alloc(sI * pl * (Cp + 6)));
-    SR(S.bw[b].alloc(sizeof(float) * pl * (Cp + 6)));
+    SR(S.xout[b].alloc(sizeof(float) * pl * (Cp + ext)));
+    SR(S.iw[b].alloc(sI * pl * (Cp + ext)));
+    SR(S.bw[b].alloc(sizeof(float) * pl * (Cp + ext)));
+    for (int j = 1; j < MS; ++j) SR(S.sw[j][b].alloc(sizeof(float) * pl * (Cp + ext)));
   }
   const int per_init = init_blocks_per_plane((int)nx, (int)ny);
   long long items_all = 0;
-  for (int k = 0; k < chunk_count(S); ++k)
-    items_all += fused3d_items(S.H->lv[0], S.H->lv[1], k * Cp, std::min<int>(k * Cp + Cp, (int)nz));
+  for (int j = 0; j < MS; ++j) {  // the norms stage can sit at any lag
+    long long it = 0;
+    for (int k = 0; k < chunk_count(S); ++k) {
+      int lo, hi;
+      stage_range(S, k, j, lo, hi);
+      if (hi > lo) it += fused3d_items(S.H->lv[0], S.H->lv[1], lo, hi);
+    }
+    items_all = std::max(items_all, it);
+  }
   S.part_cap = std::max<size_t>({(size_t)per_init * nz, (size_t)items_all,
                                  (size_t)norms_blocks_per_plane((int)nx, (int)ny) * Cp});
   SR(S.part.alloc(sizeof(double2) * S.part_cap));
@@ -323,7 +427,7 @@ int stream_diffuse_z(Ctx& C, const void* I0h, int tI, float* xh, long long nx, l
   r.dx_inf = -1.0;  // the a9 correction norm is measured by the single-rank in-core solve only
   r.levels = (int)S.H->lv.size();
   // initial guess x0 = I0, b, initial residual
-  SR(stream_pass(S, SP_INIT, false, 0, nullptr));
+  SR(stream_pass(S, SP_INIT));
   double rr, bb;
   SR(read_norms(S, static_cast<double2*>(S.part.p), per_init, (int)nz, rr, bb));
   double rel = bb > 0 ? std::sqrt(rr / bb) : std::sqrt(rr);
@@ -336,30 +440,51 @@ int stream_diffuse_z(Ctx& C, const void* I0h, int tI, float* xh, long long nx, l
   const int cap = std::min(o.max_vcycles, GDP_MAX_CYCLES);
   bool stored16 = false;  // the host iterate currently lives in the fp16 scratch (NEXT-4)
   double q = 0.1;         // contraction per cycle, observed (first cycle: assumed)
-  while (rel > o.rel_tol || stored16) {
+  bool down_done = false; // the last pass already ran the next cycle's down sweeps (NEXT-2)
+  std::vector<Stage> down, up;
+  for (int i = 0; i < o.nu_pre; ++i) down.push_back(Stage{false, i == o.nu_pre - 1 ? 1 : 0});
+  for (int i = 0; i < o.nu_post; ++i) up.push_back(Stage{i == 0, i == o.nu_post - 1 ? 2 : 0});
+  while (rel > o.rel_tol || stored16 || down_done) {
     if (k >= cap) { status = GDP_ENOCONV; break; }
     // NEXT-4: this cycle stores fp16 if its residual is predicted to stay above HALF_REL
     const bool h = o.half_staging && rel * q > HALF_REL;
     if (h && !S.h16) {
-      SK(cudaMallocHost(&S.h16, sizeof(__half) * (size_t)pl * nz));
+      const size_t need = sizeof(__half) * (size_t)pl * nz;
+      if (C.h16_bytes < need) {
+        if (C.h16) cudaFreeHost(C.h16);
+        C.h16 = nullptr;
+        C.h16_bytes = 0;
+        SK(cudaMallocHost(&C.h16, need));
+        C.h16_bytes = need;
+      }
+      S.h16 = static_cast<__half*>(C.h16);
       for (int b = 0; b < 2; ++b) {
         SR(S.xin16[b].alloc(sizeof(__half) * pl * (Cp + 6)));
-        SR(S.xout16[b].alloc(sizeof(__half) * pl * Cp));
+        SR(S.xout16[b].alloc(sizeof(__half) * pl * (Cp + ext)));
       }
     }
-    bool in16 = stored16;
-    for (int i = 0; i < o.nu_pre; ++i) {
-      SR(stream_pass(S, SP_SWEEP, false, i == o.nu_pre - 1 ? 1 : 0, nullptr, in16, h));
-      in16 = h;
-    }
+    // a list of sweeps: one streaming pass (stream_fuse) or one pass per sweep
+    auto run = [&](const std::vector<Stage>& list, long long* items) -> int {
+      if (fuse) { SR(stream_sweeps(S, list, items, stored16, h)); stored16 = h; return GDP_OK; }
+      for (const Stage& g : list) {
+        long long it = 0;
+        SR(stream_sweeps(S, std::vector<Stage>{g}, &it, stored16, h));
+        stored16 = h;
+        if (g.tail == 2 && items) *items = it;
+      }
+      return GDP_OK;
+    };
+    if (!down_done) SR(run(down, nullptr));
     SR(run_vcycle(C, *S.H, f, o, S.st.s, 1));
     SK(cudaStreamSynchronize(S.st.s));
+    // NEXT-2: unless this cycle is predicted to be the last, its up pass also runs the next
+    // cycle's down sweeps (one host-link round trip per V-cycle instead of two)
+    const bool fz = fuse && k + 1 < cap && rel > o.rel_tol && rel * q > 4.0 * o.rel_tol;
+    std::vector<Stage> pass = up;
+    if (fz) pass.insert(pass.end(), down.begin(), down.end());
     long long items = 0;
-    for (int i = 0; i < o.nu_post; ++i) {
-      SR(stream_pass(S, SP_SWEEP, i == 0, i == o.nu_post - 1 ? 2 : 0, &items, in16, h));
-      in16 = h;
-    }
-    stored16 = h;
+    SR(run(pass, &items));
+    down_done = fz;
     SR(read_norms(S, static_cast<double2*>(S.part.p), (int)items, 1, rr, bb));
     const double nrel = bb > 0 ? std::sqrt(rr / bb) : std::sqrt(rr);
     ++k;
@@ -367,19 +492,18 @@ int stream_diffuse_z(Ctx& C, const void* I0h, int tI, float* xh, long long nx, l
     if (!std::isfinite(nrel)) return set_err(GDP_EINVAL, "non-finite residual after V-cycle %d", k);
     q = std::min(1.0, std::max(1e-3, nrel / std::max(rel, 1e-300)));
     if (o.stagnation > 0 && nrel > 0.9 * rel) {
-      if (++stall >= o.stagnation) { rel = nrel; status = nrel <= o.rel_tol ? GDP_OK : GDP_ENOCONV; break; }
+      // (not after a fused pass: the stored iterate is then one the norms did not measure)
+      if (++stall >= o.stagnation && !down_done) { rel = nrel; status = nrel <= o.rel_tol ? GDP_OK : GDP_ENOCONV; break; }
     } else {
       stall = 0;
     }
     rel = nrel;
   }
-  if (stored16) SR(stream_pass(S, SP_WIDEN, false, 0, nullptr, true, false));  // ended on an fp16 cycle (cap)
-  if (S.h16) cudaFreeHost(S.h16);
-  S.h16 = nullptr;
+  if (stored16) SR(stream_pass(S, SP_WIDEN, true, false));  // ended on an fp16 cycle (cap)
   r.vcycles = k;
   r.status = status;
   // a10: mean pin, per-plane fp64 sums in plane order (the in-core reduction)
-  SR(stream_pass(S, SP_SUMS, false, 0, nullptr));
+  SR(stream_pass(S, SP_SUMS));
   double2* hp = nullptr;
   SK(cudaMallocHost(&hp, sizeof(double2) * nz));
   cudaMemcpy(hp, S.psum.p, sizeof(double2) * nz, cudaMemcpyDeviceToHost);

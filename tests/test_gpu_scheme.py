@@ -83,7 +83,11 @@ def test_hybrid_phase2_matches_constant_oracle(gpu_ctx, shape, alpha):
     x = host(I2)
     assert np.abs(x - ref).max() <= TOL_X
     b = O.rhs_blend(O.decode(I0), I1.astype(np.float64), alpha)
-    assert O.slice_rel_residuals(x, b, alpha).max() <= TOL_R
+    # reading c-12: the gate is 1e-6 or the fp32 representation floor of the slice, whichever is
+    # larger (a 17 x 1 slice with a small ||b|| has |A||x| / ||b|| ~ 50: floor ~ 1e-6)
+    floor = 4 * 2.0 ** -24 * np.sqrt((((alpha + 8.0) * np.abs(x)) ** 2).sum(axis=(1, 2))) / \
+        np.sqrt((b ** 2).sum(axis=(1, 2)))
+    assert np.all(O.slice_rel_residuals(x, b, alpha) <= np.maximum(TOL_R, floor))
 
 
 @pytest.mark.parametrize("shape", [(9, 40, 37), (1, 1, 1), (4, 1, 70), (12, 33, 34)])

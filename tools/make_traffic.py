@@ -20,6 +20,13 @@ for name, v in best.items():
             continue
         classes["up3d@L0" if prolong else "down3d@L0"].append(v)
         continue
+    m = re.search(r"k_m3v<(\d+), (\d+), (\d+)>", name)
+    if m:  # vertical-pack z-march: TAIL 1 restricts (down), PROLONG or TAIL 2 (norms) is the up pass
+        tail, prolong, zc = int(m.group(1)), int(m.group(2)), int(m.group(3))
+        if zc:
+            continue
+        classes["up3d@L0" if (prolong or tail == 2) else "down3d@L0"].append(v)
+        continue
     m = re.search(r"k_pass2d<(\d+), (\d+)>", name)
     if m:
         classes["down2d@L0" if int(m.group(2)) else "up2d@L0"].append(v)

@@ -1,0 +1,55 @@
+"""Out-of-core streamer timing (a13 + NEXT-2 streaming fusion + NEXT-4 fp16 staging): both phases
+through gdp_destripe_host with the finest level host-resident, for stream_fuse x half_staging.
+
+    python tools/ooc_bench.py NX NY NZ BUDGET_GB [p6]
+p6: the closed-form offset-striped stack (fast to generate, exact answer T + mean(c)); otherwise
+the config generator (slow to generate on the host beyond ~2048^2 x 128).  One JSON line per run."""
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+
+import gdp_synth as synth
+import paper_1310_0041_b200 as gdp
+
+nx, ny, nz = int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3])
+budget = int(float(sys.argv[4]) * 2**30)
+p6 = len(sys.argv) > 5 and sys.argv[5] == "p6"
+t0 = time.perf_counter()
+if p6:
+    I0, T, c = synth.offset_striped_u8(nx, ny, nz, 13)
+    exp = (T.astype(np.float64) + c.mean()) / 255.0
+else:
+    I0 = synth.make_stack(nx, ny, nz, 3, "u8")
+gen_s = time.perf_counter() - t0
+I0t = torch.from_numpy(I0).pin_memory()
+del I0
+I1 = torch.empty((nz, ny, nx), dtype=torch.float32).pin_memory()
+I2 = torch.empty((nz, ny, nx), dtype=torch.float32).pin_memory()
+ctx = gdp.Ctx(0)
+ref = None
+for fuse, half in ((0, 0), (1, 0), (1, 1)):
+    o = gdp.default_opts(stream_fuse=fuse, half_staging=half, fmg=0, fmg_slices=0)
+    t = time.perf_counter()
+    r1, r2 = gdp.gdp_destripe_host(ctx, I0t, I2, I1=I1, alpha=0.01, hbm_budget_bytes=budget, opts=o)
+    el = time.perf_counter() - t
+    line = {"dims": [nz, ny, nx], "stream_fuse": fuse, "half_staging": half, "seconds": el,
+            "voxels_per_s": nx * ny * nz / el, "phase1_s": r1["seconds"], "phase2_s": r2["seconds"],
+            "cycles": [r1["vcycles"], r2["vcycles"]], "rel_res_phase1": r1["rel_res"],
+            "link_bytes_phase1": r1["hbm_bytes_est"], "status": [r1["status"], r2["status"]], "gen_s": gen_s}
+    if p6:
+        d = 0.0
+        for z0 in range(0, nz, 64):
+            d = max(d, (I1[z0:z0 + 64].double() - torch.from_numpy(exp)[None]).abs().max().item())
+        line["max_err_I1_vs_closed_form"] = d
+    if ref is None:
+        ref = I1.clone()
+    else:
+        line["I1_bit_identical_to_unfused"] = bool(torch.equal(ref, I1)) if not half else None
+        line["max_diff_I1_vs_unfused"] = float((ref - I1).abs().max())
+    print(json.dumps(line), flush=True)
+ctx.close()

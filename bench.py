@@ -99,6 +99,8 @@ def run_cpu_baseline(cfg, alpha):
 
     import gdp_synth as synth
     import oracle as O
+    if synth.CONFIGS[cfg]["nz"] == 1:
+        return run_cpu_baseline_slice(cfg, alpha)
     I0 = cpu_sample(cfg, CPU_SAMPLE)
     t = time.perf_counter()
     it1, it2 = cpu_oracle_step(I0, alpha)
@@ -119,6 +121,46 @@ def run_cpu_baseline(cfg, alpha):
     except Exception as e:  # noqa: BLE001 (report, do not fail the bench)
         out["dct_closed_form"] = {"error": str(e)[:200]}
     _ = np
+    return out
+
+
+def slice_pair(cfg, nx=None, ny=None):
+    """Config 2 (phase 2 only, one slice): I0 = generator slice 0, I1 = generator slice 1 of the same
+    seed — an independent slice standing in for the diffused one (the SP solve's cost does not depend
+    on where I1 came from)."""
+    import numpy as np
+
+    import gdp_synth as synth
+    c = synth.CONFIGS[cfg]
+    nx, ny = nx or c["nx"], ny or c["ny"]
+    I0 = synth.make_slice(nx, ny, c["seed"], 0).astype(np.float32)[None]
+    I1 = synth.make_slice(nx, ny, c["seed"], 1).astype(np.float32)[None]
+    return I0, I1
+
+
+def run_cpu_baseline_slice(cfg, alpha):
+    """Config 2: the C/OpenMP CG oracle of phase 2 on a 2048 x 2048 crop, and the DCT closed form of
+    phase 2 on the full slice."""
+    from oracle import cg_omp
+    import oracle as O
+    I0, I1 = slice_pair(cfg, 2048, 2048)
+    t = time.perf_counter()
+    _, it2 = cg_omp.screened_poisson_slices(I0, I1.astype("float64"), alpha, return_iters=True)
+    el = time.perf_counter() - t
+    info = cpu_info()
+    out = {"value": I0.size / el, "unit": UNIT, "cores": info["cores"], "kind": "oracle",
+           "sample": "oracle (C/OpenMP fp64 CG to 1e-10, phase 2) on a 2048x2048 crop of the config-2 slice pair",
+           "cpu_model": info["cpu_model"], "nproc": info["nproc"], "seconds": el,
+           "cg_iterations": {"phase2_sum_over_slices": it2}}
+    try:
+        J0, J1 = slice_pair(cfg)
+        t = time.perf_counter()
+        O.screened_poisson_slices_dct(J0, J1.astype("float64"), alpha)
+        el = time.perf_counter() - t
+        out["dct_closed_form"] = {"value": J0.size / el, "unit": UNIT, "seconds": el,
+                                  "sample": f"full {workload_name(cfg)} (scipy dctn fp64, workers=-1)"}
+    except Exception as e:  # noqa: BLE001
+        out["dct_closed_form"] = {"error": str(e)[:200]}
     return out
 
 
@@ -246,12 +288,16 @@ def main():
 
     c = synth.CONFIGS[args.config]
     nx, ny, nz = c["nx"], c["ny"], c["nz"]
+    slice_only = nz == 1  # config 2: the 2D screened-Poisson solve of one full-resolution slice
     # rank r owns slices [nz r, nz (r + 1)) of a stack of nz * world slices (weak scaling)
     z0g, nzg = nz * rank, nz * world
-    I0_host = np.empty((nz, ny, nx), dtype=np.uint8 if c["dtype"] == "u8" else np.float32)
-    for k in range(nz):
-        s_ = synth.make_slice(nx, ny, c["seed"], z0g + k)
-        I0_host[k] = np.rint(255.0 * s_).astype(np.uint8) if c["dtype"] == "u8" else s_.astype(np.float32)
+    if slice_only:
+        I0_host, I1_host = slice_pair(args.config)
+    else:
+        I0_host = np.empty((nz, ny, nx), dtype=np.uint8 if c["dtype"] == "u8" else np.float32)
+        for k in range(nz):
+            s_ = synth.make_slice(nx, ny, c["seed"], z0g + k)
+            I0_host[k] = np.rint(255.0 * s_).astype(np.uint8) if c["dtype"] == "u8" else s_.astype(np.float32)
     I0 = torch.from_numpy(I0_host).cuda()
     I1 = torch.empty(I0.shape, dtype=torch.float32, device="cuda")
     I2 = torch.empty(I0.shape, dtype=torch.float32, device="cuda")
@@ -271,7 +317,14 @@ def main():
     stream = torch.cuda.Stream()
     nvox = nx * ny * nz
 
+    if slice_only:
+        I1.copy_(torch.from_numpy(I1_host))
+        rep_void = {"vcycles": 0, "rel_res": [0.0], "status": "GDP_OK"}
+
     def step():
+        if slice_only:  # phase 2 only (Eq. 2 on one slice): report slot 2 is empty
+            I2_, r2 = gdp.gdp_screened_poisson_slices(ctx, I0, I1, I2, alpha=args.alpha, opts=opts, stream=stream)
+            return I1, I2_, rep_void, r2
         return gdp.gdp_destripe(ctx, I0, alpha=args.alpha, W=W, I1=I1, I2=I2, opts=opts, stream=stream,
                                 z0_global=z0g, nz_global=nzg)
 
@@ -350,7 +403,28 @@ def main():
 
     # --- end to end through the host-buffer C entry (pinned host I0 -> host I2) -------------
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and slice_only:  # H2D of I0, I1 and D2H of I2 around the device call, pinned
+        I0_pin = torch.from_numpy(I0_host).pin_memory()
+        I1_pin = torch.from_numpy(I1_host).pin_memory()
+        I2_pin = torch.empty(I0.shape, dtype=torch.float32).pin_memory()
+
+        def e2e_step():
+            with torch.cuda.stream(stream):
+                I0.copy_(I0_pin, non_blocking=True)
+                I1.copy_(I1_pin, non_blocking=True)
+                gdp.gdp_screened_poisson_slices(ctx, I0, I1, I2, alpha=args.alpha, opts=opts, stream=stream)
+                I2_pin.copy_(I2, non_blocking=True)
+            stream.synchronize()
+        e2e_step()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            e2e_step()
+        el = time.perf_counter() - t0
+        e2e = {"value": nvox * args.steps / el, "unit": UNIT,
+               "h2d_bytes_per_step": int(I0_pin.numel() * 4 + I1_pin.numel() * 4),
+               "d2h_bytes_per_step": int(I2_pin.numel() * 4),
+               "timing": "host wall clock around H2D(I0, I1) + gdp_screened_poisson_slices + D2H(I2), pinned"}
+    elif not args.no_e2e:
         I0_pin = torch.from_numpy(I0_host).pin_memory()
         I2_pin = torch.empty(I0.shape, dtype=torch.float32).pin_memory()
         hkw = dict(alpha=args.alpha, W=W, opts=opts, z0_global=z0g, nz_global=nzg)
@@ -383,8 +457,11 @@ def main():
                            "schedule": "fused" if args.fused else "reference",
                            "fmg": [opts.fmg, opts.fmg_slices], "use_graphs": opts.use_graphs,
                            "dx_tol": opts.dx_tol, "scheme": args.scheme,
-                           "l2": "working set > L2 (I0 134 MB + three 537 MB fp32 volumes); no flush",
-                           "parallelism": f"z-slabs x{world} (phase 1 NCCL halo, phase 2 slab-local)",
+                           "l2": (f"working set > L2 (I0 {I0.numel() * I0.element_size() / 1e6:.0f} MB + "
+                                  f"fp32 volumes of {nvox * 4 / 1e6:.0f} MB each); no flush"),
+                           "phases": "2 only (one slice, Eq. 2)" if slice_only else "1 + 2",
+                           "parallelism": ("one slice, one GPU" if slice_only else
+                                           f"z-slabs x{world} (phase 1 NCCL halo, phase 2 slab-local)"),
                            "global_dims": [nx, ny, nzg]},
                 "vcycles": {"phase1": conv[0][0], "phase2": conv[0][1], "rel_res_phase1": conv[0][2],
                             "rel_res_phase2_max_slice": conv[0][3], "all_converged": status_ok},

@@ -60,15 +60,57 @@ struct TsLv {
   const TsRow* ty;
   const TsRow* tz;   // unused (z uncoupled) when per_slice
   float alpha, bx, by, bz;
+  // translation-invariant interior: rows ulo[d]..uhi[d] of every axis table are equal, so the 27
+  // coefficients there are constants (cst[(c+1)*9 + (b+1)*3 + (a+1)], diagonal cst[13], row sum crs)
+  int ulo[3], uhi[3];
+  float cst[27];
+  float crs;
+  int seven;  // every M is the identity: 7-point operator from the K tables
 };
 
 __device__ __forceinline__ float tsel(const float4& v, int a) { return a < 0 ? v.x : (a == 0 ? v.y : v.z); }
 
-// S = sum_{n != v} A_vn (x_n - x_v) and the diagonal A_vv of cell (i, j, k); Z: z coupling.
+// S = sum_{n != v} A_vn (x_n - x_v) and the diagonal A_vv of cell (i, j, k); Z: z coupling;
+// L.seven: every M of the level is the identity (the Hybrid finest level: 7-point, K tables only).
 // Neighbours outside the grid have zero coefficients; their indices are clamped to v (d = 0).
 template <bool Z, typename LD>
-__device__ __forceinline__ void ts_row(const TsLv& L, int i, int j, int k, LD ld, float xv, float& S,
+__device__ __forceinline__ void ts_row(const TsLv& L, int i, int j, int k, size_t v, LD ld, float xv, float& S,
                                        float& diag, float& rs) {
+  const long long sy = L.nx, sz = (long long)L.nx * L.ny;
+  if (L.seven) {  // boundary coefficients are 0 in the K tables; the clamped neighbour is v itself
+    const float4 kx = L.tx[i].k, ky = L.ty[j].k;
+    float s = L.bx * (kx.x * ((i > 0 ? ld.off(v, -1) : xv) - xv) + kx.z * ((i + 1 < L.nx ? ld.off(v, 1) : xv) - xv)) +
+              L.by * (ky.x * ((j > 0 ? ld.off(v, -sy) : xv) - xv) + ky.z * ((j + 1 < L.ny ? ld.off(v, sy) : xv) - xv));
+    float d = L.alpha + L.bx * kx.y + L.by * ky.y;
+    if (Z) {
+      const float4 kz = L.tz[k].k;
+      s += L.bz * (kz.x * ((k > 0 ? ld.off(v, -sz) : xv) - xv) + kz.z * ((k + 1 < L.nz ? ld.off(v, sz) : xv) - xv));
+      d += L.bz * kz.y;
+    }
+    S = s;
+    diag = d;
+    rs = L.alpha;
+    return;
+  }
+  if (i >= L.ulo[0] && i <= L.uhi[0] && j >= L.ulo[1] && j <= L.uhi[1] &&
+      (!Z || (k >= L.ulo[2] && k <= L.uhi[2]))) {  // interior: constant coefficients, no table loads
+    float s = 0.f;
+#pragma unroll
+    for (int c = -1; c <= 1; ++c) {
+      if (!Z && c != 0) continue;
+#pragma unroll
+      for (int b = -1; b <= 1; ++b)
+#pragma unroll
+        for (int a = -1; a <= 1; ++a) {
+          if (a == 0 && b == 0 && c == 0) continue;
+          s += L.cst[(c + 1) * 9 + (b + 1) * 3 + (a + 1)] * (ld.off(v, a + b * sy + c * sz) - xv);
+        }
+    }
+    S = s;
+    diag = L.cst[13];
+    rs = L.crs;
+    return;
+  }
   const TsRow X = L.tx[i], Y = L.ty[j];
   TsRow Zr;
   if (Z) Zr = L.tz[k];
@@ -107,6 +149,7 @@ struct LdF {
   const float* x;
   int nx, ny;
   __device__ float operator()(int i, int j, int k) const { return __ldg(x + ((size_t)k * ny + j) * nx + i); }
+  __device__ float off(size_t v, long long d) const { return __ldg(x + (long long)v + d); }
 };
 struct LdU8 {
   const uint8_t* x;
@@ -114,6 +157,7 @@ struct LdU8 {
   __device__ float operator()(int i, int j, int k) const {
     return decode_u8(__ldg(x + ((size_t)k * ny + j) * nx + i));
   }
+  __device__ float off(size_t v, long long d) const { return decode_u8(__ldg(x + (long long)v + d)); }
 };
 
 // one colour of the multicoloured Gauss-Seidel sweep: ncol 8 (i, j, k parities), 4 (i, j parities,
@@ -136,7 +180,7 @@ __global__ void __launch_bounds__(256) k_ts_gs(TsLv L, float* __restrict__ x, co
   const size_t v = ((size_t)k * L.ny + j) * L.nx + i;
   const float xv = x[v];
   float S, dg, rs;
-  ts_row<Z>(L, i, j, k, LdF{x, L.nx, L.ny}, xv, S, dg, rs);
+  ts_row<Z>(L, i, j, k, v, LdF{x, L.nx, L.ny}, xv, S, dg, rs);
   const float r = b[v] - (rs * xv + S);
   x[v] = xv + omega * r / dg;
 }
@@ -154,7 +198,7 @@ __global__ void __launch_bounds__(256) k_ts_resid(TsLv L, const float* __restric
     const size_t v = ((size_t)k * L.ny + j) * L.nx + i;
     const float xv = __ldg(x + v);
     float S, dg, rs;
-    ts_row<Z>(L, i, j, k, LdF{x, L.nx, L.ny}, xv, S, dg, rs);
+    ts_row<Z>(L, i, j, k, v, LdF{x, L.nx, L.ny}, xv, S, dg, rs);
     const float bv = __ldg(b + v);
     const float rv = bv - (rs * xv + S);
     if (r) r[v] = rv;
@@ -178,7 +222,7 @@ __global__ void __launch_bounds__(256) k_ts_apply(TsLv L, LD ld, float* __restri
   const size_t v = ((size_t)k * L.ny + j) * L.nx + i;
   const float uv = ld(i, j, k);
   float S, dg, rs;
-  ts_row<Z>(L, i, j, k, ld, uv, S, dg, rs);
+  ts_row<Z>(L, i, j, k, v, ld, uv, S, dg, rs);
   const float y = rs * uv + S;
   out[v] = accumulate ? out[v] + y : y;
 }
@@ -279,7 +323,8 @@ __device__ void ts_axis(const float* __restrict__ src, float* __restrict__ dst, 
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(1024) k_ts_coarse(TsCoarse C, const float* __restrict__ b, float* __restrict__ x) {
+// (b and x may alias: every CTA reads its system into shared memory before it writes)
+__global__ void __launch_bounds__(1024) k_ts_coarse(TsCoarse C, const float* b, float* x) {
   extern __shared__ float sm[];
   const int nzs = C.per_slice ? 1 : C.nz;
   const int N = C.nx * C.ny * nzs;
@@ -299,6 +344,11 @@ __global__ void __launch_bounds__(1024) k_ts_coarse(TsCoarse C, const float* __r
   ts_axis(a, c, C.Vy, C.nx, C.ny, nzs, 1, false);
   ts_axis(c, a, C.Vx, C.nx, C.ny, nzs, 0, false);
   for (int t = threadIdx.x; t < N; t += blockDim.x) x[off + t] = a[t];
+}
+
+__global__ void k_ts_add(float* __restrict__ x, const float* __restrict__ e, long long n) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < n) x[i] += e[i];
 }
 
 // fixed-order fp64 sums of per-block partials: out[g] = sum of partials [g*n, (g+1)*n)
@@ -470,6 +520,7 @@ struct TsLevelH {
   float* x = nullptr;  // level >= 1: correction
   float* b = nullptr;  // level >= 1: restricted residual
   bool rb = false;     // red-black suffices (every M diagonal)
+  int ulo[3], uhi[3];  // per axis: rows equal to the middle row (translation-invariant interior)
 };
 
 struct TsKey {
@@ -569,6 +620,20 @@ static int ts_build(const TsKey& key, std::unique_ptr<TsHier>& out) {
   }
   for (auto& L : H->lv) {
     L.rb = is_diag(L.M[0]) && is_diag(L.M[1]) && is_diag(L.M[2]);
+    for (int d = 0; d < 3; ++d) {  // the interior range whose rows equal the middle row
+      const Tri &M = L.M[d], &K = L.K[d];
+      const int n = M.n(), mid = n / 2;
+      auto same = [&](int i) {
+        return i >= 1 && i + 1 < n && M.lo[i] == M.lo[mid] && M.d[i] == M.d[mid] && M.hi[i] == M.hi[mid] &&
+               K.lo[i] == K.lo[mid] && K.d[i] == K.d[mid] && K.hi[i] == K.hi[mid];
+      };
+      if (!same(mid)) { L.ulo[d] = 1; L.uhi[d] = 0; continue; }
+      int lo = mid, hi = mid;
+      while (same(lo - 1)) --lo;
+      while (same(hi + 1)) ++hi;
+      L.ulo[d] = lo;
+      L.uhi[d] = hi;
+    }
     std::vector<TsRow> rows;
     for (int d = 0; d < 3; ++d) {
       auto r = rows_of(L.M[d], L.K[d]);
@@ -629,6 +694,30 @@ static int ts_get(Ctx& C, const TsKey& k, TsHier** out) {
   return GDP_OK;
 }
 
+// the constant coefficients of the interior (from the middle rows, fp64 rounded once)
+static void set_interior(TsLv& v, const TsLevelH& L, bool per_slice) {
+  for (int d = 0; d < 3; ++d) { v.ulo[d] = L.ulo[d]; v.uhi[d] = L.uhi[d]; }
+  const int mx = L.n[0] / 2, my = L.n[1] / 2, mz = L.n[2] / 2;
+  auto e = [](const Tri& t, int i, int a) { return a < 0 ? t.lo[i] : (a == 0 ? t.d[i] : t.hi[i]); };
+  double rs = v.alpha;
+  for (int d = 0; d < (per_slice ? 2 : 3); ++d) {
+    const int m = L.n[d] / 2;
+    rs *= L.M[d].lo[m] + L.M[d].d[m] + L.M[d].hi[m];
+  }
+  v.crs = (float)rs;
+  for (int c = -1; c <= 1; ++c)
+    for (int b = -1; b <= 1; ++b)
+      for (int a = -1; a <= 1; ++a) {
+        double zm = 1.0, zk = 0.0;
+        if (!per_slice) { zm = e(L.M[2], mz, c); zk = e(L.K[2], mz, c); }
+        else if (c != 0) zm = 0.0;
+        const double xm = e(L.M[0], mx, a), xk = e(L.K[0], mx, a), ym = e(L.M[1], my, b), yk = e(L.K[1], my, b);
+        const double C = (double)v.alpha * xm * ym * zm + (double)v.bx * xk * ym * zm + (double)v.by * xm * yk * zm +
+                         (double)v.bz * xm * ym * zk;
+        v.cst[(c + 1) * 9 + (b + 1) * 3 + (a + 1)] = (float)C;
+      }
+}
+
 static TsLv dev_level(const TsHier& H, const TsLevelH& L) {
   TsLv v;
   v.nx = L.n[0]; v.ny = L.n[1]; v.nz = L.n[2];
@@ -638,6 +727,8 @@ static TsLv dev_level(const TsHier& H, const TsLevelH& L) {
   v.alpha = H.key.alpha;
   v.bx = H.key.bx; v.by = H.key.by;
   v.bz = H.key.per_slice ? 0.f : H.key.bz;
+  v.seven = L.rb ? 1 : 0;
+  set_interior(v, L, H.key.per_slice != 0);
   return v;
 }
 
@@ -725,8 +816,18 @@ static int ts_cycle(TsHier& H, float* x0, const float* b0, int nu_pre, int nu_po
     cc.inv = H.cinv;
     const int nsys = H.key.per_slice ? L.n[2] : 1;
     const int N = L.n[0] * L.n[1] * (H.key.per_slice ? 1 : L.n[2]);
-    ProfScope ps(KC_COARSE, 8.0 * (double)cells(L), s);
-    k_ts_coarse<<<nsys, 1024, 2 * N * sizeof(float), s>>>(cc, bs[nl - 1], xs[nl - 1]);
+    if (nl == 1) {  // the finest level is the coarsest: correction form (iterative refinement in fp32)
+      RETS(ts_resid(H, L, xs[0], bs[0], H.r, false, s));
+      {
+        ProfScope ps(KC_COARSE, 8.0 * (double)cells(L), s);
+        k_ts_coarse<<<nsys, 1024, 2 * N * sizeof(float), s>>>(cc, H.r, H.r);
+      }
+      ProfScope ps(KC_UTIL, 12.0 * (double)cells(L), s);
+      k_ts_add<<<(int)((cells(L) + 255) / 256), 256, 0, s>>>(xs[0], H.r, (long long)cells(L));
+    } else {
+      ProfScope ps(KC_COARSE, 8.0 * (double)cells(L), s);
+      k_ts_coarse<<<nsys, 1024, 2 * N * sizeof(float), s>>>(cc, bs[nl - 1], xs[nl - 1]);
+    }
   }
   for (int l = nl - 2; l >= 0; --l) {
     const TsLevelH& L = H.lv[l];
@@ -805,6 +906,7 @@ static void ts_apply_with(const TsHier& H, float alpha, float bx, float by, floa
                           float* out, int acc, cudaStream_t s) {
   TsLv v = dev_level(H, H.lv[0]);
   v.alpha = alpha; v.bx = bx; v.by = by; v.bz = bz;
+  set_interior(v, H.lv[0], H.key.per_slice != 0);
   const bool Z = !H.key.per_slice;
   if (tI == 0) ts_launch_apply(v, Z, LdU8{(const uint8_t*)u, v.nx, v.ny}, out, acc, s);
   else ts_launch_apply(v, Z, LdF{(const float*)u, v.nx, v.ny}, out, acc, s);

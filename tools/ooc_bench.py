@@ -34,9 +34,10 @@ ctx = gdp.Ctx(0)
 ref = None
 for fuse, half in ((0, 0), (1, 0), (1, 1)):
     o = gdp.default_opts(stream_fuse=fuse, half_staging=half, fmg=0, fmg_slices=0)
-    t = time.perf_counter()
-    r1, r2 = gdp.gdp_destripe_host(ctx, I0t, I2, I1=I1, alpha=0.01, hbm_budget_bytes=budget, opts=o)
-    el = time.perf_counter() - t
+    for rep in range(2):  # the second call is timed (the first pins the fp16 scratch)
+        t = time.perf_counter()
+        r1, r2 = gdp.gdp_destripe_host(ctx, I0t, I2, I1=I1, alpha=0.01, hbm_budget_bytes=budget, opts=o)
+        el = time.perf_counter() - t
     line = {"dims": [nz, ny, nx], "stream_fuse": fuse, "half_staging": half, "seconds": el,
             "voxels_per_s": nx * ny * nz / el, "phase1_s": r1["seconds"], "phase2_s": r2["seconds"],
             "cycles": [r1["vcycles"], r2["vcycles"]], "rel_res_phase1": r1["rel_res"],

@@ -162,48 +162,72 @@ struct LdU8 {
 
 // one colour of the multicoloured Gauss-Seidel sweep: ncol 8 (i, j, k parities), 4 (i, j parities,
 // every slice) or 2 (red-black, (i + j + k) parity)
+// Each thread updates NPT cells of the colour in rows NPT apart (a block covers NPT x blockDim.y
+// row slots), computing all of them before storing any: the loads of the NPT cells are in flight
+// together (the launches are latency-bound at one cell per thread; neighbours of a colour are
+// never written by the same launch, so the order of loads and stores does not matter).
+constexpr int NPT = 4;
+
 template <bool Z>
 __global__ void __launch_bounds__(256) k_ts_gs(TsLv L, float* __restrict__ x, const float* __restrict__ b,
                                                int ncol, int colour, float omega) {
   const int ih = blockIdx.x * blockDim.x + threadIdx.x;
-  int j = blockIdx.y * blockDim.y + threadIdx.y;
-  int k = blockIdx.z;
-  int i;
-  if (ncol == 2) {
-    i = 2 * ih + ((j + k + colour) & 1);
-  } else {
-    i = 2 * ih + (colour & 1);
-    j = 2 * j + ((colour >> 1) & 1);
-    if (ncol == 8) k = 2 * k + ((colour >> 2) & 1);
+  const int j0 = blockIdx.y * blockDim.y * NPT + threadIdx.y;
+  const int k0 = blockIdx.z;
+  float nv[NPT];
+  size_t vv[NPT];
+  bool ok[NPT];
+#pragma unroll
+  for (int q = 0; q < NPT; ++q) {
+    int j = j0 + q * blockDim.y, k = k0, i;
+    if (ncol == 2) {
+      i = 2 * ih + ((j + k + colour) & 1);
+    } else {
+      i = 2 * ih + (colour & 1);
+      j = 2 * j + ((colour >> 1) & 1);
+      if (ncol == 8) k = 2 * k + ((colour >> 2) & 1);
+    }
+    ok[q] = i < L.nx && j < L.ny && k < L.nz;
+    vv[q] = ((size_t)k * L.ny + j) * L.nx + i;
+    nv[q] = 0.f;
+    if (ok[q]) {
+      const size_t v = vv[q];
+      const float xv = __ldg(x + v);
+      float S, dg, rs;
+      ts_row<Z>(L, i, j, k, v, LdF{x, L.nx, L.ny}, xv, S, dg, rs);
+      const float r = __ldg(b + v) - (rs * xv + S);
+      nv[q] = xv + omega * r / dg;
+    }
   }
-  if (i >= L.nx || j >= L.ny || k >= L.nz) return;
-  const size_t v = ((size_t)k * L.ny + j) * L.nx + i;
-  const float xv = x[v];
-  float S, dg, rs;
-  ts_row<Z>(L, i, j, k, v, LdF{x, L.nx, L.ny}, xv, S, dg, rs);
-  const float r = b[v] - (rs * xv + S);
-  x[v] = xv + omega * r / dg;
+#pragma unroll
+  for (int q = 0; q < NPT; ++q)
+    if (ok[q]) x[vv[q]] = nv[q];
 }
 
 // r = b - A x (r may be null) with fp64 partials (sum r^2, sum b^2) per block; a block row covers
-// one slice (blockIdx.z = k) so per-slice sums are a fixed-order reduction of its blocks
+// one slice (blockIdx.z = k) so per-slice sums are a fixed-order reduction of its blocks; NPT
+// rows per thread (the block reduction is the costly part at one cell per thread)
 template <bool Z>
 __global__ void __launch_bounds__(256) k_ts_resid(TsLv L, const float* __restrict__ x, const float* __restrict__ b,
                                                   float* __restrict__ r, double2* __restrict__ part) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  const int j = blockIdx.y * blockDim.y + threadIdx.y;
+  const int j0 = blockIdx.y * blockDim.y * NPT + threadIdx.y;
   const int k = blockIdx.z;
   double a2 = 0.0, b2 = 0.0;
-  if (i < L.nx && j < L.ny) {
-    const size_t v = ((size_t)k * L.ny + j) * L.nx + i;
-    const float xv = __ldg(x + v);
-    float S, dg, rs;
-    ts_row<Z>(L, i, j, k, v, LdF{x, L.nx, L.ny}, xv, S, dg, rs);
-    const float bv = __ldg(b + v);
-    const float rv = bv - (rs * xv + S);
-    if (r) r[v] = rv;
-    a2 = (double)rv * rv;
-    b2 = (double)bv * bv;
+#pragma unroll
+  for (int q = 0; q < NPT; ++q) {
+    const int j = j0 + q * blockDim.y;
+    if (i < L.nx && j < L.ny) {
+      const size_t v = ((size_t)k * L.ny + j) * L.nx + i;
+      const float xv = __ldg(x + v);
+      float S, dg, rs;
+      ts_row<Z>(L, i, j, k, v, LdF{x, L.nx, L.ny}, xv, S, dg, rs);
+      const float bv = __ldg(b + v);
+      const float rv = bv - (rs * xv + S);
+      if (r) r[v] = rv;
+      a2 += (double)rv * rv;
+      b2 += (double)bv * bv;
+    }
   }
   if (part) {
     block_sum2(a2, b2);
@@ -747,7 +771,7 @@ static void ts_sweep(const TsHier& H, const TsLevelH& L, float* x, const float* 
     const int hx = (v.nx + 1) / 2;
     const int gy = ncol == 2 ? v.ny : (v.ny + 1) / 2;
     const int gz = ncol == 8 ? (v.nz + 1) / 2 : v.nz;
-    dim3 g((hx + kBlk.x - 1) / kBlk.x, (gy + kBlk.y - 1) / kBlk.y, gz);
+    dim3 g((hx + kBlk.x - 1) / kBlk.x, (gy + kBlk.y * NPT - 1) / (kBlk.y * NPT), gz);
     ProfScope ps(KC_RBGS, per_launch, s, (double)cells(L));
     if (Z) k_ts_gs<true><<<g, kBlk, 0, s>>>(v, x, b, ncol, c, omega);
     else k_ts_gs<false><<<g, kBlk, 0, s>>>(v, x, b, ncol, c, omega);
@@ -767,7 +791,7 @@ static int ts_ensure_part(TsHier& H, size_t n) {
 static int ts_resid(TsHier& H, const TsLevelH& L, const float* x, const float* b, float* r, bool norms,
                     cudaStream_t s) {
   const TsLv v = dev_level(H, L);
-  const dim3 g = grid_xy(v.nx, v.ny, v.nz, kBlk);
+  const dim3 g((v.nx + kBlk.x - 1) / kBlk.x, (v.ny + kBlk.y * NPT - 1) / (kBlk.y * NPT), v.nz);
   const size_t nb = (size_t)g.x * g.y;
   if (norms) RETS(ts_ensure_part(H, nb * v.nz));
   {

@@ -136,6 +136,7 @@ struct Stream1 {
   DevBuf xin[2], xout[2], iw[2], bw[2];
   DevBuf xin16[2], xout16[2];  // fp16 staging of the iterate's window (NEXT-4)
   static constexpr int MAXS = 8;  // sweeps per streaming pass (NEXT-2)
+  int ms = 1;                     // sweeps one pass may hold (window memory)
   DevBuf sw[MAXS][2];             // input windows of stages 1.. of a multi-sweep pass
   __half* h16 = nullptr;       // host fp16 iterate (pinned; Ctx::h16, allocated on first use)
   DevBuf part;                // norm partials (init: per plane rows; sweeps: per item)
@@ -373,34 +374,47 @@ int stream_diffuse_z(Ctx& C, const void* I0h, int tI, float* xh, long long nx, l
   for (size_t l = 1; l < chain.size(); ++l) coarse += 12.0 * chain[l].nx * chain[l].ny * chain[l].nzl;
   const long long pl = nx * ny;
   const size_t sI = tI == 0 ? 1 : 4;
-  // NEXT-2: the up pass of a cycle and the down pass of the next stream as one pass (gdp_opts.stream_fuse)
-  const bool fuse = o.stream_fuse != 0;
-  const int MS0 = fuse ? o.nu_pre + o.nu_post : std::max(o.nu_pre, o.nu_post);
-  // two window sets: x, I0, b and one input window per further stage (chunk + lagged halo planes)
-  const double per_plane = 2.0 * (double)pl * ((4.0 + sI + 4.0) + 4.0 + 4.0 * (MS0 - 1));
+  // NEXT-2: sweeps per streaming pass.  MS = nu_pre + nu_post fuses a cycle's up pass with the next
+  // cycle's down pass, max(nu_pre, nu_post) keeps one pass per half-cycle, 1 is one pass per sweep.
+  // Device windows per pass (two sets): x in C + 6 planes, the last stage's output C + 3 (MS - 1),
+  // I0 and b C + 3 MS + 3, stage j's input C + 3 j + 6 (j >= 1), fp16 staging 2 B per x plane.
+  auto fixed_planes = [&](int ms) {  // bytes per plane x: the C-independent part of the windows
+    double f = 4.0 * 6 + 4.0 * 3 * (ms - 1) + (4.0 + sI) * (3 * ms + 3) + 2.0 * (6 + 3 * (ms - 1));
+    for (int j = 1; j < ms; ++j) f += 4.0 * (3 * j + 6);
+    return 2.0 * f;
+  };
+  auto per_plane_of = [&](int ms) { return 2.0 * (4.0 + 4.0 + sI + 4.0 + 4.0 * (ms - 1) + 4.0); };
+  size_t freeb = 0, totb = 0;
+  SK(cudaMemGetInfo(&freeb, &totb));
+  const double hard = 0.9 * (double)freeb - coarse;  // what the windows may take at most
+  int MS = std::max(o.nu_pre, o.nu_post);
+  if (o.stream_fuse && (double)pl * (fixed_planes(o.nu_pre + o.nu_post) + 2 * per_plane_of(o.nu_pre + o.nu_post)) <= hard)
+    MS = o.nu_pre + o.nu_post;
+  else if (!o.stream_fuse || (double)pl * (fixed_planes(MS) + 2 * per_plane_of(MS)) > hard)
+    MS = 1;  // no room (or no wish) for multi-sweep windows: one pass per sweep
+  if (MS > Stream1::MAXS) return set_err(GDP_EINVAL, "out-of-core phase 1: at most %d sweeps per pass", Stream1::MAXS);
+  const bool fuse = MS == o.nu_pre + o.nu_post && o.stream_fuse;  // cross-cycle fusion in this solve
   // the budget is a target: below two-plane windows the streamer still runs (C = 2) and only
-  // a failing allocation is an error
-  const double left = (double)budget - coarse - 4.0 * 1024 * 1024;
-  // windows beyond a few dozen planes buy nothing (the pipeline keeps two in flight) and would
-  // crowd out the coarse levels' lazily allocated buffers
-  int Cp = (int)std::min<double>(std::min<double>((double)nz, 64.0), std::max(2.0, std::floor(left / per_plane) - 6.0));
+  // a failing allocation is an error; windows beyond a few dozen planes buy nothing (the pipeline
+  // keeps two in flight) and would crowd out the coarse levels' lazily allocated buffers
+  const double left = std::min((double)budget - coarse - 4.0 * 1024 * 1024, hard) - (double)pl * fixed_planes(MS);
+  int Cp = (int)std::min<double>(std::min<double>((double)nz, 64.0), std::max(2.0, std::floor(left / ((double)pl * per_plane_of(MS)))));
   Cp = std::max(2, Cp & ~1);
   Stream1 S;
   S.I0h = I0h; S.xh = xh; S.tI = tI; S.nx = nx; S.ny = ny; S.plane = pl; S.nz = (int)nz; S.C = Cp; S.sI = sI;
+  S.ms = MS;
   std::unique_ptr<Hier> Hp;
   SR(build_hier_levels(key, chain, 0, (int)chain.size(), false, true, Hp));
   S.H = Hp.get();
   if (!fusable3d(S.H->lv[0], S.H->lv[1], o))
     return set_err(GDP_EINVAL, "out-of-core phase 1 needs an x/y-coarsened second level (stack too small?)");
-  const int MS = fuse ? o.nu_pre + o.nu_post : std::max(o.nu_pre, o.nu_post);  // sweeps per pass
-  if (MS > Stream1::MAXS) return set_err(GDP_EINVAL, "out-of-core phase 1: at most %d sweeps per pass", Stream1::MAXS);
-  const int ext = LAG * MS + 6;  // planes a lagged stage window reaches beyond the chunk
+  const int cz = (int)nz + 6;  // no window exceeds the stack plus its halo
   for (int b = 0; b < 2; ++b) {
-    SR(S.xin[b].alloc(sizeof(float) * pl * (Cp + 6)));
-    SR(S.xout[b].alloc(sizeof(float) * pl * (Cp + ext)));
-    SR(S.iw[b].alloc(sI * pl * (Cp + ext)));
-    SR(S.bw[b].alloc(sizeof(float) * pl * (Cp + ext)));
-    for (int j = 1; j < MS; ++j) SR(S.sw[j][b].alloc(sizeof(float) * pl * (Cp + ext)));
+    SR(S.xin[b].alloc(sizeof(float) * pl * std::min(Cp + 6, cz)));
+    SR(S.xout[b].alloc(sizeof(float) * pl * std::min(Cp + 3 * (MS - 1), cz)));
+    SR(S.iw[b].alloc(sI * pl * std::min(Cp + 3 * MS + 3, cz)));
+    SR(S.bw[b].alloc(sizeof(float) * pl * std::min(Cp + 3 * MS + 3, cz)));
+    for (int j = 1; j < MS; ++j) SR(S.sw[j][b].alloc(sizeof(float) * pl * std::min(Cp + 3 * j + 6, cz)));
   }
   const int per_init = init_blocks_per_plane((int)nx, (int)ny);
   long long items_all = 0;
@@ -459,18 +473,20 @@ int stream_diffuse_z(Ctx& C, const void* I0h, int tI, float* xh, long long nx, l
       }
       S.h16 = static_cast<__half*>(C.h16);
       for (int b = 0; b < 2; ++b) {
-        SR(S.xin16[b].alloc(sizeof(__half) * pl * (Cp + 6)));
-        SR(S.xout16[b].alloc(sizeof(__half) * pl * (Cp + ext)));
+        SR(S.xin16[b].alloc(sizeof(__half) * pl * std::min(Cp + 6, cz)));
+        SR(S.xout16[b].alloc(sizeof(__half) * pl * std::min(Cp + 3 * (MS - 1), cz)));
       }
     }
     // a list of sweeps: one streaming pass (stream_fuse) or one pass per sweep
-    auto run = [&](const std::vector<Stage>& list, long long* items) -> int {
-      if (fuse) { SR(stream_sweeps(S, list, items, stored16, h)); stored16 = h; return GDP_OK; }
-      for (const Stage& g : list) {
+    auto run = [&](const std::vector<Stage>& list, long long* items) -> int {  // passes of <= S.ms sweeps
+      for (size_t a = 0; a < list.size(); a += S.ms) {
+        const std::vector<Stage> part(list.begin() + a, list.begin() + std::min(list.size(), a + S.ms));
         long long it = 0;
-        SR(stream_sweeps(S, std::vector<Stage>{g}, &it, stored16, h));
+        SR(stream_sweeps(S, part, &it, stored16, h));
         stored16 = h;
-        if (g.tail == 2 && items) *items = it;
+        bool norms = false;
+        for (const Stage& g : part) norms |= g.tail == 2;
+        if (norms && items) *items = it;
       }
       return GDP_OK;
     };

@@ -146,3 +146,27 @@ def test_config3_out_of_core_offset_striping(gpu_ctx):
         d1 = max(d1, (I1[z0:z0 + 64].double() - exp[None]).abs().max().item())
         d2 = max(d2, (I2[z0:z0 + 64].double() - exp[None]).abs().max().item())
     assert d1 <= TOL_X and d2 <= 1e-4, (d1, d2)
+
+
+def test_config4_downscaled_out_of_core(gpu_ctx):
+    """BASELINE config 4 (16384 x 16384 x 1024 u8, 275 GB) exceeds this box's host memory; its
+    16384^2 planes (1 GiB each in fp32) are exercised on a 16-plane down-scaled stack streamed
+    with a 12 GiB HBM budget (a few planes per window, deep hierarchies), with NEXT-2 multi-sweep
+    passes and NEXT-4 fp16 staging.  P6: the exact answer is T + mean(c)."""
+    nx = ny = 16384
+    nz = 16
+    I0, T, c = synth.offset_striped_u8(nx, ny, nz, 14)
+    I0t = torch.from_numpy(I0).pin_memory()
+    del I0
+    I1 = torch.empty((nz, ny, nx), dtype=torch.float32).pin_memory()
+    I2 = torch.empty((nz, ny, nx), dtype=torch.float32).pin_memory()
+    r1, r2 = gdp.gdp_destripe_host(gpu_ctx, I0t, I2, I1=I1, alpha=0.01, hbm_budget_bytes=12 << 30,
+                                   opts=gdp.default_opts(half_staging=1))
+    assert r1["status"] == "GDP_OK" and r2["status"] == "GDP_OK", (r1, r2)
+    assert r1["hbm_bytes_est"] > 0  # streamed
+    exp = torch.from_numpy((T.astype(np.float64) + c.mean()) / 255.0)
+    d1 = d2 = 0.0
+    for z in range(nz):
+        d1 = max(d1, (I1[z].double() - exp).abs().max().item())
+        d2 = max(d2, (I2[z].double() - exp).abs().max().item())
+    assert d1 <= TOL_X and d2 <= 1e-4, (d1, d2)

@@ -237,7 +237,13 @@ int gdp_destripe(gdp_ctx* ctx, const void* I0, gdp_dtype dtype, float* I1, float
  * HOST arrays of the whole local stack (on a distributed ctx: this rank's slab at
  * z0_global of nz_global; single rank: 0 and local.nz).  The library streams z-slabs host->device on
  * side streams, runs both phases, and streams I2 back.  If the stack does not fit in
- * `hbm_budget_bytes` (0 = 90% of free device memory) it returns GDP_ENOMEM.          */
+ * `hbm_budget_bytes` (0 = 90% of free device memory), a single-rank ctx runs OUT OF CORE: the
+ * finest level of phase 1 stays in the host buffers (I1 is then required scratch as well as
+ * output: NULL is allowed, the library pins a scratch) and is streamed through the device in
+ * z-chunks — several sweeps per host-link round trip (opts->stream_fuse, NEXT-2), optionally fp16
+ * staging of early iterates (opts->half_staging, NEXT-4) — and phase 2 streams slice batches.
+ * Out of core is Constant-scheme and single-rank only: otherwise GDP_ENOMEM.  The report's
+ * hbm_bytes_est is then the host-link bytes of phase 1.                                  */
 int gdp_destripe_host(gdp_ctx* ctx, const void* I0_host, gdp_dtype dtype, float* I1_host,
                       float* I2_host, gdp_dims local, int64_t z0_global, int64_t nz_global,
                       gdp_weights W, float alpha, size_t hbm_budget_bytes, const gdp_opts* opts,

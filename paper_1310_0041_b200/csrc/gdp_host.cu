@@ -73,6 +73,9 @@ extern "C" int gdp_destripe_host(gdp_ctx* ctx, const void* I0_host, gdp_dtype dt
     gdp_opts o;
     gdp_opts_default(&o);
     if (opts) o = *opts;
+    if (o.scheme != GDP_SCHEME_CONSTANT)
+      return set_err(GDP_ENOMEM, "stack needs ~%zu B of HBM, budget %zu B; the Hybrid / Linear schemes run in "
+                     "core only in this build", need, budget);
     HostPin pin0, pin1, pin2;
     int rc = pin0.pin(I0_host, n * sI);
     if (rc == GDP_OK) rc = pin2.pin(I2_host, n * 4);

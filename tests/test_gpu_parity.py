@@ -345,6 +345,28 @@ def test_out_of_core_matches_in_core(gpu_ctx, shape, dtype, pin):
     assert rb["hbm_bytes_est"] > 0  # host-link bytes of the streamed finest level
 
 
+@pytest.mark.parametrize("shape,budget,fuse", [((5, 96, 100), 1, 1), ((7, 64, 80), 1, 0),
+                                               ((64, 512, 512), 300 << 20, 1), ((64, 512, 512), 300 << 20, 0)])
+def test_out_of_core_stream_fusion_bit_identical(gpu_ctx, shape, budget, fuse):
+    """NEXT-2: multi-sweep streaming passes (z-lagged stages, cross-cycle fusion) and one pass per
+    sweep give the in-core phase-1 iterate bit for bit, for stacks shorter than the stage lag and
+    for windows wider than it (a 300 MB budget: 4-plane chunks of 512^2)."""
+    nz, ny, nx = shape
+    I0 = synth.make_stack(nx, ny, nz, 62, "u8")
+    t0 = torch.from_numpy(I0).pin_memory()
+    outs = []
+    for b in (0, budget):
+        I1 = torch.empty(shape, dtype=torch.float32).pin_memory()
+        I2 = torch.empty(shape, dtype=torch.float32).pin_memory()
+        r1, r2 = gdp.gdp_destripe_host(gpu_ctx, t0, I2, I1=I1, alpha=0.01, hbm_budget_bytes=b,
+                                       opts=gdp.default_opts(fmg=0, fmg_slices=0, stream_fuse=fuse))
+        assert r1["status"] == "GDP_OK" and r2["status"] == "GDP_OK", (b, r1, r2)
+        outs.append((I1.numpy().copy(), r1))
+    (a1, ra), (b1, rb) = outs
+    assert rb["hbm_bytes_est"] > 0 and ra["vcycles"] == rb["vcycles"]
+    assert np.array_equal(a1, b1)
+
+
 # ------------------------------------------------------------------ NEXT-1: the §6 NPR filter
 @pytest.mark.parametrize("shape,dtype,params", [((16, 135, 240), "u8", (0.001, 1.25, 5 / 255)),
                                                 ((9, 63, 65), "f32", (0.01, 1.0, 0.05)),

@@ -76,15 +76,14 @@ __device__ __forceinline__ float tsel(const float4& v, int a) { return a < 0 ? v
 template <bool Z, typename LD>
 __device__ __forceinline__ void ts_row(const TsLv& L, int i, int j, int k, size_t v, LD ld, float xv, float& S,
                                        float& diag, float& rs) {
-  const long long sy = L.nx, sz = (long long)L.nx * L.ny;
   if (L.seven) {  // boundary coefficients are 0 in the K tables; the clamped neighbour is v itself
     const float4 kx = L.tx[i].k, ky = L.ty[j].k;
-    float s = L.bx * (kx.x * ((i > 0 ? ld.off(v, -1) : xv) - xv) + kx.z * ((i + 1 < L.nx ? ld.off(v, 1) : xv) - xv)) +
-              L.by * (ky.x * ((j > 0 ? ld.off(v, -sy) : xv) - xv) + ky.z * ((j + 1 < L.ny ? ld.off(v, sy) : xv) - xv));
+    float s = L.bx * (kx.x * ((i > 0 ? ld.off(v, -1, 0, 0) : xv) - xv) + kx.z * ((i + 1 < L.nx ? ld.off(v, 1, 0, 0) : xv) - xv)) +
+              L.by * (ky.x * ((j > 0 ? ld.off(v, 0, -1, 0) : xv) - xv) + ky.z * ((j + 1 < L.ny ? ld.off(v, 0, 1, 0) : xv) - xv));
     float d = L.alpha + L.bx * kx.y + L.by * ky.y;
     if (Z) {
       const float4 kz = L.tz[k].k;
-      s += L.bz * (kz.x * ((k > 0 ? ld.off(v, -sz) : xv) - xv) + kz.z * ((k + 1 < L.nz ? ld.off(v, sz) : xv) - xv));
+      s += L.bz * (kz.x * ((k > 0 ? ld.off(v, 0, 0, -1) : xv) - xv) + kz.z * ((k + 1 < L.nz ? ld.off(v, 0, 0, 1) : xv) - xv));
       d += L.bz * kz.y;
     }
     S = s;
@@ -103,7 +102,7 @@ __device__ __forceinline__ void ts_row(const TsLv& L, int i, int j, int k, size_
 #pragma unroll
         for (int a = -1; a <= 1; ++a) {
           if (a == 0 && b == 0 && c == 0) continue;
-          s += L.cst[(c + 1) * 9 + (b + 1) * 3 + (a + 1)] * (ld.off(v, a + b * sy + c * sz) - xv);
+          s += L.cst[(c + 1) * 9 + (b + 1) * 3 + (a + 1)] * (ld.off(v, a, b, c) - xv);
         }
     }
     S = s;
@@ -149,7 +148,9 @@ struct LdF {
   const float* x;
   int nx, ny;
   __device__ float operator()(int i, int j, int k) const { return __ldg(x + ((size_t)k * ny + j) * nx + i); }
-  __device__ float off(size_t v, long long d) const { return __ldg(x + (long long)v + d); }
+  __device__ float off(size_t v, int a, int b, int c) const {
+    return __ldg(x + (long long)v + a + (long long)b * nx + (long long)c * nx * ny);
+  }
 };
 struct LdU8 {
   const uint8_t* x;
@@ -157,7 +158,19 @@ struct LdU8 {
   __device__ float operator()(int i, int j, int k) const {
     return decode_u8(__ldg(x + ((size_t)k * ny + j) * nx + i));
   }
-  __device__ float off(size_t v, long long d) const { return decode_u8(__ldg(x + (long long)v + d)); }
+  __device__ float off(size_t v, int a, int b, int c) const {
+    return decode_u8(__ldg(x + (long long)v + a + (long long)b * nx + (long long)c * nx * ny));
+  }
+};
+// shared-memory tile of three planes (k - 1, k, k + 1) of the staged region (k_ts_gs_tile): global
+// (i, j, k) -> slot of plane k, row j - j0, column i - i0; `v` is the cell's index within its plane
+// tile.  Cells outside the grid are staged as 0: their coefficients are 0, so they add 0 * (0 - x_v).
+struct LdS {
+  const float *pm, *p0, *pp;  // planes k - 1, k, k + 1 (pm, pp unused without z coupling)
+  int i0, j0, k, sy;
+  __device__ const float* pl(int c) const { return c < 0 ? pm : (c > 0 ? pp : p0); }
+  __device__ float operator()(int i, int j, int kk) const { return pl(kk - k)[(j - j0) * sy + (i - i0)]; }
+  __device__ float off(size_t v, int a, int b, int c) const { return pl(c)[(int)v + a + b * sy]; }
 };
 
 // one colour of the multicoloured Gauss-Seidel sweep: ncol 8 (i, j, k parities), 4 (i, j parities,
@@ -202,6 +215,100 @@ __global__ void __launch_bounds__(256) k_ts_gs(TsLv L, float* __restrict__ x, co
 #pragma unroll
   for (int q = 0; q < NPT; ++q)
     if (ok[q]) x[vv[q]] = nv[q];
+}
+
+// Half of a multicoloured sweep of a 27-point level in shared-memory tiles: the planes of parity
+// ck (slices of parity ck without z coupling) get their four in-plane colours (ci, cj) = (0,0),
+// (1,0), (0,1), (1,1), which is the colour order ck*4 + ci + 2cj of the one-launch-per-colour path:
+// colours of plane k read planes k +- 1 (the other parity, unchanged by this launch) and earlier
+// colours of plane k only, so plane-by-plane order gives the same iterate bit for bit.  A CTA owns a
+// GT_X x GT_Y tile and marches over the planes of the parity with a three-plane ring; the tile is
+// staged with a GT_H = 4 halo and colour phase p recomputes the halo cells within 3 - p of the tile
+// (a colour's update reads its 26 neighbours only), so no CTA waits on another.  xin -> xout:
+// planes of the other parity are copied through (two launches, ck = 0 then 1, return the iterate
+// to the first buffer).  One HBM read and write of x per half-sweep instead of four (per colour).
+constexpr int GT_X = 64, GT_Y = 32, GT_H = 4, GT_T = 256;
+constexpr int GS_X = GT_X + 2 * GT_H, GS_Y = GT_Y + 2 * GT_H;
+
+template <bool Z>
+__global__ void __launch_bounds__(GT_T) k_ts_gs_tile(TsLv L, const float* __restrict__ xin, float* __restrict__ xout,
+                                                     const float* __restrict__ b, int ck, float omega, int chunk) {
+  __shared__ float sx[3][GS_Y * GS_X];  // planes p at slot p mod 3
+  __shared__ float sb[GS_Y * GS_X];
+  const int i0 = blockIdx.x * GT_X - GT_H, j0 = blockIdx.y * GT_Y - GT_H;
+  const int tid = threadIdx.x;
+  const size_t plane = (size_t)L.nx * L.ny;
+  auto slot = [](int p) { return ((p % 3) + 3) % 3; };
+  const int lane = tid & 31, warp = tid >> 5;
+  constexpr int NW = GT_T / 32;
+  auto stage = [&](float* dst, const float* src, int p) {  // region of plane p (0 outside the grid)
+    const bool pin = p >= 0 && p < L.nz;
+    for (int r = warp; r < GS_Y; r += NW) {
+      const int j = j0 + r;
+      const bool rin = pin && j >= 0 && j < L.ny;
+      const float* row = src + (rin ? p * plane + (size_t)j * L.nx : 0);
+      for (int c = lane; c < GS_X; c += 32) {
+        const int i = i0 + c;
+        dst[r * GS_X + c] = (rin && i >= 0 && i < L.nx) ? row[i] : 0.f;
+      }
+    }
+  };
+  auto store = [&](const float* src, int p) {  // tile interior of plane p -> xout
+    for (int r = warp; r < GT_Y; r += NW) {
+      const int j = j0 + GT_H + r;
+      if (j >= L.ny) break;
+      float* row = xout + p * plane + (size_t)j * L.nx;
+      for (int c = lane; c < GT_X; c += 32) {
+        const int i = i0 + GT_H + c;
+        if (i < L.nx) row[i] = src[(r + GT_H) * GS_X + c + GT_H];
+      }
+    }
+  };
+  bool first = true;
+  const int kend = min(L.nz, ck + 2 * (int)(blockIdx.z + 1) * chunk);  // this CTA's planes of the parity
+  for (int k = ck + 2 * (int)blockIdx.z * chunk; k < kend; k += 2) {
+    __syncthreads();  // the previous step's stores have read their slots
+    if (first && k >= 1) {
+      stage(sx[slot(k - 1)], xin, k - 1);
+      __syncthreads();
+      store(sx[slot(k - 1)], k - 1);  // the other parity's plane below the first: copied through
+    }
+    first = false;
+    stage(sx[slot(k)], xin, k);
+    if (k + 1 < L.nz) stage(sx[slot(k + 1)], xin, k + 1);
+    else if (Z) stage(sx[slot(k + 1)], xin, k + 1);  // zeros (out of the grid)
+    stage(sb, b, k);
+    __syncthreads();
+    float* xs = sx[slot(k)];
+    LdS ld;
+    ld.pm = sx[slot(k - 1)];
+    ld.p0 = xs;
+    ld.pp = sx[slot(k + 1)];
+    ld.i0 = i0; ld.j0 = j0; ld.k = k; ld.sy = GS_X;
+#pragma unroll 1
+    for (int ph = 0; ph < 4; ++ph) {
+      const int ci = ph & 1, cj = ph >> 1, m = GT_H - 1 - ph;  // cells within m of the tile
+      const int rlo = GT_H - m, clo = GT_H - m;
+      // first row / column of the region with the colour's global parity
+      const int r1 = rlo + (((j0 + rlo) & 1) != cj), c1 = clo + (((i0 + clo) & 1) != ci);
+      const int nr = (GT_Y + 2 * m - (r1 - rlo) + 1) / 2, nc = (GT_X + 2 * m - (c1 - clo) + 1) / 2;
+      for (int t = tid; t < nr * nc; t += GT_T) {
+        const int rr = t / nc, cc = t - rr * nc;
+        const int r = r1 + 2 * rr, c = c1 + 2 * cc;
+        const int i = i0 + c, j = j0 + r;
+        if (i < 0 || i >= L.nx || j < 0 || j >= L.ny) continue;
+        const int v = r * GS_X + c;
+        const float xv = xs[v];
+        float S, dg, rs;
+        ts_row<Z>(L, i, j, k, (size_t)v, ld, xv, S, dg, rs);
+        const float rv = sb[v] - (rs * xv + S);
+        xs[v] = xv + omega * rv / dg;
+      }
+      __syncthreads();
+    }
+    store(xs, k);
+    if (k + 1 < L.nz) store(sx[slot(k + 1)], k + 1);  // the other parity's plane above: copied through
+  }
 }
 
 // r = b - A x (r may be null) with fp64 partials (sum r^2, sum b^2) per block; a block row covers
@@ -765,6 +872,32 @@ static const dim3 kBlk(64, 4, 1);
 static void ts_sweep(const TsHier& H, const TsLevelH& L, float* x, const float* b, float omega, cudaStream_t s) {
   const TsLv v = dev_level(H, L);
   const bool Z = !H.key.per_slice;
+  // opt-in (GDP_TS_TILE=1): bit-identical, but measured slower than the per-colour launches on
+  // config 1 (Linear 174 vs 133 ms per step: the redundant halo phases and per-cell index math
+  // cost more than the HBM passes they save)
+  static const bool tile_env = getenv("GDP_TS_TILE") && atoi(getenv("GDP_TS_TILE")) != 0;
+  if (!L.rb && tile_env && cells(L) >= (size_t)(1 << 16)) {  // 27-point level: two tiled half-sweeps
+    // z-chunks of the parity's planes so that the grid holds ~4 CTAs per SM (planes of one parity are
+    // independent in a half-sweep; the other parity's planes at chunk ends are copied twice, same values)
+    const int tiles = ((v.nx + GT_X - 1) / GT_X) * ((v.ny + GT_Y - 1) / GT_Y);
+    const int npar = (v.nz + 1) / 2;
+    const int nch = std::max(1, std::min(npar, (148 * 4 + tiles - 1) / tiles));
+    const int chunk = (npar + nch - 1) / nch;
+    const dim3 g((v.nx + GT_X - 1) / GT_X, (v.ny + GT_Y - 1) / GT_Y, (npar + chunk - 1) / chunk);
+    float* bufs[2] = {x, H.r};  // x -> scratch (ck = 0) -> x (ck = 1)
+    for (int ck = 0; ck < 2; ++ck) {
+      const float* src = bufs[ck];
+      float* dst = bufs[ck ^ 1];
+      ProfScope ps(KC_RBGS, 6.0 * (double)cells(L), s, (double)cells(L));
+      if (ck >= v.nz) {
+        cudaMemcpyAsync(dst, src, sizeof(float) * cells(L), cudaMemcpyDeviceToDevice, s);
+        continue;
+      }
+      if (Z) k_ts_gs_tile<true><<<g, GT_T, 0, s>>>(v, src, dst, b, ck, omega, chunk);
+      else k_ts_gs_tile<false><<<g, GT_T, 0, s>>>(v, src, dst, b, ck, omega, chunk);
+    }
+    return;
+  }
   const int ncol = L.rb ? 2 : (Z ? 8 : 4);
   const double per_launch = 12.0 / ncol * (double)cells(L);  // x in + b + x out per sweep, split over colours
   for (int c = 0; c < ncol; ++c) {

@@ -5,6 +5,8 @@ hierarchy; oracle/gdp_oracle.py for Hybrid, whose finest system is the Constant 
 Bars as tests/test_gpu_parity.py: solutions within 5e-5 per phase (1e-4 end to end), relative
 residual <= 1e-6 evaluated by the oracle in fp64; operators (every Galerkin level) within fp32
 rounding of the oracle's fp64 sparse products: |y_gpu - y| <= 64 eps32 (|A| |x|)."""
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -158,3 +160,38 @@ def test_scheme_rejects_distributed_and_npr(gpu_ctx):
     with pytest.raises(gdp.GdpError):
         gdp.gdp_diffuse_z(ctx, I0, opts=gdp.default_opts(scheme="hybrid"))
     ctx.close()
+
+
+_REF_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, {root!r})
+import gdp_synth as synth, paper_1310_0041_b200 as gdp
+ctx = gdp.Ctx(0)
+out = {{}}
+for scheme in ("hybrid", "linear"):
+    for shape in {shapes!r}:
+        I0 = torch.from_numpy(synth.make_stack(shape[2], shape[1], shape[0], 9, "u8")).cuda()
+        I1, I2, r1, r2 = gdp.gdp_destripe(ctx, I0, alpha=0.01, opts=gdp.default_opts(scheme=scheme))
+        out[f"{{scheme}}_{{shape}}_1"] = I1.cpu().numpy()
+        out[f"{{scheme}}_{{shape}}_2"] = I2.cpu().numpy()
+np.savez({path!r}, **out)
+"""
+
+
+def test_tiled_half_sweeps_bit_identical_to_colour_launches(gpu_ctx, tmp_path):
+    """The shared-memory tiled half-sweeps of the 27-point levels (k_ts_gs_tile, opt-in with
+    GDP_TS_TILE=1) reproduce the default one-launch-per-colour sweeps bit for bit (same colour
+    order, same per-cell arithmetic); each variant runs in a subprocess of its own."""
+    import subprocess
+    import sys
+    shapes = [(12, 100, 90), (7, 257, 131), (33, 64, 72)]
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for tile in ("0", "1"):
+        path = str(tmp_path / f"out{tile}.npz")
+        env = dict(os.environ, GDP_TS_TILE=tile)
+        subprocess.run([sys.executable, "-c", _REF_SCRIPT.format(root=root, shapes=shapes, path=path)], env=env,
+                       check=True, timeout=600)
+        outs.append(np.load(path))
+    for key in outs[0].files:
+        assert np.array_equal(outs[0][key], outs[1][key]), key

@@ -24,6 +24,9 @@ DistPlan::~DistPlan() {
   for (auto* p : bw) if (p) cudaFree(p);
   for (auto* p : cw) if (p) cudaFree(p);
   if (fpart) cudaFree(fpart);
+  if (ev_bnd) cudaEventDestroy(ev_bnd);
+  if (ev_comm) cudaEventDestroy(ev_comm);
+  if (cs) cudaStreamDestroy(cs);
 }
 
 #define CKD(call)                                                                         \
@@ -192,22 +195,54 @@ static int team_fused_sweeps(Ctx& c, DistPlan& D, int* cur, int nu, bool prolong
     }
     RETD(comm_ghosts(c, D, D.cw.data(), s, 1));
   }
+  // Boundary first (H7): a sweep followed by another one in this pass computes its G bottom and G top
+  // planes first, hands their ghost exchange to the communication stream and computes its interior
+  // meanwhile; the next sweep waits for the exchange.  Sub-range z-marches are bit-identical to the
+  // whole-slab one (the out-of-core streamer relies on the same property); tail sweeps (restriction,
+  // norms) and z-coarsened level-1 restrictions stay whole.  The exchange issues the same NCCL calls
+  // in the same order on every rank, only on another stream.
+  bool ovl = !coarse_of(D, 0).tz.coarsened;
+  for (int i = 0; i < np; ++i) ovl = ovl && D.nzl[i] >= 2 * G + 1;
+  if (ovl && !D.cs) {
+    CKD(cudaStreamCreateWithFlags(&D.cs, cudaStreamNonBlocking));
+    CKD(cudaEventCreateWithFlags(&D.ev_bnd, cudaEventDisableTiming));
+    CKD(cudaEventCreateWithFlags(&D.ev_comm, cudaEventDisableTiming));
+  }
+  bool exchanged = false;  // the ghosts of the current source were exchanged on D.cs
   for (int k = 0; k < nu; ++k) {
     std::vector<float*>& src = *cur ? D.w1 : D.w0;
     std::vector<float*>& dst = *cur ? D.w0 : D.w1;
-    RETD(comm_ghosts(c, D, src.data(), s));
+    if (exchanged) CKD(cudaStreamWaitEvent(s, D.ev_comm, 0));
+    else RETD(comm_ghosts(c, D, src.data(), s));
+    exchanged = false;
     const bool last = k == nu - 1;
-    for (int i = 0; i < np; ++i) {
+    const int t = last ? tail : 0;
+    const bool split = ovl && !last;
+    auto sweep = [&](int i, int zlo, int zhi) {
       const Level& L = D.parts[i]->lv[0];
       Level C = coarse_of(D, i);
       if (prolong && D.ff > 1)
         C.x = D.cw[i] + ((long long)G - D.parts[i]->lv[1].z0) * (long long)C.nx * C.ny;
       const long long off = (long long)G - D.z0[i];  // window offset of global plane 0 (planes)
-      const int t = last ? tail : 0;
       const int n = fused_sweep3d(L, C, src[i] + off * (long long)pl, dst[i] + off * (long long)pl,
                                   D.bw[i] + off * (long long)pl, false, prolong && k == 0, t,
-                                  t == 2 ? D.fpart + items : nullptr, s, (int)D.z0[i], (int)(D.z0[i] + D.nzl[i]));
+                                  t == 2 ? D.fpart + items : nullptr, s, zlo, zhi);
       if (t == 2) items += n;  // partials of the norms sweep only
+    };
+    if (!split) {
+      for (int i = 0; i < np; ++i) sweep(i, (int)D.z0[i], (int)(D.z0[i] + D.nzl[i]));
+    } else {
+      for (int i = 0; i < np; ++i) {
+        const int z0 = (int)D.z0[i], z1 = (int)(D.z0[i] + D.nzl[i]);
+        sweep(i, z0, z0 + G);
+        sweep(i, z1 - G, z1);
+      }
+      CKD(cudaEventRecord(D.ev_bnd, s));
+      CKD(cudaStreamWaitEvent(D.cs, D.ev_bnd, 0));
+      RETD(comm_ghosts(c, D, dst.data(), D.cs));
+      CKD(cudaEventRecord(D.ev_comm, D.cs));
+      for (int i = 0; i < np; ++i) sweep(i, (int)D.z0[i] + G, (int)(D.z0[i] + D.nzl[i]) - G);
+      exchanged = true;
     }
     *cur ^= 1;
   }

@@ -106,6 +106,10 @@ struct DistPlan {
   std::vector<float*> cw;                    // split level 1: x with G ghost planes (prolongation source)
   double2* fpart = nullptr;                  // norm partials of the fused up pass (all local slabs)
   size_t fpart_cap = 0;
+  // boundary-first halo overlap: the ghost exchange of a sweep's output runs on
+  // a communication stream while the sweep's interior planes are computed
+  cudaStream_t cs = nullptr;
+  cudaEvent_t ev_bnd = nullptr, ev_comm = nullptr;
   ~DistPlan();
 };
 

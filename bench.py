@@ -265,6 +265,19 @@ def ncu_traffic(kernel_class):
         return None
 
 
+def ncu_step():
+    """DRAM bytes over kernel time of every kernel of one destripe step, from the
+    committed ncu capture (tools/ncu_step.py -> profiles/ncu_step_r02.json), or None."""
+    p = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "ncu_step_r02.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return {"GBps": d["dram_GBps"], "bytes": d["dram_bytes"], "kernel_ms": d["kernel_ms"],
+                "launches": d["launches"], "source": d["source"]}
+    except Exception:  # noqa: BLE001
+        return None
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -346,15 +359,18 @@ def main():
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     reps = []
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     e0.record(stream)
-    for _ in range(args.steps):
+    for i in range(args.steps):
         reps.append(step())
+        evs[i].record(stream)  # per-step boundaries (the solve synchronises its stream per cycle anyway)
     e1.record(stream)
     torch.cuda.synchronize()
     barrier()
     clocks = clk.stop()
     launches = gdp.kernel_launch_count() - launches0
     ms = e0.elapsed_time(e1)
+    step_ms = [e0.elapsed_time(evs[0])] + [evs[i - 1].elapsed_time(evs[i]) for i in range(1, args.steps)]
     t = torch.tensor([ms], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -396,7 +412,9 @@ def main():
                                         "GBps_model": round(s["alg_bytes"] / max(s["ms"], 1e-9) / 1e6, 1)}
                             for s in stats}}
     whole_gbs = sum(s["alg_bytes_8d"] for s in stats) / (tot_ms * 1e-3) / 1e9
+    nstep = ncu_step()
     whole = {"alg_GBps_8d": whole_gbs, "frac_8d": whole_gbs / peak if peak else None,
+             "ncu_dram": nstep,
              "alg_GBps_design_model": sum(s["alg_bytes"] for s in stats) / (tot_ms * 1e-3) / 1e9,
              "alg_bytes_per_voxel_8d": sum(s["alg_bytes_8d"] for s in stats) / args.steps / (nvox * world),
              "kernel_ms_per_step": tot_ms / args.steps}
@@ -465,6 +483,11 @@ def main():
                            "global_dims": [nx, ny, nzg]},
                 "vcycles": {"phase1": conv[0][0], "phase2": conv[0][1], "rel_res_phase1": conv[0][2],
                             "rel_res_phase2_max_slice": conv[0][3], "all_converged": status_ok},
+                # the median of the runs and both phases separately (device time of each
+                # solve from its own events)
+                "step_ms_median": float(np.median(step_ms)), "step_ms_min": float(min(step_ms)),
+                "phase_ms_median": {"phase1": float(np.median([r[2].get("seconds", 0.0) * 1e3 for r in reps])),
+                                    "phase2": float(np.median([r[3].get("seconds", 0.0) * 1e3 for r in reps]))},
                 "roofline": roofline, "whole_step": whole,
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
                 "gpu_launches_per_step": launches / max(args.steps, 1), "clocks": clocks}

@@ -135,6 +135,9 @@ struct Stream1 {
   size_t sI = 1;
   DevBuf xin[2], xout[2], iw[2], bw[2];
   DevBuf xin16[2], xout16[2];  // fp16 staging of the iterate's window (NEXT-4)
+  int R = 0;                      // partial residency: planes [0, R) of the iterate live in xres (HBM)
+  DevBuf xres;                    //   (no host-link traffic per pass; copied back once at the end)
+  DevBuf i0res;                   // I0 resident on the device (when every plane of x is)
   static constexpr int MAXS = 8;  // sweeps per streaming pass (NEXT-2)
   int ms = 1;                     // sweeps one pass may hold (window memory)
   DevBuf sw[MAXS][2];             // input windows of stages 1.. of a multi-sweep pass
@@ -149,6 +152,67 @@ struct Stream1 {
 enum { SP_INIT = 0, SP_SUMS = 2, SP_WIDEN = 3 };  // the sweeps stream through stream_sweeps
 
 static int chunk_count(const Stream1& S) { return (S.nz + S.C - 1) / S.C; }
+
+// Planes [from, to) of the iterate into the device window dst: the resident planes (< S.R) by a
+// device copy, the others over the host link (fp32, or the fp16 scratch converted on the way).
+static int x_load(Stream1& S, float* dst, void* stage16, int from, int to, bool in16, cudaStream_t st) {
+  const long long pl = S.plane;
+  const int r = std::min(to, S.R);
+  if (r > from)
+    SK(cudaMemcpyAsync(dst, S.xres.f() + (long long)from * pl, sizeof(float) * pl * (r - from), cudaMemcpyDeviceToDevice, st));
+  const int h0 = std::max(from, S.R);
+  if (to > h0) {
+    float* d = dst + (long long)(h0 - from) * pl;
+    const long long n = pl * (to - h0);
+    if (in16) {
+      SK(cudaMemcpyAsync(stage16, S.h16 + h0 * pl, sizeof(__half) * n, cudaMemcpyHostToDevice, st));
+      convert(stage16, d, n, false, st);
+      S.h2d += (long long)sizeof(__half) * n;
+    } else {
+      SK(cudaMemcpyAsync(d, S.xh + h0 * pl, sizeof(float) * n, cudaMemcpyHostToDevice, st));
+      S.h2d += (long long)sizeof(float) * n;
+    }
+  }
+  return GDP_OK;
+}
+// the I0 planes [lo, hi) into the device window
+static int i0_load(Stream1& S, unsigned char* dst, int lo, int hi, cudaStream_t st) {
+  const long long pl = S.plane;
+  if (hi <= lo) return GDP_OK;
+  if (S.i0res.p) {
+    SK(cudaMemcpyAsync(dst, S.i0res.u() + S.sI * lo * pl, S.sI * pl * (hi - lo), cudaMemcpyDeviceToDevice, st));
+  } else {
+    SK(cudaMemcpyAsync(dst, static_cast<const unsigned char*>(S.I0h) + S.sI * lo * pl, S.sI * pl * (hi - lo),
+                       cudaMemcpyHostToDevice, st));
+    S.h2d += (long long)S.sI * pl * (hi - lo);
+  }
+  return GDP_OK;
+}
+// fp16 conversion of the host part of output planes [lo, hi) held in src (on the kernel stream)
+static void x_convert_out(Stream1& S, const float* src, void* stage16, int lo, int hi, cudaStream_t st) {
+  const int h0 = std::max(lo, S.R);
+  if (hi > h0) convert(src + (long long)(h0 - lo) * S.plane, stage16, S.plane * (hi - h0), true, st);
+}
+// output planes [lo, hi) of src back to the iterate: resident planes by a device copy, the others over
+// the host link (fp32, or the fp16 staged by x_convert_out)
+static int x_store(Stream1& S, const float* src, const void* stage16, int lo, int hi, bool out16, cudaStream_t st) {
+  const long long pl = S.plane;
+  const int r = std::min(hi, S.R);
+  if (r > lo)
+    SK(cudaMemcpyAsync(S.xres.f() + (long long)lo * pl, src, sizeof(float) * pl * (r - lo), cudaMemcpyDeviceToDevice, st));
+  const int h0 = std::max(lo, S.R);
+  if (hi > h0) {
+    const long long n = pl * (hi - h0);
+    if (out16) {
+      SK(cudaMemcpyAsync(S.h16 + h0 * pl, stage16, sizeof(__half) * n, cudaMemcpyDeviceToHost, st));
+      S.d2h += (long long)sizeof(__half) * n;
+    } else {
+      SK(cudaMemcpyAsync(S.xh + h0 * pl, src + (long long)(h0 - lo) * pl, sizeof(float) * n, cudaMemcpyDeviceToHost, st));
+      S.d2h += (long long)sizeof(float) * n;
+    }
+  }
+  return GDP_OK;
+}
 
 // One streaming pass over the finest level.  SP_INIT: x0 = I0 (written to the host iterate),
 // initial residual partials (per plane rows).  SP_SUMS: per-plane fp64 sums of x and I0 (the mean pin).  SP_WIDEN:
@@ -166,25 +230,8 @@ static int stream_pass(Stream1& S, int kind, bool in16 = false, bool out16 = fal
     const int wlo = std::max(p_lo - 3, 0), whi = std::min(p_hi + 3, S.nz);
     // ---- inputs of the window: retained planes (device), new planes (host), I0 (host)
     SK(cudaStreamWaitEvent(T.ci, T.evK[b], 0));  // chunk k-2's kernels are done with buffer set b
-    if (kind != SP_INIT) {
-      const int from = p_lo, to = p_hi;  // SP_SUMS / SP_WIDEN: the chunk's own planes
-      const long long base = 0;
-      if (to > from && in16) {
-        SK(cudaMemcpyAsync(S.xin16[b].p, S.h16 + from * pl, sizeof(__half) * pl * (to - from),
-                           cudaMemcpyHostToDevice, T.ci));
-        convert(S.xin16[b].p, S.xin[b].f() + base * pl, pl * (to - from), false, T.ci);
-        S.h2d += (long long)sizeof(__half) * pl * (to - from);
-      } else if (to > from) {
-        SK(cudaMemcpyAsync(S.xin[b].f() + base * pl, S.xh + from * pl, sizeof(float) * pl * (to - from),
-                           cudaMemcpyHostToDevice, T.ci));
-        S.h2d += (long long)sizeof(float) * pl * (to - from);
-      }
-    }
-    if (kind != SP_WIDEN) {
-      SK(cudaMemcpyAsync(S.iw[b].u(), static_cast<const unsigned char*>(S.I0h) + S.sI * wlo * pl,
-                         S.sI * pl * (whi - wlo), cudaMemcpyHostToDevice, T.ci));
-      S.h2d += (long long)S.sI * pl * (whi - wlo);
-    }
+    if (kind != SP_INIT) SR(x_load(S, S.xin[b].f(), S.xin16[b].p, p_lo, p_hi, in16, T.ci));  // the chunk's own planes
+    if (kind != SP_WIDEN) SR(i0_load(S, S.iw[b].u(), wlo, whi, T.ci));
     SK(cudaEventRecord(T.evI[b], T.ci));
     // ---- kernels
     SK(cudaStreamWaitEvent(T.s, T.evI[b], 0));
@@ -207,21 +254,13 @@ static int stream_pass(Stream1& S, int kind, bool in16 = false, bool out16 = fal
                         static_cast<double2*>(S.part.p), static_cast<double2*>(S.psum.p) + p_lo, T.s);
       (void)per;
     }
-    if (kind != SP_SUMS && out16) convert(S.xout[b].f(), S.xout16[b].p, pl * (p_hi - p_lo), true, T.s);
+    if (kind != SP_SUMS && out16) x_convert_out(S, S.xout[b].f(), S.xout16[b].p, p_lo, p_hi, T.s);
     SK(cudaGetLastError());
     SK(cudaEventRecord(T.evK[b], T.s));
-    // ---- output of the window back to the host iterate (in place: no later window reads it)
+    // ---- output of the window back to the iterate (in place: no later window reads it)
     if (kind != SP_SUMS) {
       SK(cudaStreamWaitEvent(T.co, T.evK[b], 0));
-      if (out16) {
-        SK(cudaMemcpyAsync(S.h16 + p_lo * pl, S.xout16[b].p, sizeof(__half) * pl * (p_hi - p_lo),
-                           cudaMemcpyDeviceToHost, T.co));
-        S.d2h += (long long)sizeof(__half) * pl * (p_hi - p_lo);
-      } else {
-        SK(cudaMemcpyAsync(S.xh + p_lo * pl, S.xout[b].f(), sizeof(float) * pl * (p_hi - p_lo),
-                           cudaMemcpyDeviceToHost, T.co));
-        S.d2h += (long long)sizeof(float) * pl * (p_hi - p_lo);
-      }
+      SR(x_store(S, S.xout[b].f(), S.xout16[b].p, p_lo, p_hi, out16, T.co));
       SK(cudaEventRecord(T.evO[b], T.co));
     }
   }
@@ -280,21 +319,8 @@ static int stream_sweeps(Stream1& S, const std::vector<Stage>& st, long long* it
                          cudaMemcpyDeviceToDevice, T.ci));
       from = phi[0];
     }
-    if (whi[0] > from) {
-      const long long n = pl * (whi[0] - from);
-      if (in16) {
-        SK(cudaMemcpyAsync(S.xin16[b].p, S.h16 + from * pl, sizeof(__half) * n, cudaMemcpyHostToDevice, T.ci));
-        convert(S.xin16[b].p, S.xin[b].f() + (from - wlo[0]) * pl, n, false, T.ci);
-        S.h2d += (long long)sizeof(__half) * n;
-      } else {
-        SK(cudaMemcpyAsync(S.xin[b].f() + (from - wlo[0]) * pl, S.xh + from * pl, sizeof(float) * n,
-                           cudaMemcpyHostToDevice, T.ci));
-        S.h2d += (long long)sizeof(float) * n;
-      }
-    }
-    SK(cudaMemcpyAsync(S.iw[b].u(), static_cast<const unsigned char*>(S.I0h) + S.sI * blo * pl,
-                       S.sI * pl * (bhi - blo), cudaMemcpyHostToDevice, T.ci));
-    S.h2d += (long long)S.sI * pl * (bhi - blo);
+    if (whi[0] > from) SR(x_load(S, S.xin[b].f() + (from - wlo[0]) * pl, S.xin16[b].p, from, whi[0], in16, T.ci));
+    SR(i0_load(S, S.iw[b].u(), blo, bhi, T.ci));
     SK(cudaEventRecord(T.evI[b], T.ci));
     // ---- kernels: the rhs of the window, then the stages in order
     SK(cudaStreamWaitEvent(T.s, T.evI[b], 0));
@@ -319,19 +345,13 @@ static int stream_sweeps(Stream1& S, const std::vector<Stage>& st, long long* it
       if (tail == 2) items += n;  // the norms stage's partials, in plane order over the chunks
     }
     const int olo = lo[m - 1], ohi = hi[m - 1];
-    if (ohi > olo && out16) convert(S.xout[b].f(), S.xout16[b].p, pl * (ohi - olo), true, T.s);
+    if (ohi > olo && out16) x_convert_out(S, S.xout[b].f(), S.xout16[b].p, olo, ohi, T.s);
     SK(cudaGetLastError());
     SK(cudaEventRecord(T.evK[b], T.s));
-    // ---- the last stage's planes back to the host iterate (no later window reads them)
+    // ---- the last stage's planes back to the iterate (no later window reads them)
     if (ohi > olo) {
       SK(cudaStreamWaitEvent(T.co, T.evK[b], 0));
-      if (out16) {
-        SK(cudaMemcpyAsync(S.h16 + olo * pl, S.xout16[b].p, sizeof(__half) * pl * (ohi - olo), cudaMemcpyDeviceToHost, T.co));
-        S.d2h += (long long)sizeof(__half) * pl * (ohi - olo);
-      } else {
-        SK(cudaMemcpyAsync(S.xh + olo * pl, S.xout[b].f(), sizeof(float) * pl * (ohi - olo), cudaMemcpyDeviceToHost, T.co));
-        S.d2h += (long long)sizeof(float) * pl * (ohi - olo);
-      }
+      SR(x_store(S, S.xout[b].f(), S.xout16[b].p, olo, ohi, out16, T.co));
     }
     SK(cudaEventRecord(T.evO[b], T.co));
     for (int j = 0; j < m; ++j) { plo[j] = wlo[j]; phi[j] = whi[j]; }
@@ -397,8 +417,14 @@ int stream_diffuse_z(Ctx& C, const void* I0h, int tI, float* xh, long long nx, l
   // the budget is a target: below two-plane windows the streamer still runs (C = 2) and only
   // a failing allocation is an error; windows beyond a few dozen planes buy nothing (the pipeline
   // keeps two in flight) and would crowd out the coarse levels' lazily allocated buffers
-  const double left = std::min((double)budget - coarse - 4.0 * 1024 * 1024, hard) - (double)pl * fixed_planes(MS);
-  int Cp = (int)std::min<double>(std::min<double>((double)nz, 64.0), std::max(2.0, std::floor(left / ((double)pl * per_plane_of(MS)))));
+  const double wcap = std::min((double)budget - coarse - 4.0 * 1024 * 1024, hard) - (double)pl * fixed_planes(MS);
+  // a13 partial residency first: with 4-plane chunks, what the budget leaves holds planes [0, R) of the
+  // iterate in HBM (no host-link traffic for them per pass); the chunks then take what remains, up to
+  // 16 planes (two chunks in flight keep the copies and kernels overlapped; more buys nothing)
+  const double xb = 4.0 * (double)pl, margin = 64.0 * 1024 * 1024;
+  const int Rp = (int)std::max(0.0, std::min((double)nz, std::floor((wcap - margin - 4.0 * pl * per_plane_of(MS)) / xb)));
+  const double left = wcap - margin - xb * Rp;
+  int Cp = (int)std::min<double>(std::min<double>((double)nz, 16.0), std::max(2.0, std::floor(left / ((double)pl * per_plane_of(MS)))));
   Cp = std::max(2, Cp & ~1);
   Stream1 S;
   S.I0h = I0h; S.xh = xh; S.tI = tI; S.nx = nx; S.ny = ny; S.plane = pl; S.nz = (int)nz; S.C = Cp; S.sI = sI;
@@ -409,6 +435,8 @@ int stream_diffuse_z(Ctx& C, const void* I0h, int tI, float* xh, long long nx, l
   if (!fusable3d(S.H->lv[0], S.H->lv[1], o))
     return set_err(GDP_EINVAL, "out-of-core phase 1 needs an x/y-coarsened second level (stack too small?)");
   const int cz = (int)nz + 6;  // no window exceeds the stack plus its halo
+  size_t free_before = 0;
+  SK(cudaMemGetInfo(&free_before, &totb));
   for (int b = 0; b < 2; ++b) {
     SR(S.xin[b].alloc(sizeof(float) * pl * std::min(Cp + 6, cz)));
     SR(S.xout[b].alloc(sizeof(float) * pl * std::min(Cp + 3 * (MS - 1), cz)));
@@ -431,6 +459,21 @@ int stream_diffuse_z(Ctx& C, const void* I0h, int tI, float* xh, long long nx, l
                                  (size_t)norms_blocks_per_plane((int)nx, (int)ny) * Cp});
   SR(S.part.alloc(sizeof(double2) * S.part_cap));
   SR(S.psum.alloc(sizeof(double2) * nz));
+  // a13 partial residency (sized above): planes [0, R) of the iterate stay in HBM (one copy back at
+  // the end), and I0 as well when every plane does and the budget allows
+  {
+    size_t free_now = 0;
+    SK(cudaMemGetInfo(&free_now, &totb));
+    const double windows = (double)free_before - (double)free_now;
+    const double avail = std::min((double)budget - coarse - windows, 0.85 * (double)free_now - coarse) - margin;
+    S.R = (int)std::max(0.0, std::min((double)Rp, std::floor(avail / xb)));
+    if (S.R > 0) SR(S.xres.alloc(sizeof(float) * pl * S.R));
+    if (S.R == nz && avail - xb * nz >= (double)sI * pl * nz) {
+      SR(S.i0res.alloc(sI * pl * nz));
+      SK(cudaMemcpy(S.i0res.p, I0h, sI * pl * nz, cudaMemcpyHostToDevice));  // once, before any stream work
+      S.h2d += (long long)sI * pl * nz;
+    }
+  }
   SR(S.st.create());
   cudaEvent_t e0, e1;
   SK(cudaEventCreate(&e0));
@@ -527,6 +570,11 @@ int stream_diffuse_z(Ctx& C, const void* I0h, int tI, float* xh, long long nx, l
   for (long long z = 0; z < nz; ++z) { sx += hp[z].x; si += hp[z].y; }
   cudaFreeHost(hp);
   *shift_out = (si - sx) / ((double)pl * nz);
+  if (S.R > 0) {  // the resident planes back to the caller's iterate, once
+    SK(cudaMemcpyAsync(S.xh, S.xres.p, sizeof(float) * pl * S.R, cudaMemcpyDeviceToHost, S.st.s));
+    SK(cudaStreamSynchronize(S.st.s));
+    S.d2h += (long long)sizeof(float) * pl * S.R;
+  }
   SK(cudaEventRecord(e1, S.st.s));
   SK(cudaEventSynchronize(e1));
   float ms = 0.f;

@@ -367,6 +367,29 @@ def test_out_of_core_stream_fusion_bit_identical(gpu_ctx, shape, budget, fuse):
     assert np.array_equal(a1, b1)
 
 
+@pytest.mark.parametrize("budget_mb", [1600, 2000])
+def test_out_of_core_partial_residency(gpu_ctx, budget_mb):
+    """a13 partial residency: a budget below the in-core need (~2.1 GB for 96 x 1024^2 u8) keeps as
+    many planes of the iterate in HBM as it can (1.6 GB: about half of them; 2.0 GB: all, and I0):
+    the iterate stays bit-identical to the in-core solve and fewer bytes cross the host link than
+    when everything streams."""
+    shape = (96, 1024, 1024)
+    I0 = synth.make_stack(shape[2], shape[1], shape[0], 63, "u8")
+    t0 = torch.from_numpy(I0).pin_memory()
+    outs = []
+    for b in (0, budget_mb << 20, 1):
+        I1 = torch.empty(shape, dtype=torch.float32).pin_memory()
+        I2 = torch.empty(shape, dtype=torch.float32).pin_memory()
+        r1, r2 = gdp.gdp_destripe_host(gpu_ctx, t0, I2, I1=I1, alpha=0.01, hbm_budget_bytes=b,
+                                       opts=gdp.default_opts(fmg=0, fmg_slices=0))
+        assert r1["status"] == "GDP_OK" and r2["status"] == "GDP_OK", (b, r1, r2)
+        outs.append((I1.numpy().copy(), r1))
+    (a1, ra), (p1, rp), (s1, rs) = outs
+    assert ra["vcycles"] == rp["vcycles"] == rs["vcycles"]
+    assert np.array_equal(a1, p1) and np.array_equal(a1, s1)
+    assert 0 < rp["hbm_bytes_est"] < rs["hbm_bytes_est"]
+
+
 # ------------------------------------------------------------------ NEXT-1: the §6 NPR filter
 @pytest.mark.parametrize("shape,dtype,params", [((16, 135, 240), "u8", (0.001, 1.25, 5 / 255)),
                                                 ((9, 63, 65), "f32", (0.01, 1.0, 0.05)),

@@ -89,12 +89,20 @@ extern "C" int gdp_destripe_host(gdp_ctx* ctx, const void* I0_host, gdp_dtype dt
     }
     double shift = 0.0;
     const int tI = dtype == GDP_U8 ? 0 : 1;
+    float* x_res = nullptr;  // phase 1's HBM-resident planes of I1, read in place by phase 2
+    int R = 0;
     int st1 = stream_diffuse_z(C, I0_host, tI, xh, dims.nx, dims.ny, dims.nz, W.bx, W.by, W.bz, o, budget, rep1,
-                               &shift);
+                               &shift, &x_res, &R);
     int st2 = GDP_OK;
-    if (st1 == GDP_OK || st1 == GDP_ENOCONV)
-      st2 = stream_slices(C, ctx, I0_host, dtype, xh, I2_host, dims.nx, dims.ny, dims.nz, alpha, shift, o, budget,
-                          rep2);
+    if (st1 == GDP_OK || st1 == GDP_ENOCONV) {
+      // phase 2 batches need their own HBM; the resident planes keep what the budget gave phase 1
+      const size_t budget2 = budget > (size_t)R * (size_t)dims.nx * dims.ny * 4 ? budget - (size_t)R * dims.nx * dims.ny * 4 : 1;
+      st2 = stream_slices(C, ctx, I0_host, dtype, xh, I2_host, dims.nx, dims.ny, dims.nz, alpha, shift, o, budget2,
+                          rep2, x_res, R);
+    } else if (x_res) {  // failed phase 1: no phase 2, but the caller still gets the best iterate
+      cudaMemcpy(xh, x_res, sizeof(float) * (size_t)R * dims.nx * dims.ny, cudaMemcpyDeviceToHost);
+    }
+    if (x_res) cudaFree(x_res);
     if (scratch) cudaFreeHost(scratch);
     if (st1 != GDP_OK && st1 != GDP_ENOCONV) return st1;
     if (st2 != GDP_OK) return st2;

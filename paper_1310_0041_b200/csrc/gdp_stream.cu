@@ -375,7 +375,7 @@ static int read_norms(Stream1& S, double2* plane_rows, int per, int nplanes, dou
 // is the pin, applied by the caller).
 int stream_diffuse_z(Ctx& C, const void* I0h, int tI, float* xh, long long nx, long long ny, long long nz,
                      float bx, float by, float bz, const gdp_opts& o0, size_t budget, gdp_report* rep,
-                     double* shift_out) {
+                     double* shift_out, float** keep_x, int* keep_R) {
   gdp_opts o = o0;
   o.fused |= 2;
   if (o.nu_pre < 1 || o.nu_post < 1)  // every finest-level pass is a fused sweep (restrict / prolong inside)
@@ -570,7 +570,12 @@ int stream_diffuse_z(Ctx& C, const void* I0h, int tI, float* xh, long long nx, l
   for (long long z = 0; z < nz; ++z) { sx += hp[z].x; si += hp[z].y; }
   cudaFreeHost(hp);
   *shift_out = (si - sx) / ((double)pl * nz);
-  if (S.R > 0) {  // the resident planes back to the caller's iterate, once
+  if (S.R > 0 && keep_x && keep_R) {  // phase 2 takes the resident planes over (reads them in place)
+    SK(cudaStreamSynchronize(S.st.s));
+    *keep_x = S.xres.f();
+    *keep_R = S.R;
+    S.xres.p = nullptr;
+  } else if (S.R > 0) {  // the resident planes back to the caller's iterate, once
     SK(cudaMemcpyAsync(S.xh, S.xres.p, sizeof(float) * pl * S.R, cudaMemcpyDeviceToHost, S.st.s));
     SK(cudaStreamSynchronize(S.st.s));
     S.d2h += (long long)sizeof(float) * pl * S.R;
@@ -591,7 +596,7 @@ int stream_diffuse_z(Ctx& C, const void* I0h, int tI, float* xh, long long nx, l
 // back so the caller's I1 is the pinned solution).
 int stream_slices(Ctx& C, gdp_ctx* cctx, const void* I0h, gdp_dtype dtype, float* I1h, float* I2h, long long nx,
                   long long ny, long long nz, float alpha, double shift, const gdp_opts& o, size_t budget,
-                  gdp_report* rep) {
+                  gdp_report* rep, const float* I1dev, int R) {
   const long long pl = nx * ny;
   const size_t sI = dtype == GDP_U8 ? 1 : 4;
   // per slice on the device: I0, I1, I2 of two batches + the batch hierarchy (~4 fp32 arrays)
@@ -617,14 +622,22 @@ int stream_slices(Ctx& C, gdp_ctx* cctx, const void* I0h, gdp_dtype dtype, float
     SK(cudaStreamWaitEvent(T.ci, T.evO[b], 0));
     SK(cudaMemcpyAsync(i0[b].u(), static_cast<const unsigned char*>(I0h) + sI * z * pl, sI * pl * nb,
                        cudaMemcpyHostToDevice, T.ci));
-    SK(cudaMemcpyAsync(i1[b].f(), I1h + z * pl, sizeof(float) * pl * nb, cudaMemcpyHostToDevice, T.ci));
+    // I1 of the batch: slices still resident from phase 1 by a device copy, the others from the host
+    const long long zr = std::min<long long>(z + nb, R);
+    if (zr > z)
+      SK(cudaMemcpyAsync(i1[b].f(), I1dev + z * pl, sizeof(float) * pl * (zr - z), cudaMemcpyDeviceToDevice, T.ci));
+    const long long zh = std::max<long long>(z, R);
+    if (z + nb > zh)
+      SK(cudaMemcpyAsync(i1[b].f() + (zh - z) * pl, I1h + zh * pl, sizeof(float) * pl * (z + nb - zh),
+                         cudaMemcpyHostToDevice, T.ci));
     SK(cudaEventRecord(T.evI[b], T.ci));
     SK(cudaStreamWaitEvent(T.s, T.evI[b], 0));
-    if (fs != 0.f) {
-      launch_add_scalar(i1[b].f(), pl * nb, fs, T.s);  // a10 on the way (k_add_scalar arithmetic)
+    if (fs != 0.f || z < R) {  // the pinned (or still device-resident) I1 of the batch back to the caller
+      if (fs != 0.f) launch_add_scalar(i1[b].f(), pl * nb, fs, T.s);  // a10 on the way (k_add_scalar arithmetic)
       SK(cudaEventRecord(T.evK[b], T.s));
       SK(cudaStreamWaitEvent(T.co, T.evK[b], 0));
-      SK(cudaMemcpyAsync(I1h + z * pl, i1[b].f(), sizeof(float) * pl * nb, cudaMemcpyDeviceToHost, T.co));
+      const long long z1 = fs != 0.f ? z + nb : std::min<long long>(z + nb, R);
+      SK(cudaMemcpyAsync(I1h + z * pl, i1[b].f(), sizeof(float) * pl * (z1 - z), cudaMemcpyDeviceToHost, T.co));
     }
     gdp_report r{};
     gdp_dims d{nx, ny, nb};

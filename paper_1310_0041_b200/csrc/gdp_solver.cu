@@ -1315,7 +1315,7 @@ int gdp_residual(gdp_ctx* ctx, const float* x, const float* b, float* r, gdp_dim
 int gdp_scheme_levels(gdp_ctx* ctx, int scheme, gdp_dims dims, gdp_weights W, float alpha, int per_slice,
                       const gdp_opts* opts, int* nlev, gdp_dims* level_dims, int* coarsened, int max_levels) {
   RET(check_common(ctx, dims, 0, dims.nz));
-  RET(check_params(W, per_slice ? alpha : alpha));
+  RET(check_params(W, alpha));
   if (!nlev) return set_err(GDP_EINVAL, "null nlev");
   gdp_opts o = resolve_opts(opts);
   o.scheme = scheme;

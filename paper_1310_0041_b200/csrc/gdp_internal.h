@@ -186,13 +186,17 @@ struct HostPin {
 };
 // keep_x / keep_R (may be NULL): phase 1 hands its HBM-resident planes [0, R) of the iterate (unpinned
 // I1) to the caller instead of copying them back (cudaFree by the caller); phase 2 then reads them
-// in place and writes the pinned I1 back (NEXT-2 (ii): phase 2 consumes phase 1's output on the device)
+// in place and writes the pinned I1 back (NEXT-2 (ii): phase 2 consumes phase 1's output on the device).
+// xh == NULL (the caller does not want I1; needs keep_x / keep_R): the host planes [R, nz) live in a
+// pinned scratch returned in *host_scratch (cudaFreeHost by the caller); the returned *host_scratch
+// minus R planes is the host iterate's base pointer for phase 2.
 int stream_diffuse_z(Ctx& C, const void* I0h, int tI, float* xh, long long nx, long long ny, long long nz,
                      float bx, float by, float bz, const gdp_opts& o, size_t budget, gdp_report* rep,
-                     double* shift_out, float** keep_x = nullptr, int* keep_R = nullptr);
+                     double* shift_out, float** keep_x = nullptr, int* keep_R = nullptr,
+                     float** host_scratch = nullptr);
 int stream_slices(Ctx& C, gdp_ctx* cctx, const void* I0h, gdp_dtype dtype, float* I1h, float* I2h, long long nx,
                   long long ny, long long nz, float alpha, double shift, const gdp_opts& o, size_t budget,
-                  gdp_report* rep, const float* I1dev = nullptr, int R = 0);
+                  gdp_report* rep, const float* I1dev = nullptr, int R = 0, bool write_i1 = true);
 
 void jacobi_eig(int n, std::vector<double>& A, std::vector<double>& Q, std::vector<double>& lam);
 

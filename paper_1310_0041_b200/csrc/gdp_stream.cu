@@ -375,7 +375,9 @@ static int read_norms(Stream1& S, double2* plane_rows, int per, int nplanes, dou
 // is the pin, applied by the caller).
 int stream_diffuse_z(Ctx& C, const void* I0h, int tI, float* xh, long long nx, long long ny, long long nz,
                      float bx, float by, float bz, const gdp_opts& o0, size_t budget, gdp_report* rep,
-                     double* shift_out, float** keep_x, int* keep_R) {
+                     double* shift_out, float** keep_x, int* keep_R, float** host_scratch) {
+  if (!xh && (!keep_x || !keep_R || !host_scratch))
+    return set_err(GDP_EINVAL, "stream_diffuse_z: a NULL host iterate needs the residency hand-off");
   gdp_opts o = o0;
   o.fused |= 2;
   if (o.nu_pre < 1 || o.nu_post < 1)  // every finest-level pass is a fused sweep (restrict / prolong inside)
@@ -468,6 +470,12 @@ int stream_diffuse_z(Ctx& C, const void* I0h, int tI, float* xh, long long nx, l
     const double avail = std::min((double)budget - coarse - windows, 0.85 * (double)free_now - coarse) - margin;
     S.R = (int)std::max(0.0, std::min((double)Rp, std::floor(avail / xb)));
     if (S.R > 0) SR(S.xres.alloc(sizeof(float) * pl * S.R));
+    if (!xh) {  // no caller I1: a pinned scratch for the planes that do not stay in HBM only
+      float* scr = nullptr;
+      if (S.R < nz) SK(cudaMallocHost(&scr, sizeof(float) * pl * (nz - S.R)));
+      *host_scratch = scr;
+      S.xh = scr ? scr - (long long)S.R * pl : nullptr;  // planes >= R are addressed as in a full array
+    }
     if (S.R == nz && avail - xb * nz >= (double)sI * pl * nz) {
       SR(S.i0res.alloc(sI * pl * nz));
       SK(cudaMemcpy(S.i0res.p, I0h, sI * pl * nz, cudaMemcpyHostToDevice));  // once, before any stream work
@@ -596,7 +604,7 @@ int stream_diffuse_z(Ctx& C, const void* I0h, int tI, float* xh, long long nx, l
 // back so the caller's I1 is the pinned solution).
 int stream_slices(Ctx& C, gdp_ctx* cctx, const void* I0h, gdp_dtype dtype, float* I1h, float* I2h, long long nx,
                   long long ny, long long nz, float alpha, double shift, const gdp_opts& o, size_t budget,
-                  gdp_report* rep, const float* I1dev, int R) {
+                  gdp_report* rep, const float* I1dev, int R, bool write_i1) {
   const long long pl = nx * ny;
   const size_t sI = dtype == GDP_U8 ? 1 : 4;
   // per slice on the device: I0, I1, I2 of two batches + the batch hierarchy (~4 fp32 arrays)
@@ -632,7 +640,7 @@ int stream_slices(Ctx& C, gdp_ctx* cctx, const void* I0h, gdp_dtype dtype, float
                          cudaMemcpyHostToDevice, T.ci));
     SK(cudaEventRecord(T.evI[b], T.ci));
     SK(cudaStreamWaitEvent(T.s, T.evI[b], 0));
-    if (fs != 0.f || z < R) {  // the pinned (or still device-resident) I1 of the batch back to the caller
+    if (write_i1 && (fs != 0.f || z < R)) {  // the pinned (or still device-resident) I1 back to the caller
       if (fs != 0.f) launch_add_scalar(i1[b].f(), pl * nb, fs, T.s);  // a10 on the way (k_add_scalar arithmetic)
       SK(cudaEventRecord(T.evK[b], T.s));
       SK(cudaStreamWaitEvent(T.co, T.evK[b], 0));

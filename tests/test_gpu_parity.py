@@ -388,6 +388,14 @@ def test_out_of_core_partial_residency(gpu_ctx, budget_mb):
     assert ra["vcycles"] == rp["vcycles"] == rs["vcycles"]
     assert np.array_equal(a1, p1) and np.array_equal(a1, s1)
     assert 0 < rp["hbm_bytes_est"] < rs["hbm_bytes_est"]
+    # without a caller I1 the streamer pins a scratch for the non-resident planes only: same I2
+    I2a = torch.empty(shape, dtype=torch.float32).pin_memory()
+    I2b = torch.empty(shape, dtype=torch.float32).pin_memory()
+    o = gdp.default_opts(fmg=0, fmg_slices=0)
+    gdp.gdp_destripe_host(gpu_ctx, t0, I2a, I1=torch.empty(shape, dtype=torch.float32).pin_memory(), alpha=0.01,
+                          hbm_budget_bytes=budget_mb << 20, opts=o)
+    gdp.gdp_destripe_host(gpu_ctx, t0, I2b, alpha=0.01, hbm_budget_bytes=budget_mb << 20, opts=o)
+    assert torch.equal(I2a, I2b)
 
 
 # ------------------------------------------------------------------ NEXT-1: the §6 NPR filter

@@ -640,8 +640,8 @@ int stream_slices(Ctx& C, gdp_ctx* cctx, const void* I0h, gdp_dtype dtype, float
                          cudaMemcpyHostToDevice, T.ci));
     SK(cudaEventRecord(T.evI[b], T.ci));
     SK(cudaStreamWaitEvent(T.s, T.evI[b], 0));
+    if (fs != 0.f) launch_add_scalar(i1[b].f(), pl * nb, fs, T.s);  // a10 on the way (k_add_scalar arithmetic)
     if (write_i1 && (fs != 0.f || z < R)) {  // the pinned (or still device-resident) I1 back to the caller
-      if (fs != 0.f) launch_add_scalar(i1[b].f(), pl * nb, fs, T.s);  // a10 on the way (k_add_scalar arithmetic)
       SK(cudaEventRecord(T.evK[b], T.s));
       SK(cudaStreamWaitEvent(T.co, T.evK[b], 0));
       const long long z1 = fs != 0.f ? z + nb : std::min<long long>(z + nb, R);

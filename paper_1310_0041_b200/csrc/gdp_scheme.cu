@@ -668,6 +668,8 @@ struct TsKey {
 struct TsHier {
   TsKey key{};
   std::vector<TsLevelH> lv;
+  Hier* main7 = nullptr;     // Hybrid 3D: the main path's hierarchy of the same finest operator, whose
+                             // fused z-march sweeps smooth level 0 (non-owning: cached in the Ctx)
   float* r = nullptr;        // residual scratch of level 0 size
   float* b0 = nullptr;       // finest rhs (whole solves)
   double2* part = nullptr;   // block partials
@@ -869,6 +871,36 @@ static dim3 grid_xy(int nx, int ny, int nz, dim3 blk) {
 
 static const dim3 kBlk(64, 4, 1);
 
+static void ts_sweep(const TsHier& H, const TsLevelH& L, float* x, const float* b, float omega, cudaStream_t s);
+
+// nu sweeps of a level.  The Hybrid finest level of a 3D system is the main path's 7-point operator,
+// so its sweeps run on the main path's fused red-black z-march (one HBM pass per sweep instead of one
+// per colour; ping-pong through the residual scratch, a final copy when nu is odd).
+static void ts_smooth(const TsHier& H, const TsLevelH& L, float* x, const float* b, int nu, float omega,
+                      cudaStream_t s) {
+  if (&L == &H.lv[0] && L.rb && !H.key.per_slice && H.main7 && H.main7->lv.size() > 1 && nu > 0) {
+    const Level& M0 = H.main7->lv[0];
+    const Level& M1 = H.main7->lv[1];
+    gdp_opts fo;
+    gdp_opts_default(&fo);
+    fo.fused = 2;
+    if (fusable3d(M0, M1, fo)) {
+      for (int k = 0; k < nu; ++k) {
+        const float* src = (k & 1) ? H.r : x;
+        float* dst = (k & 1) ? x : H.r;
+        int items = 0;
+        if (sweep3dv_ok(M0, M1, false, src, dst, b) &&
+            fused_sweep3dv(M0, M1, src, dst, b, false, false, 0, nullptr, s, &items) == GDP_OK)
+          continue;
+        fused_sweep3d(M0, M1, src, dst, b, false, false, 0, nullptr, s);
+      }
+      if (nu & 1) cudaMemcpyAsync(x, H.r, sizeof(float) * (size_t)L.n[0] * L.n[1] * L.n[2], cudaMemcpyDeviceToDevice, s);
+      return;
+    }
+  }
+  for (int k = 0; k < nu; ++k) ts_sweep(H, L, x, b, omega, s);
+}
+
 static void ts_sweep(const TsHier& H, const TsLevelH& L, float* x, const float* b, float omega, cudaStream_t s) {
   const TsLv v = dev_level(H, L);
   const bool Z = !H.key.per_slice;
@@ -958,7 +990,7 @@ static int ts_cycle(TsHier& H, float* x0, const float* b0, int nu_pre, int nu_po
     const TsLevelH& L = H.lv[l];
     const TsLevelH& C = H.lv[l + 1];
     if (l > 0) CKS(cudaMemsetAsync(xs[l], 0, sizeof(float) * cells(L), s));
-    for (int k = 0; k < nu_pre; ++k) ts_sweep(H, L, xs[l], bs[l], omega, s);
+    ts_smooth(H, L, xs[l], bs[l], nu_pre, omega, s);
     RETS(ts_resid(H, L, xs[l], bs[l], H.r, false, s));
     const TsXfer T = xfer_of(L, C);
     ProfScope ps(KC_RESTRICT, 4.0 * (double)cells(L) + 4.0 * (double)cells(C), s);
@@ -994,7 +1026,7 @@ static int ts_cycle(TsHier& H, float* x0, const float* b0, int nu_pre, int nu_po
       ProfScope ps(KC_PROLONG, 8.0 * (double)cells(L) + 4.0 * (double)cells(C), s, (double)cells(L));
       k_ts_prolong<<<grid_xy(L.n[0], L.n[1], L.n[2], kBlk), kBlk, 0, s>>>(T, xs[l + 1], xs[l]);
     }
-    for (int k = 0; k < nu_post; ++k) ts_sweep(H, L, xs[l], bs[l], omega, s);
+    ts_smooth(H, L, xs[l], bs[l], nu_post, omega, s);
   }
   CKS(cudaGetLastError());
   return GDP_OK;
@@ -1091,10 +1123,25 @@ static TsKey key_of(int scheme, long long nx, long long ny, long long nz, float 
   return k;
 }
 
+// Hybrid, 3D: the main path's hierarchy for the same (dims, W, alpha) lends its fused finest-level
+// sweeps to ts_smooth (the Hybrid finest operator is the Constant one)
+static int attach_main7(Ctx& C, TsHier& H, const gdp_opts& o) {
+  if (H.key.scheme != GDP_SCHEME_HYBRID || H.key.per_slice || H.main7) return GDP_OK;
+  static const bool off = getenv("GDP_HYBRID_MAIN7") && atoi(getenv("GDP_HYBRID_MAIN7")) == 0;
+  if (off) return GDP_OK;
+  HierKey k{};
+  k.nx = H.key.nx; k.ny = H.key.ny; k.nzl = H.key.nz; k.z0 = 0; k.nzg = H.key.nz;
+  k.bx = H.key.bx; k.by = H.key.by; k.bz = H.key.bz; k.alpha = H.key.alpha;
+  k.coarse_max = o.coarse_max;
+  k.omega = o.omega;
+  return C.get_hier(k, &H.main7);
+}
+
 int scheme_diffuse_z(Ctx& C, const void* I0, int tI, float* I1, long long nx, long long ny, long long nz, float bx,
                      float by, float bz, float alpha, const gdp_opts& o, gdp_report* rep, cudaStream_t s) {
   TsHier* H;
   RETS(ts_get(C, key_of(o.scheme, nx, ny, nz, bx, by, bz, alpha, 0, o), &H));
+  RETS(attach_main7(C, *H, o));
   const long long before = g_launches.load();
   const size_t n = (size_t)nx * ny * nz;
   if (!H->b0) CKS(cudaMalloc(&H->b0, sizeof(float) * n));
@@ -1170,6 +1217,7 @@ int scheme_vcycle(Ctx& C, float* x, const float* b, long long nx, long long ny, 
                   float bz, float alpha, const gdp_opts& o, double* rel, cudaStream_t s) {
   TsHier* H;
   RETS(ts_get(C, key_of(o.scheme, nx, ny, nz, bx, by, bz, alpha, 0, o), &H));
+  RETS(attach_main7(C, *H, o));
   RETS(ts_cycle(*H, x, b, o.nu_pre, o.nu_post, o.omega, s));
   if (rel) {
     double nb;

@@ -898,6 +898,14 @@ static void ts_smooth(const TsHier& H, const TsLevelH& L, float* x, const float*
       return;
     }
   }
+  if (&L == &H.lv[0] && L.rb && H.key.per_slice && H.main7 && H.main7->lv.size() > 1 && L.n[0] >= 128 &&
+      nu >= 1 && nu <= 2) {  // per-slice 5-point finest level: the main path's row-marching nu-sweep pass
+    const Level& M0 = H.main7->lv[0];
+    const Level& M1 = H.main7->lv[1];
+    rows2d_pass(false, nu, M0, M1, x, H.r, b, false, nullptr, s, false);
+    cudaMemcpyAsync(x, H.r, sizeof(float) * (size_t)L.n[0] * L.n[1] * L.n[2], cudaMemcpyDeviceToDevice, s);
+    return;
+  }
   for (int k = 0; k < nu; ++k) ts_sweep(H, L, x, b, omega, s);
 }
 
@@ -955,6 +963,15 @@ static int ts_ensure_part(TsHier& H, size_t n) {
 // residual of level l (into r, may be null) and, if sums != null, per-slice (or whole) fp64 sums
 static int ts_resid(TsHier& H, const TsLevelH& L, const float* x, const float* b, float* r, bool norms,
                     cudaStream_t s) {
+  if (&L == &H.lv[0] && L.rb && H.main7) {
+    // Hybrid finest level: the main path's residual kernel (same 7-/5-point operator), per-plane sums
+    Hier& M = *H.main7;
+    const Level& M0 = M.lv[0];
+    launch_norms(M0.K, x, M0.xlo, M0.xhi, RhsK{b, nullptr, nullptr, 0.f, 0}, RHS_B, 1, r, M.partials, M.plane_sums, s);
+    if (norms) CKS(cudaMemcpyAsync(H.sums, M.plane_sums, sizeof(double2) * L.n[2], cudaMemcpyDeviceToDevice, s));
+    CKS(cudaGetLastError());
+    return GDP_OK;
+  }
   const TsLv v = dev_level(H, L);
   const dim3 g((v.nx + kBlk.x - 1) / kBlk.x, (v.ny + kBlk.y * NPT - 1) / (kBlk.y * NPT), v.nz);
   const size_t nb = (size_t)g.x * g.y;
@@ -1126,12 +1143,12 @@ static TsKey key_of(int scheme, long long nx, long long ny, long long nz, float 
 // Hybrid, 3D: the main path's hierarchy for the same (dims, W, alpha) lends its fused finest-level
 // sweeps to ts_smooth (the Hybrid finest operator is the Constant one)
 static int attach_main7(Ctx& C, TsHier& H, const gdp_opts& o) {
-  if (H.key.scheme != GDP_SCHEME_HYBRID || H.key.per_slice || H.main7) return GDP_OK;
+  if (H.key.scheme != GDP_SCHEME_HYBRID || H.main7) return GDP_OK;
   static const bool off = getenv("GDP_HYBRID_MAIN7") && atoi(getenv("GDP_HYBRID_MAIN7")) == 0;
   if (off) return GDP_OK;
   HierKey k{};
   k.nx = H.key.nx; k.ny = H.key.ny; k.nzl = H.key.nz; k.z0 = 0; k.nzg = H.key.nz;
-  k.bx = H.key.bx; k.by = H.key.by; k.bz = H.key.bz; k.alpha = H.key.alpha;
+  k.bx = H.key.bx; k.by = H.key.by; k.bz = H.key.per_slice ? 0.f : H.key.bz; k.alpha = H.key.alpha;
   k.coarse_max = o.coarse_max;
   k.omega = o.omega;
   return C.get_hier(k, &H.main7);
@@ -1184,6 +1201,7 @@ int scheme_slices(Ctx& C, const void* I0, int tI, const float* I1, float* I2, lo
                   long long nz, float alpha, float vshift, const gdp_opts& o, gdp_report* rep, cudaStream_t s) {
   TsHier* H;
   RETS(ts_get(C, key_of(o.scheme, nx, ny, nz, 1.f, 1.f, 0.f, alpha, 1, o), &H));
+  RETS(attach_main7(C, *H, o));
   const long long before = g_launches.load();
   const size_t n = (size_t)nx * ny * nz;
   if (!H->b0) CKS(cudaMalloc(&H->b0, sizeof(float) * n));

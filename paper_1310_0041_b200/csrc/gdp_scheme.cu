@@ -426,6 +426,37 @@ __global__ void __launch_bounds__(256) k_ts_prolong(TsXfer T, const float* __res
   xf[v] += s;
 }
 
+// the same with x coarsened: a thread owns the fine pair (2I, 2I + 1), which shares the coarse
+// columns I, I + 1 of each parent row (half the coarse loads); per cell the sum is the generic
+// kernel's (rows outer, columns inner), so both kernels give the same values
+__global__ void __launch_bounds__(256) k_ts_prolong2(TsXfer T, const float* __restrict__ xc, float* __restrict__ xf) {
+  const int I = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = blockIdx.y * blockDim.y + threadIdx.y;
+  const int k = blockIdx.z;
+  const int i0 = 2 * I;
+  if (i0 >= T.fx || j >= T.fy) return;
+  int Iy[2], Iz[2];
+  float wy[2], wz[2];
+  const int ny = xf_parents(j, T.co_y, T.cy, Iy, wy);
+  const int nz = xf_parents(k, T.co_z, T.cz, Iz, wz);
+  const bool has1 = i0 + 1 < T.fx, two = I + 1 < T.cx;  // odd cell exists / has a right parent
+  float s0 = 0.f, s1 = 0.f;
+  for (int c = 0; c < nz; ++c)
+    for (int bb = 0; bb < ny; ++bb) {
+      const float* row = xc + ((size_t)Iz[c] * T.cy + Iy[bb]) * T.cx;
+      const float a = __ldg(row + I);
+      const float t0 = 1.f * a;
+      float t1 = two ? 0.5f * a : 1.f * a;
+      if (two) t1 += 0.5f * __ldg(row + I + 1);
+      const float w = wz[c] * wy[bb];
+      s0 += w * t0;
+      s1 += w * t1;
+    }
+  float* out = xf + ((size_t)k * T.fy + j) * T.fx + i0;
+  out[0] += s0;
+  if (has1) out[1] += s1;
+}
+
 // coarsest solve by fast diagonalisation, one CTA per independent system (all slices of a
 // per-slice level share the x / y factors): y = V^T b along each axis, y /= (alpha + sum beta
 // lambda) (0 for the null mode), x = V y.  Vd: n_d x n_d row-major, column p = eigenvector p.
@@ -1041,7 +1072,8 @@ static int ts_cycle(TsHier& H, float* x0, const float* b0, int nu_pre, int nu_po
     const TsXfer T = xfer_of(L, C);
     {
       ProfScope ps(KC_PROLONG, 8.0 * (double)cells(L) + 4.0 * (double)cells(C), s, (double)cells(L));
-      k_ts_prolong<<<grid_xy(L.n[0], L.n[1], L.n[2], kBlk), kBlk, 0, s>>>(T, xs[l + 1], xs[l]);
+      if (T.co_x) k_ts_prolong2<<<grid_xy((L.n[0] + 1) / 2, L.n[1], L.n[2], kBlk), kBlk, 0, s>>>(T, xs[l + 1], xs[l]);
+      else k_ts_prolong<<<grid_xy(L.n[0], L.n[1], L.n[2], kBlk), kBlk, 0, s>>>(T, xs[l + 1], xs[l]);
     }
     ts_smooth(H, L, xs[l], bs[l], nu_post, omega, s);
   }

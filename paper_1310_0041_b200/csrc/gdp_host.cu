@@ -86,20 +86,23 @@ extern "C" int gdp_destripe_host(gdp_ctx* ctx, const void* I0_host, gdp_dtype dt
     double shift = 0.0;
     const int tI = dtype == GDP_U8 ? 0 : 1;
     float* x_res = nullptr;  // phase 1's HBM-resident planes of I1, read in place by phase 2
+    void* i0_res = nullptr;  // and I0, when it stayed resident too
     int R = 0;
     int st1 = stream_diffuse_z(C, I0_host, tI, xh, dims.nx, dims.ny, dims.nz, W.bx, W.by, W.bz, o, budget, rep1,
-                               &shift, &x_res, &R, &scratch);
+                               &shift, &x_res, &R, &scratch, &i0_res);
     if (!xh) xh = scratch ? scratch - (size_t)R * dims.nx * dims.ny : nullptr;
     int st2 = GDP_OK;
     if (st1 == GDP_OK || st1 == GDP_ENOCONV) {
       // phase 2 batches need their own HBM; the resident planes keep what the budget gave phase 1
-      const size_t budget2 = budget > (size_t)R * (size_t)dims.nx * dims.ny * 4 ? budget - (size_t)R * dims.nx * dims.ny * 4 : 1;
+      const size_t held = (size_t)R * dims.nx * dims.ny * 4 + (i0_res ? n * sI : 0);
+      const size_t budget2 = budget > held ? budget - held : 1;
       st2 = stream_slices(C, ctx, I0_host, dtype, xh, I2_host, dims.nx, dims.ny, dims.nz, alpha, shift, o, budget2,
-                          rep2, x_res, R, I1_host != nullptr);
+                          rep2, x_res, R, I1_host != nullptr, i0_res);
     } else if (x_res && I1_host) {  // failed phase 1: no phase 2, but the caller still gets the best iterate
       cudaMemcpy(I1_host, x_res, sizeof(float) * (size_t)R * dims.nx * dims.ny, cudaMemcpyDeviceToHost);
     }
     if (x_res) cudaFree(x_res);
+    if (i0_res) cudaFree(i0_res);
     if (scratch) cudaFreeHost(scratch);
     if (st1 != GDP_OK && st1 != GDP_ENOCONV) return st1;
     if (st2 != GDP_OK) return st2;

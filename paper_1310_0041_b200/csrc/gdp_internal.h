@@ -193,10 +193,11 @@ struct HostPin {
 int stream_diffuse_z(Ctx& C, const void* I0h, int tI, float* xh, long long nx, long long ny, long long nz,
                      float bx, float by, float bz, const gdp_opts& o, size_t budget, gdp_report* rep,
                      double* shift_out, float** keep_x = nullptr, int* keep_R = nullptr,
-                     float** host_scratch = nullptr);
+                     float** host_scratch = nullptr, void** keep_i0 = nullptr);
 int stream_slices(Ctx& C, gdp_ctx* cctx, const void* I0h, gdp_dtype dtype, float* I1h, float* I2h, long long nx,
                   long long ny, long long nz, float alpha, double shift, const gdp_opts& o, size_t budget,
-                  gdp_report* rep, const float* I1dev = nullptr, int R = 0, bool write_i1 = true);
+                  gdp_report* rep, const float* I1dev = nullptr, int R = 0, bool write_i1 = true,
+                  const void* I0dev = nullptr);
 
 void jacobi_eig(int n, std::vector<double>& A, std::vector<double>& Q, std::vector<double>& lam);
 

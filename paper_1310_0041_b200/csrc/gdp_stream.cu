@@ -375,7 +375,7 @@ static int read_norms(Stream1& S, double2* plane_rows, int per, int nplanes, dou
 // is the pin, applied by the caller).
 int stream_diffuse_z(Ctx& C, const void* I0h, int tI, float* xh, long long nx, long long ny, long long nz,
                      float bx, float by, float bz, const gdp_opts& o0, size_t budget, gdp_report* rep,
-                     double* shift_out, float** keep_x, int* keep_R, float** host_scratch) {
+                     double* shift_out, float** keep_x, int* keep_R, float** host_scratch, void** keep_i0) {
   if (!xh && (!keep_x || !keep_R || !host_scratch))
     return set_err(GDP_EINVAL, "stream_diffuse_z: a NULL host iterate needs the residency hand-off");
   gdp_opts o = o0;
@@ -583,6 +583,10 @@ int stream_diffuse_z(Ctx& C, const void* I0h, int tI, float* xh, long long nx, l
     *keep_x = S.xres.f();
     *keep_R = S.R;
     S.xres.p = nullptr;
+    if (keep_i0 && S.i0res.p) {  // I0 resident too: phase 2 reads it in place
+      *keep_i0 = S.i0res.p;
+      S.i0res.p = nullptr;
+    }
   } else if (S.R > 0) {  // the resident planes back to the caller's iterate, once
     SK(cudaMemcpyAsync(S.xh, S.xres.p, sizeof(float) * pl * S.R, cudaMemcpyDeviceToHost, S.st.s));
     SK(cudaStreamSynchronize(S.st.s));
@@ -604,7 +608,7 @@ int stream_diffuse_z(Ctx& C, const void* I0h, int tI, float* xh, long long nx, l
 // back so the caller's I1 is the pinned solution).
 int stream_slices(Ctx& C, gdp_ctx* cctx, const void* I0h, gdp_dtype dtype, float* I1h, float* I2h, long long nx,
                   long long ny, long long nz, float alpha, double shift, const gdp_opts& o, size_t budget,
-                  gdp_report* rep, const float* I1dev, int R, bool write_i1) {
+                  gdp_report* rep, const float* I1dev, int R, bool write_i1, const void* I0dev) {
   const long long pl = nx * ny;
   const size_t sI = dtype == GDP_U8 ? 1 : 4;
   // per slice on the device: I0, I1, I2 of two batches + the batch hierarchy (~4 fp32 arrays)
@@ -628,8 +632,12 @@ int stream_slices(Ctx& C, gdp_ctx* cctx, const void* I0h, gdp_dtype dtype, float
     const int b = k & 1;
     const long long nb = std::min(B, nz - z);
     SK(cudaStreamWaitEvent(T.ci, T.evO[b], 0));
-    SK(cudaMemcpyAsync(i0[b].u(), static_cast<const unsigned char*>(I0h) + sI * z * pl, sI * pl * nb,
-                       cudaMemcpyHostToDevice, T.ci));
+    if (I0dev)  // I0 still resident from phase 1
+      SK(cudaMemcpyAsync(i0[b].u(), static_cast<const unsigned char*>(I0dev) + sI * z * pl, sI * pl * nb,
+                         cudaMemcpyDeviceToDevice, T.ci));
+    else
+      SK(cudaMemcpyAsync(i0[b].u(), static_cast<const unsigned char*>(I0h) + sI * z * pl, sI * pl * nb,
+                         cudaMemcpyHostToDevice, T.ci));
     // I1 of the batch: slices still resident from phase 1 by a device copy, the others from the host
     const long long zr = std::min<long long>(z + nb, R);
     if (zr > z)

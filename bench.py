@@ -164,6 +164,24 @@ def run_cpu_baseline_slice(cfg, alpha):
     return out
 
 
+def run_cpu_baseline_linear(cfg, alpha):
+    """NEXT-3 Linear: its own oracle (oracle/fem_linear.py: the B-spline finite-element systems, scipy
+    sparse + numpy CG to 1e-10, both phases) on a 128 x 128 x 32 crop of the config generator."""
+    import os as _os
+    from oracle import fem_linear
+    I0 = cpu_sample(cfg, {"nx": 128, "ny": 128, "nz": 32})
+    t = time.perf_counter()
+    I1, i1 = fem_linear.diffuse_z_linear(I0, W, return_info=True)
+    _, i2 = fem_linear.screened_poisson_slices_linear(I0, I1, alpha, return_info=True)
+    el = time.perf_counter() - t
+    info = cpu_info()
+    return {"value": I0.size / el, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": sample_desc(I0, "Linear oracle (oracle/fem_linear.py: scipy sparse + numpy CG to 1e-10, "
+                                  "both phases)"),
+            "cpu_model": info["cpu_model"], "nproc": _os.cpu_count(), "seconds": el,
+            "cg_iterations": {"phase1": int(i1["iterations"]), "phase2_sum_over_slices": int(i2["iterations"])}}
+
+
 def reference_arm(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -462,8 +480,10 @@ def main():
                "timing": "host wall clock around gdp_destripe_host (blocking), max over ranks"}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.scheme == "constant":
-        cpu = run_cpu_baseline(args.config, args.alpha)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        # Hybrid solves the Constant system (same oracle); Linear has its own finite-element oracle
+        cpu = (run_cpu_baseline_linear(args.config, args.alpha) if args.scheme == "linear"
+               else run_cpu_baseline(args.config, args.alpha))
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,

@@ -39,7 +39,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     objdir = os.path.join(HERE, "build")
     os.makedirs(objdir, exist_ok=True)
     flags = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v" if verbose else "-O3",
-                    "-I", os.path.join(ROOT, "include"), "-I", CSRC]
+                    "-I", os.path.join(ROOT, "include"), "-I", CSRC] + os.environ.get("GDP_NVCC_DEFS", "").split()
     objs = []
     procs = []
     for src in SOURCES:

@@ -704,9 +704,14 @@ void fused_down2d(const Level& L, const Level& C, const float* xin, float* xout,
   // row-marching kernel (gdp_rows2d.cu) for wide planes: no row halo, no barriers (measured
   // 0.81 vs 1.12 ms on a 1024^2 x 128 down pass); the tile kernel below elsewhere.
   // prolong (FMG start): x += P C.x, added at load by the row kernel (coarse rows staged in
-  // shared memory; +0.2 ms at 1024^2 x 128 against 0.31 ms for its own pass), else by its own pass
+  // shared memory) on planes under 1M cells, else by its own pass
   if (C.tx.coarsened && C.ty.coarsened && L.nx >= 128) {
-    rows2d_pass(true, nu, L, C, xin, xout, R.b, zero_x, nullptr, s, prolong);
+    // planes of >= 1M cells: the prolongation by its own pass measured faster at 1024^2 x 128
+    // (0.31 + 0.48 ms against 0.99 ms with the coarse rows staged inside the row kernel)
+    const bool split = prolong && !zero_x && (long long)L.nx * L.ny >= (1LL << 20);
+    if (split)
+      launch_prolong(L.K, const_cast<float*>(xin), C.tx, C.ty, C.tz, C.nx, C.ny, C.nzl, C.z0, C.x, C.xlo, C.xhi, s);
+    rows2d_pass(true, nu, L, C, xin, xout, R.b, zero_x, nullptr, s, prolong && !split);
     return;
   }
   if (prolong)

@@ -417,6 +417,9 @@ __global__ void __launch_bounds__(256) k_init(LevelK L, RhsK R, float* __restric
     };
     float rm[4], rc[4], rp[4], dn[4], up[4];
     float acc[4] = {0.f, 0.f, 0.f, 0.f};  // X.bc: restriction of r0 (per coarse column)
+    float wxc[4];                          // X.bc: the columns' restriction weights (row invariant)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) wxc[c] = X.bc ? rweight(X.tx, gx0 + c) : 1.f;
     ldrow(pbase + (long long)(y0 - 1) * nx, y0 - 1 >= 0, rm);
     ldrow(pbase + (long long)y0 * nx, y0 < L.ny, rc);
     for (int gy = y0; gy < y1; ++gy) {
@@ -489,7 +492,7 @@ __global__ void __launch_bounds__(256) k_init(LevelK L, RhsK R, float* __restric
             float a = first ? 0.f : acc[h];
 #pragma unroll
             for (int c = 2 * h; c < 2 * h + 2; ++c)
-              if (in[c]) a = __fmaf_rn(rw3(1.f, wy, rweight(X.tx, gx0 + c)), ro[c], a);
+              if (in[c]) a = __fmaf_rn(rw3(1.f, wy, wxc[c]), ro[c], a);
             acc[h] = a;
             if (last && in[2 * h]) X.bc[cbase + (gx0 >> 1) + h] = a;
           }

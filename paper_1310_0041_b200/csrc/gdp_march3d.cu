@@ -733,7 +733,7 @@ int fused_sweep3d(const Level& L, const Level& C, const float* xin, float* xout,
   plan3d(L.K, zc, zlo, zhi, P);
   const double N = (double)L.nx * L.ny * (zhi - zlo), Nc = (double)C.nx * C.ny * C.nzl * (zhi - zlo) / L.nzl;
   const double bytes = N * ((zero_x ? 4.0 : 8.0) + 4.0) + ((tail == 1 || prolong) ? Nc * 4.0 : 0.0);
-  ProfScope ps(tail == 1 || !prolong ? KC_DOWN3D : KC_UP3D, bytes, s, zhi - zlo == L.nzl ? N : 0.0, true);
+  ProfScope ps(tail == 2 || prolong ? KC_UP3D : KC_DOWN3D, bytes, s, zhi - zlo == L.nzl ? N : 0.0, true);
   if (prolong) {
     if (tail == 2) { if (zc) launch_m3<2, true, true>(P, s); else launch_m3<2, true, false>(P, s); }
     else { if (zc) launch_m3<0, true, true>(P, s); else launch_m3<0, true, false>(P, s); }

@@ -475,6 +475,7 @@ __global__ void __launch_bounds__(MT, 1) k_m3v(const __grid_constant__ Sweep P) 
           const float wz = ZC ? rweight(P.tz, q) : 1.f;
           const bool first = !ZC || ZP == 0;
           float2 acc[2] = {first ? f2(0.f) : racc[0], first ? f2(0.f) : racc[1]};
+          float2 nr = f2(0.f), nb = f2(0.f);  // norms: this plane's 16 cells in fp32, then fp64 once
           // order per coarse pair: (rows 2m: c 0, c 1), (rows 2m + 1: c 0, c 1) = fy outer, fx inner
           static_for<8>([&](auto Ic) {
             constexpr int i = decltype(Ic)::value;
@@ -489,17 +490,19 @@ __global__ void __launch_bounds__(MT, 1) k_m3v(const __grid_constant__ Sweep P) 
               const float2 n = __ffma2_rn(w, r, ac);
               if (lane_full && rfull) ac = n;
               else ac = make_float2(cin[CC] && rin[RR] ? n.x : ac.x, cin[CC] && rin[RR + 2] ? n.y : ac.y);
-            } else if (TAIL == TAIL_NORMS && pin && cin[CC]) {
-              if (rint[RR] && rin[RR]) {
-                sr += (double)r.x * (double)r.x;
-                sbb += (double)bb.x * (double)bb.x;
-              }
-              if (rint[RR + 2] && rin[RR + 2]) {
-                sr += (double)r.y * (double)r.y;
-                sbb += (double)bb.y * (double)bb.y;
-              }
+            } else if (TAIL == TAIL_NORMS) {
+              const bool mx = pin && cin[CC] && rint[RR] && rin[RR];
+              const bool my = pin && cin[CC] && rint[RR + 2] && rin[RR + 2];
+              const float2 rm = make_float2(mx ? r.x : 0.f, my ? r.y : 0.f);
+              const float2 bm = make_float2(mx ? bb.x : 0.f, my ? bb.y : 0.f);
+              nr = __ffma2_rn(rm, rm, nr);
+              nb = __ffma2_rn(bm, bm, nb);
             }
           });
+          if (TAIL == TAIL_NORMS) {
+            sr += (double)nr.x + (double)nr.y;
+            sbb += (double)nb.x + (double)nb.y;
+          }
           if (TAIL == TAIL_RESTRICT && pin) {
             const bool last = !ZC || ZP == 1 || q == nzg - 1;
             if (last) {
@@ -656,7 +659,7 @@ int fused_sweep3dv(const Level& L, const Level& C, const float* xin, float* xout
   }
   const double N = (double)L.nx * L.ny * L.nzl, Nc = (double)C.nx * C.ny * C.nzl;
   const double bytes = N * ((zero_x ? 4.0 : 8.0) + 4.0) + ((tail == 1 || prolong) ? Nc * 4.0 : 0.0);
-  ProfScope ps(tail == 1 || !prolong ? KC_DOWN3D : KC_UP3D, bytes, s, N, true);
+  ProfScope ps(tail == 2 || prolong ? KC_UP3D : KC_DOWN3D, bytes, s, N, true);  // the norms sweep ends the up pass
   cudaError_t e;
   using namespace mv;
   if (prolong) {

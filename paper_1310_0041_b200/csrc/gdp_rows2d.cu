@@ -188,6 +188,8 @@ __device__ __forceinline__ void rows2d_march(const Rows2D& P, float4 (*sx)[R2_WA
 
   float2 racc = f2(0.f);  // down: restriction accumulated over the two child rows
   double sr = 0.0, sbb = 0.0;
+  float2 nr = make_float2(0.f, 0.f), nb = nr;  // norms: up to 8 rows (32 cells) in fp32, then fp64
+  int nrows = 0;
 
   // (A x) of pack PK of the row in X[KO] (KS south, KN north), apply_from order (z terms exact 0)
   auto stencil = [&](auto PKc, const Row4& Xo, const Row4& Xs, const Row4& Xn, float2 yl, float2 yr) -> float2 {
@@ -314,10 +316,18 @@ __device__ __forceinline__ void rows2d_march(const Rows2D& P, float4 (*sx)[R2_WA
           }
         } else if (!DOWN && pin) {
           const float2 bA = Bv[KO].A, bB = Bv[KO].B;
-          if (cin[0]) { sr = fma((double)rA.x, (double)rA.x, sr); sbb = fma((double)bA.x, (double)bA.x, sbb); }
-          if (cin[1]) { sr = fma((double)rB.x, (double)rB.x, sr); sbb = fma((double)bB.x, (double)bB.x, sbb); }
-          if (cin[2]) { sr = fma((double)rA.y, (double)rA.y, sr); sbb = fma((double)bA.y, (double)bA.y, sbb); }
-          if (cin[3]) { sr = fma((double)rB.y, (double)rB.y, sr); sbb = fma((double)bB.y, (double)bB.y, sbb); }
+          const float2 ra = make_float2(cin[0] ? rA.x : 0.f, cin[2] ? rA.y : 0.f);
+          const float2 rb = make_float2(cin[1] ? rB.x : 0.f, cin[3] ? rB.y : 0.f);
+          const float2 ba = make_float2(cin[0] ? bA.x : 0.f, cin[2] ? bA.y : 0.f);
+          const float2 bbv = make_float2(cin[1] ? bB.x : 0.f, cin[3] ? bB.y : 0.f);
+          nr = __ffma2_rn(rb, rb, __ffma2_rn(ra, ra, nr));
+          nb = __ffma2_rn(bbv, bbv, __ffma2_rn(ba, ba, nb));
+          if (++nrows == 8) {
+            sr += (double)nr.x + (double)nr.y;
+            sbb += (double)nb.x + (double)nb.y;
+            nr = nb = make_float2(0.f, 0.f);
+            nrows = 0;
+          }
         }
       }
       if (pin && lane_any) {  // store row q
@@ -341,6 +351,8 @@ __device__ __forceinline__ void rows2d_march(const Rows2D& P, float4 (*sx)[R2_WA
   }
   if (t < tend) step(IC<0>{}, t);
   if (!DOWN && P.partials) {
+    sr += (double)nr.x + (double)nr.y;
+    sbb += (double)nb.x + (double)nb.y;
     for (int o = 16; o > 0; o >>= 1) {
       sr += __shfl_down_sync(FULL, sr, o);
       sbb += __shfl_down_sync(FULL, sbb, o);

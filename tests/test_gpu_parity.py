@@ -231,10 +231,11 @@ def test_fused_3d_bit_identical_to_reference(gpu_ctx, shape, dtype):
         reps.append(rep)
     for k in range(1, len(outs)):
         assert np.array_equal(outs[0], outs[k]), k
-        # the reported residual history too (fp64 norm sums in another order: rounding only)
+        # the reported residual history too (norm sums in another order, the fused tails adding
+        # up to 32 squares per thread in fp32 before fp64: relative 1e-6)
         n = reps[0]["vcycles"] + 1
         assert reps[k]["vcycles"] == reps[0]["vcycles"], k
-        np.testing.assert_allclose(reps[k]["rel_res"][:n], reps[0]["rel_res"][:n], rtol=1e-9, atol=0)
+        np.testing.assert_allclose(reps[k]["rel_res"][:n], reps[0]["rel_res"][:n], rtol=1e-6, atol=0)
 
 
 @pytest.mark.parametrize("nu", [(1, 1), (2, 1), (1, 2), (2, 2), (3, 1)])
@@ -273,7 +274,7 @@ def test_loopback_partition_bit_identical(gpu_ctx, shape, world, fmg):
         lb.close()
     # norms are fp64 sums in different orders (fused initial residual vs per-slab partials)
     assert r1["vcycles"] == r2["vcycles"]
-    assert np.allclose(r1["rel_res"], r2["rel_res"], rtol=1e-9, atol=0)
+    assert np.allclose(r1["rel_res"], r2["rel_res"], rtol=1e-6, atol=0)
     assert np.array_equal(ref.cpu().numpy(), out.cpu().numpy())
     assert np.abs(host(out) - O.diffuse_z(I0)).max() <= TOL_X
 
@@ -295,7 +296,7 @@ def test_loopback_fused_partition_bit_identical(gpu_ctx, shape, world, fmg):
     finally:
         lb.close()
     assert r1["vcycles"] == r2["vcycles"]
-    assert np.allclose(r1["rel_res"], r2["rel_res"], rtol=1e-9, atol=0)
+    assert np.allclose(r1["rel_res"], r2["rel_res"], rtol=1e-6, atol=0)
     assert np.array_equal(ref.cpu().numpy(), out.cpu().numpy())
 
 

@@ -7,10 +7,10 @@ import paper_1310_0041_b200 as gdp
 
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 1
 nz = (int(sys.argv[2]) or None) if len(sys.argv) > 2 else None
-fused = int(sys.argv[3]) if len(sys.argv) > 3 else 1
+fused = int(sys.argv[3]) if len(sys.argv) > 3 else None  # None: the library default
 ctx = gdp.Ctx(0)
 I0 = torch.from_numpy(synth.make_config(cfg, nz=nz)).cuda()
-o = gdp.default_opts(fused=fused)
+o = gdp.default_opts() if fused is None else gdp.default_opts(fused=fused)
 for _ in range(2):
     gdp.gdp_destripe(ctx, I0, opts=o)
 torch.cuda.synchronize()

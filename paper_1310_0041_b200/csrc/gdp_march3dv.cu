@@ -117,7 +117,9 @@ static __device__ __noinline__ float2 rw_pair8(XferAxis tx, XferAxis ty, int gx,
   return make_float2(rw3(wz, rweight(ty, gy), wx), rw3(wz, rweight(ty, gy + 2), wx));
 }
 
-template <int TAIL, bool PROLONG, bool ZC>
+// EV (restriction on levels of even nx and ny): every in-level child has its sibling in the level,
+// so out-of-level cells only feed coarse cells that are never stored -> no per-cell masks
+template <int TAIL, bool PROLONG, bool ZC, bool EV = false>
 __global__ void __launch_bounds__(MT, 1) k_m3v(const __grid_constant__ Sweep P) {
   using SM = Smem<PROLONG>;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -485,10 +487,10 @@ __global__ void __launch_bounds__(MT, 1) k_m3v(const __grid_constant__ Sweep P) 
             const float2 r = sub2(bb, stencil(IC<PP>{}, IC<CC>{}, Xo, Xl, X[KU], CC ? tsv.y : tsv.x,
                                               CC ? tnv.y : tnv.x, zl2, zr2));
             if (TAIL == TAIL_RESTRICT) {
-              const float2 w = rwreg ? f2(rw3(wz, 0.5f, 0.5f)) : rw_pair8(P.tx, P.ty, gx0 + CC, gyw + RR, wz);
+              const float2 w = (EV || rwreg) ? f2(rw3(wz, 0.5f, 0.5f)) : rw_pair8(P.tx, P.ty, gx0 + CC, gyw + RR, wz);
               float2& ac = acc[PP >> 1];
               const float2 n = __ffma2_rn(w, r, ac);
-              if (lane_full && rfull) ac = n;
+              if (EV || (lane_full && rfull)) ac = n;
               else ac = make_float2(cin[CC] && rin[RR] ? n.x : ac.x, cin[CC] && rin[RR + 2] ? n.y : ac.y);
             } else if (TAIL == TAIL_NORMS) {
               const bool mx = pin && cin[CC] && rint[RR] && rin[RR];
@@ -572,10 +574,10 @@ __global__ void __launch_bounds__(MT, 1) k_m3v(const __grid_constant__ Sweep P) 
   if (tid == 0) tma_store_wait_all();
 }
 
-template <int TAIL, bool PRO, bool ZC>
+template <int TAIL, bool PRO, bool ZC, bool EV = false>
 static cudaError_t launch(const Sweep& P, cudaStream_t s) {
   static_assert(sizeof(Smem<PRO>) + 128 + 512 <= 232448, "shared memory");
-  auto kern = k_m3v<TAIL, PRO, ZC>;
+  auto kern = k_m3v<TAIL, PRO, ZC, EV>;
   static bool attr = false;
   const size_t sm = sizeof(Smem<PRO>) + 128;
   if (!attr) {
@@ -667,7 +669,9 @@ int fused_sweep3dv(const Level& L, const Level& C, const float* xin, float* xout
     else if (tail == TAIL_RESTRICT) e = launch<1, true, false>(P, s);
     else e = launch<0, true, false>(P, s);
   } else if (tail == TAIL_RESTRICT) {
-    e = zc ? launch<1, false, true>(P, s) : launch<1, false, false>(P, s);
+    const bool ev = (L.nx & 1) == 0 && (L.ny & 1) == 0;  // C is x/y coarsened (sweep3dv_ok)
+    if (ev) e = zc ? launch<1, false, true, true>(P, s) : launch<1, false, false, true>(P, s);
+    else e = zc ? launch<1, false, true>(P, s) : launch<1, false, false>(P, s);
   } else if (tail == TAIL_NORMS) {
     e = launch<2, false, false>(P, s);
   } else {

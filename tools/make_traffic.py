@@ -20,7 +20,7 @@ for name, v in best.items():
             continue
         classes["up3d@L0" if prolong else "down3d@L0"].append(v)
         continue
-    m = re.search(r"k_m3v<(\d+), (\d+), (\d+)>", name)
+    m = re.search(r"k_m3v<(\d+), (\d+), (\d+)(?:, \d+)?>", name)
     if m:  # vertical-pack z-march: TAIL 1 restricts (down), PROLONG or TAIL 2 (norms) is the up pass
         tail, prolong, zc = int(m.group(1)), int(m.group(2)), int(m.group(3))
         if zc:

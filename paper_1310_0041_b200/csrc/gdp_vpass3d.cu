@@ -33,6 +33,13 @@ static int load_encode() {
   return rc;
 }
 
+// L2 promotion 128 B: the boxes start 16 B before a 224-B tile stride, so 256-B promotion over-fetches
+// the neighbouring tiles' columns, which are not shared in L2 (the persistent CTAs drift apart by more
+// planes than L2 retains): measured DRAM reads of a finest config-1 sweep 1.537 -> 1.474 GB
+// (tools/ab_tma.sh; NONE measures the same as 128 B, an evict_last cache hint changes nothing)
+#ifndef GDP_TMA_PROMO
+#define GDP_TMA_PROMO CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+#endif
 // fp32 volume nx x ny x np planes at p, box bw x bh x 1
 static int make_map(CUtensorMap* m, const float* p, int nx, int ny, long long np, int bw, int bh) {
   cuuint64_t dims[3] = {(cuuint64_t)nx, (cuuint64_t)ny, (cuuint64_t)std::max<long long>(np, 1)};
@@ -41,7 +48,7 @@ static int make_map(CUtensorMap* m, const float* p, int nx, int ny, long long np
   cuuint32_t es[3] = {1, 1, 1};
   const CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(p), dims, strides, box, es,
                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                              GDP_TMA_PROMO, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return set_err(GDP_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
   return GDP_OK;
 }

@@ -116,12 +116,26 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity
 }
 // box at (c0, c1, c2) of a 3D map; c0 * 4 must be a multiple of 16 bytes (measured on the B200:
 // an unaligned innermost coordinate traps with an illegal instruction, tools/tma_probe)
+#ifndef GDP_TMA_HINT
+#define GDP_TMA_HINT 0
+#endif
 __device__ __forceinline__ void tma3(void* dst, const CUtensorMap* m, int c0, int c1, int c2, unsigned long long* bar) {
+#if GDP_TMA_HINT
+  // L2 evict_last: a box's halo columns / rows are the neighbouring tiles' interior a few steps apart
+  unsigned long long pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(pol));
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3, %4}], [%5], %6;\n" ::"r"(
+          sa(dst)),
+      "l"(reinterpret_cast<unsigned long long>(m)), "r"(c0), "r"(c1), "r"(c2), "r"(sa(bar)), "l"(pol)
+      : "memory");
+#else
   asm volatile(
       "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(
           sa(dst)),
       "l"(reinterpret_cast<unsigned long long>(m)), "r"(c0), "r"(c1), "r"(c2), "r"(sa(bar))
       : "memory");
+#endif
 }
 
 // row / plane classes of the diagonal: the link coefficients of a row depend only on these

@@ -36,3 +36,20 @@ def test_reference_arm_other_ranks_silent():
     r = _run({"RANK": "1"})
     assert r.returncode == 0, r.stderr[-2000:]
     assert not [l for l in r.stdout.splitlines() if l.startswith("{")]
+
+
+def test_committed_ncu_summaries_cover_the_bench_classes():
+    """bench.py's roofline.traffic / whole_step.ncu_dram come from committed ncu summaries: the finest-level
+    kernel classes a config-1 or config-2 step can be dominated by must be present, with DRAM traffic at
+    least the unique bytes of one pass (1024 x 1024 x 128 fp32 volume read + written)."""
+    sys.path.insert(0, ROOT)
+    import bench
+    for cls in ("down3d@L0", "up3d@L0", "down2d@L0", "up2d@L0"):
+        tr = bench.ncu_traffic(cls)
+        assert tr is not None and tr["dram_bytes_per_launch"] > 0.5e9, cls
+        src = tr["source"]
+        assert "profiles/" in src
+        cited = src[src.index("profiles/"):].split(")")[0].split()[0]
+        assert os.path.exists(os.path.join(ROOT, cited)), cited  # the summary names a file that is committed
+    st = bench.ncu_step()
+    assert st and st["launches"] > 100 and 1e10 < st["bytes"] < 1e11 and 1000 < st["GBps"] < 8000
